@@ -1,0 +1,174 @@
+"""CPU oracle for the distributed 3D FFT — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2601_12209_b200``) never imports it and shares no code with it.
+
+Thin ctypes wrapper over ``oracle/dfft_oracle.c`` (plain C + OpenMP, fp64).  Every function
+cites the PAPER.md passage it follows in the C source; see also DESIGN.md §3.
+Arrays are numpy, x fastest: a complex box of extents (nx, ny, nz) is ``shape (nz, ny, nx)``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dfft_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_int = ctypes.c_int
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-O2 -fopenmp, no -ffast-math, no SIMD intrinsics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-std=c11", "-fopenmp", "-fPIC", "-shared", _SRC, "-o", _LIB + ".tmp", "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        lib.or_gen_complex_box.argtypes = [_u64, _i64, _i64, _i64, _i64p, _i64p, _int, _dp]
+        lib.or_gen_real_box.argtypes = [_u64, _i64, _i64, _i64, _i64p, _i64p, _int, _dp]
+        lib.or_dft1d_naive.argtypes = [_dp, _i64, _int, _dp]
+        lib.or_fft1d.argtypes = [_dp, _i64, _int]
+        lib.or_fft3d.argtypes = [_dp, _i64, _i64, _i64, _int]
+        lib.or_dft3d_naive.argtypes = [_dp, _i64, _i64, _i64, _int, _dp]
+        lib.or_rfft3d.argtypes = [_dp, _i64, _i64, _i64, _dp]
+        lib.or_irfft3d.argtypes = [_dp, _i64, _i64, _i64, _dp]
+        lib.or_dft3d_bin_seeded.argtypes = [_u64, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64, _dp]
+        lib.or_err_sums.argtypes = [_dp, _dp, _i64, _dp]
+        lib.or_num_threads.restype = _int
+        _lib = lib
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def _i3(v):
+    return (ctypes.c_int64 * 3)(*[int(t) for t in v])
+
+
+def num_threads() -> int:
+    return int(_load().or_num_threads())
+
+
+# ----------------------------------------------------------------- generator
+
+def gen_complex(seed: int, gshape, lo=(0, 0, 0), n=None, f32: bool = False) -> np.ndarray:
+    """Box [lo, lo+n) of the seeded global complex input (x,y,z order), as complex128 (nz,ny,nx)."""
+    gnx, gny, gnz = gshape
+    n = n or (gnx, gny, gnz)
+    out = np.empty((n[2], n[1], n[0]), dtype=np.complex128)
+    _load().or_gen_complex_box(seed, gnx, gny, gnz, _i3(lo), _i3(n), int(f32), _p(out.view(np.float64)))
+    return out
+
+
+def gen_real(seed: int, gshape, lo=(0, 0, 0), n=None, f32: bool = False) -> np.ndarray:
+    gnx, gny, gnz = gshape
+    n = n or (gnx, gny, gnz)
+    out = np.empty((n[2], n[1], n[0]), dtype=np.float64)
+    _load().or_gen_real_box(seed, gnx, gny, gnz, _i3(lo), _i3(n), int(f32), _p(out))
+    return out
+
+
+# ----------------------------------------------------------------- transforms
+
+def dft1d_naive(x: np.ndarray, sign: int = -1) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    X = np.empty_like(x)
+    _load().or_dft1d_naive(_p(x.view(np.float64)), x.size, sign, _p(X.view(np.float64)))
+    return X
+
+
+def fft1d(x: np.ndarray, sign: int = -1) -> np.ndarray:
+    a = np.array(x, dtype=np.complex128, copy=True, order="C")
+    _load().or_fft1d(_p(a.view(np.float64)), a.size, sign)
+    return a
+
+
+def fft3d(a: np.ndarray, sign: int = -1) -> np.ndarray:
+    """Forward (sign -1, unscaled) or inverse (sign +1, ×1/N) 3D FFT of a (nz,ny,nx) array."""
+    a = np.array(a, dtype=np.complex128, copy=True, order="C")
+    nz, ny, nx = a.shape
+    _load().or_fft3d(_p(a.view(np.float64)), nx, ny, nz, sign)
+    return a
+
+
+def fft3d_inplace(a: np.ndarray, sign: int = -1) -> np.ndarray:
+    assert a.dtype == np.complex128 and a.flags.c_contiguous
+    nz, ny, nx = a.shape
+    _load().or_fft3d(_p(a.view(np.float64)), nx, ny, nz, sign)
+    return a
+
+
+def dft3d_naive(a: np.ndarray, sign: int = -1) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    nz, ny, nx = a.shape
+    if a.size > 4096:
+        raise ValueError("dft3d_naive is O(N^2); refusing N > 4096 (16^3)")
+    out = np.empty_like(a)
+    _load().or_dft3d_naive(_p(a.view(np.float64)), nx, ny, nz, sign, _p(out.view(np.float64)))
+    return out
+
+
+def rfft3d(real: np.ndarray) -> np.ndarray:
+    real = np.ascontiguousarray(real, dtype=np.float64)
+    nz, ny, nx = real.shape
+    out = np.empty((nz, ny, nx // 2 + 1), dtype=np.complex128)
+    _load().or_rfft3d(_p(real), nx, ny, nz, _p(out.view(np.float64)))
+    return out
+
+
+def irfft3d(half: np.ndarray, nx: int) -> np.ndarray:
+    half = np.ascontiguousarray(half, dtype=np.complex128)
+    nz, ny, nxc = half.shape
+    assert nxc == nx // 2 + 1 and nx % 2 == 0
+    out = np.empty((nz, ny, nx), dtype=np.float64)
+    _load().or_irfft3d(_p(half.view(np.float64)), nx, ny, nz, _p(out))
+    return out
+
+
+def dft3d_bin_seeded(seed: int, gshape, k, f32: bool = False, real_input: bool = False) -> complex:
+    """X(kx,ky,kz) of the seeded input by the direct O(N) sum (input regenerated on the fly)."""
+    out = np.zeros(2, dtype=np.float64)
+    nx, ny, nz = gshape
+    _load().or_dft3d_bin_seeded(seed, nx, ny, nz, int(f32), int(real_input), int(k[0]), int(k[1]), int(k[2]), _p(out))
+    return complex(out[0], out[1])
+
+
+def err_sums(y: np.ndarray, ref: np.ndarray):
+    """(Σ|y-ref|², Σ|ref|²), Kahan-compensated, over the same-shape arrays."""
+    y = np.ascontiguousarray(y)
+    ref = np.ascontiguousarray(ref)
+    if np.iscomplexobj(y) or np.iscomplexobj(ref):
+        y = y.astype(np.complex128).view(np.float64)
+        ref = ref.astype(np.complex128).view(np.float64)
+    else:
+        y = y.astype(np.float64)
+        ref = ref.astype(np.float64)
+    out = np.zeros(2, dtype=np.float64)
+    _load().or_err_sums(_p(y.reshape(-1)), _p(ref.reshape(-1)), y.size, _p(out))
+    return float(out[0]), float(out[1])
+
+
+def rel_l2(y: np.ndarray, ref: np.ndarray) -> float:
+    e, r = err_sums(y, ref)
+    return (e / r) ** 0.5 if r > 0 else e ** 0.5

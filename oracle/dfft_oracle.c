@@ -1,0 +1,449 @@
+/*
+ * dfft_oracle.c — plain, slow, obviously-correct CPU oracle for the distributed 3D FFT.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2601_12209_b200/, libdfft.so) never links, imports or calls it, and this file
+ * shares no source with the CUDA library (no common headers, tables or helpers).
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, "P:n" = line n):
+ *   - the 3D DFT of P:90-96 (§III-A):
+ *       Â(kx,ky,kz) = Σ_i Σ_j Σ_l A(i,j,l) · exp(-2πi (kx·i/Nx + ky·j/Ny + kz·l/Nz))
+ *     evaluated, as P:97 says, "as a sequence of three independent 1D transforms applied
+ *     along the x, y, and z dimensions" (P:101-105 order: x, then y, then z);
+ *   - the inverse "same sequence applied in reverse order" (§IV-A): z, y, x with the
+ *     conjugate kernel, then ×1/(Nx·Ny·Nz) (reading R1: normalisation);
+ *   - R2C (§V-A/B, "exploiting Hermitian symmetry"): the c2c DFT of (x + 0i),
+ *     keeping kx ∈ [0, Nx/2] (reading R8); C2R: Hermitian extension along x
+ *     (X[Nx-kx, -ky, -kz] = conj X[kx,ky,kz] for 1 ≤ kx < Nx/2), full c2c inverse, real part;
+ *   - brute-force O(N²) DFTs (1D and 3D) used to pin the fast path above;
+ *   - direct O(N) evaluation of single output bins of the definition, regenerating the input
+ *     from the counter-based generator on the fly, for sampled parity at full size.
+ * Everything is fp64 (twiddles from x87 long double cosl/sinl, never recurrences).
+ *
+ * Input generator: value of part p ∈ {0 re, 1 im} at global
+ * linear index g = x + Nx·(y + Ny·z) is U(splitmix64((seed << 32) ^ (2g + p))),
+ * U(u) = (u >> 11)·2^-52 − 1 ∈ [−1, 1), optionally rounded to float (fp32 plans).
+ * The GPU side has its own independent implementation in inputs/; tests check the bits agree.
+ *
+ * Layout convention: a 3D complex array is interleaved (re, im) doubles, x fastest:
+ *   a[2*(x + nx*(y + ny*z)) + {0,1}].
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OR_PI_L 3.141592653589793238462643383279502884L
+
+/* ------------------------------------------------------------------ generator */
+
+static uint64_t or_splitmix64(uint64_t state) {
+    uint64_t z = state + 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+static double or_uniform(uint64_t seed, int64_t g, int part, int round_f32) {
+    uint64_t state = (seed << 32) ^ (uint64_t)(2 * g + part);
+    double v = (double)(or_splitmix64(state) >> 11) * 0x1p-52 - 1.0;
+    if (round_f32) v = (double)(float)v;
+    return v;
+}
+
+/* Fill a complex box [lo, lo+n) of the global (gnx,gny,gnz) grid, interleaved re/im. */
+void or_gen_complex_box(uint64_t seed, int64_t gnx, int64_t gny, int64_t gnz,
+                        const int64_t lo[3], const int64_t n[3], int round_f32, double* out) {
+    (void)gnz;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t z = 0; z < n[2]; ++z)
+        for (int64_t y = 0; y < n[1]; ++y)
+            for (int64_t x = 0; x < n[0]; ++x) {
+                int64_t g = (lo[0] + x) + gnx * ((lo[1] + y) + gny * (lo[2] + z));
+                int64_t l = x + n[0] * (y + n[1] * z);
+                out[2 * l] = or_uniform(seed, g, 0, round_f32);
+                out[2 * l + 1] = or_uniform(seed, g, 1, round_f32);
+            }
+}
+
+/* Real box (R2C input): the re part of the same generator. */
+void or_gen_real_box(uint64_t seed, int64_t gnx, int64_t gny, int64_t gnz,
+                     const int64_t lo[3], const int64_t n[3], int round_f32, double* out) {
+    (void)gnz;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t z = 0; z < n[2]; ++z)
+        for (int64_t y = 0; y < n[1]; ++y)
+            for (int64_t x = 0; x < n[0]; ++x) {
+                int64_t g = (lo[0] + x) + gnx * ((lo[1] + y) + gny * (lo[2] + z));
+                out[x + n[0] * (y + n[1] * z)] = or_uniform(seed, g, 0, round_f32);
+            }
+}
+
+/* ------------------------------------------------------------------ twiddles */
+
+/* w[k] = exp(sign·2πi·k/n), k ∈ [0, n), from long double; sign = -1 forward. */
+static void or_twiddles(int64_t n, int sign, double* w) {
+    for (int64_t k = 0; k < n; ++k) {
+        long double a = 2.0L * OR_PI_L * (long double)k / (long double)n;
+        w[2 * k] = (double)cosl(a);
+        w[2 * k + 1] = (double)(sign * sinl(a));
+    }
+}
+
+/* ------------------------------------------------------------------ 1D brute force */
+
+/* X[k] = Σ_t x[t]·exp(sign·2πi·k·t/n): the definition, O(n²). */
+void or_dft1d_naive(const double* x, int64_t n, int sign, double* X) {
+    double* w = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+    or_twiddles(n, sign, w);
+    for (int64_t k = 0; k < n; ++k) {
+        long double sr = 0, si = 0;
+        for (int64_t t = 0; t < n; ++t) {
+            int64_t m = (k * t) % n;
+            sr += (long double)x[2 * t] * w[2 * m] - (long double)x[2 * t + 1] * w[2 * m + 1];
+            si += (long double)x[2 * t] * w[2 * m + 1] + (long double)x[2 * t + 1] * w[2 * m];
+        }
+        X[2 * k] = (double)sr;
+        X[2 * k + 1] = (double)si;
+    }
+    free(w);
+}
+
+/* ------------------------------------------------------------------ 1D fast FFT */
+
+static int64_t or_smallest_factor(int64_t n) {
+    for (int64_t p = 2; p * p <= n; ++p)
+        if (n % p == 0) return p;
+    return n;
+}
+
+/*
+ * Recursive mixed-radix Cooley-Tukey (decimation in time), out-of-place:
+ *   n = p·m, p = smallest prime factor;
+ *   X[k1 + m·k2] = Σ_{r<p} w_n^{r·k1}·w_p^{r·k2}·Y_r[k1],  Y_r = DFT_m(x[r], x[r+p], ...).
+ * `x` is read with element stride `xs`. `w` is the length-N table exp(sign 2πi k/N) of the
+ * top-level length N, and `ws` = N/n is the step that turns it into the table for n.
+ */
+static void or_fft_rec(const double* x, int64_t xs, int64_t n, double* X,
+                       const double* w, int64_t ws, double* tmp) {
+    if (n == 1) {
+        X[0] = x[0];
+        X[1] = x[1];
+        return;
+    }
+    int64_t p = or_smallest_factor(n);
+    int64_t m = n / p;
+    if (m == 1) { /* prime length: plain DFT with the table */
+        for (int64_t k = 0; k < n; ++k) {
+            double sr = 0, si = 0;
+            for (int64_t t = 0; t < n; ++t) {
+                int64_t e = ((k * t) % n) * ws;
+                double xr = x[2 * t * xs], xi = x[2 * t * xs + 1];
+                sr += xr * w[2 * e] - xi * w[2 * e + 1];
+                si += xr * w[2 * e + 1] + xi * w[2 * e];
+            }
+            X[2 * k] = sr;
+            X[2 * k + 1] = si;
+        }
+        return;
+    }
+    /* sub-transforms Y_r (r < p) of the decimated sequences, stored in X[r·m ...] */
+    for (int64_t r = 0; r < p; ++r)
+        or_fft_rec(x + 2 * r * xs, xs * p, m, X + 2 * r * m, w, ws * p, tmp);
+    /* combine: for each k1 gather Y_r[k1]·w_n^{r·k1}, then a p-point DFT over r */
+    for (int64_t k1 = 0; k1 < m; ++k1) {
+        for (int64_t r = 0; r < p; ++r) {
+            int64_t e = (r * k1) * ws; /* w_n^{r k1} = w_N^{r k1 · N/n} */
+            double yr = X[2 * (r * m + k1)], yi = X[2 * (r * m + k1) + 1];
+            tmp[2 * r] = yr * w[2 * e] - yi * w[2 * e + 1];
+            tmp[2 * r + 1] = yr * w[2 * e + 1] + yi * w[2 * e];
+        }
+        for (int64_t k2 = 0; k2 < p; ++k2) {
+            double sr = 0, si = 0;
+            for (int64_t r = 0; r < p; ++r) {
+                int64_t e = ((r * k2) % p) * (n / p) * ws; /* w_p^{r k2} = w_N^{r k2 · N/p} */
+                sr += tmp[2 * r] * w[2 * e] - tmp[2 * r + 1] * w[2 * e + 1];
+                si += tmp[2 * r] * w[2 * e + 1] + tmp[2 * r + 1] * w[2 * e];
+            }
+            tmp[2 * (p + k2)] = sr;
+            tmp[2 * (p + k2) + 1] = si;
+        }
+        for (int64_t k2 = 0; k2 < p; ++k2) {
+            X[2 * (k1 + m * k2)] = tmp[2 * (p + k2)];
+            X[2 * (k1 + m * k2) + 1] = tmp[2 * (p + k2) + 1];
+        }
+    }
+}
+
+/* Iterative radix-2 DIT for n = 2^m: bit-reversal permutation then m butterfly passes. */
+static void or_fft_radix2(double* a, int64_t n, const double* w) {
+    for (int64_t i = 1, j = 0; i < n; ++i) {
+        int64_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j ^= bit;
+        if (i < j) {
+            double tr = a[2 * i], ti = a[2 * i + 1];
+            a[2 * i] = a[2 * j];
+            a[2 * i + 1] = a[2 * j + 1];
+            a[2 * j] = tr;
+            a[2 * j + 1] = ti;
+        }
+    }
+    for (int64_t len = 2; len <= n; len <<= 1) {
+        int64_t step = n / len;
+        for (int64_t i = 0; i < n; i += len)
+            for (int64_t k = 0; k < len / 2; ++k) {
+                double wr = w[2 * k * step], wi = w[2 * k * step + 1];
+                double* u = a + 2 * (i + k);
+                double* v = a + 2 * (i + k + len / 2);
+                double vr = v[0] * wr - v[1] * wi, vi = v[0] * wi + v[1] * wr;
+                v[0] = u[0] - vr;
+                v[1] = u[1] - vi;
+                u[0] += vr;
+                u[1] += vi;
+            }
+    }
+}
+
+/* In-place 1D FFT of a contiguous interleaved line; sign -1 forward, +1 inverse (no scale). */
+typedef struct {
+    int64_t n;
+    int sign;
+    double* w;   /* 2n */
+    double* buf; /* 2n */
+    double* tmp; /* 4n */
+} or_line_plan;
+
+static void or_line_init(or_line_plan* lp, int64_t n, int sign) {
+    lp->n = n;
+    lp->sign = sign;
+    lp->w = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+    lp->buf = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+    lp->tmp = (double*)malloc(sizeof(double) * 4 * (size_t)n + 64);
+    or_twiddles(n, sign, lp->w);
+}
+
+static void or_line_free(or_line_plan* lp) {
+    free(lp->w);
+    free(lp->buf);
+    free(lp->tmp);
+}
+
+static void or_line_exec(or_line_plan* lp, double* a) {
+    int64_t n = lp->n;
+    if ((n & (n - 1)) == 0) {
+        or_fft_radix2(a, n, lp->w);
+    } else {
+        or_fft_rec(a, 1, n, lp->buf, lp->w, 1, lp->tmp);
+        memcpy(a, lp->buf, sizeof(double) * 2 * (size_t)n);
+    }
+}
+
+void or_fft1d(double* a, int64_t n, int sign) {
+    or_line_plan lp;
+    or_line_init(&lp, n, sign);
+    or_line_exec(&lp, a);
+    or_line_free(&lp);
+}
+
+/* ------------------------------------------------------------------ 3D */
+
+/*
+ * 1D FFTs along one axis of the (nx,ny,nz) array: gather each line (strided for y, z),
+ * transform, scatter back.  axis 0 = x, 1 = y, 2 = z.
+ */
+static void or_axis_pass(double* a, int64_t nx, int64_t ny, int64_t nz, int axis, int sign) {
+    int64_t n = axis == 0 ? nx : axis == 1 ? ny : nz;
+    int64_t stride = axis == 0 ? 1 : axis == 1 ? nx : nx * ny;
+    int64_t nlines = nx * ny * nz / n;
+#pragma omp parallel
+    {
+        or_line_plan lp;
+        or_line_init(&lp, n, sign);
+        double* line = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+#pragma omp for schedule(static)
+        for (int64_t l = 0; l < nlines; ++l) {
+            int64_t base;
+            if (axis == 0) base = l * nx;                            /* l = y + ny z */
+            else if (axis == 1) base = (l % nx) + (l / nx) * nx * ny; /* l = x + nx z */
+            else base = l;                                            /* l = x + nx y */
+            for (int64_t t = 0; t < n; ++t) {
+                line[2 * t] = a[2 * (base + t * stride)];
+                line[2 * t + 1] = a[2 * (base + t * stride) + 1];
+            }
+            or_line_exec(&lp, line);
+            for (int64_t t = 0; t < n; ++t) {
+                a[2 * (base + t * stride)] = line[2 * t];
+                a[2 * (base + t * stride) + 1] = line[2 * t + 1];
+            }
+        }
+        free(line);
+        or_line_free(&lp);
+    }
+}
+
+/* Forward (sign -1): x, y, z.  Inverse (sign +1): z, y, x, ×1/N. */
+void or_fft3d(double* a, int64_t nx, int64_t ny, int64_t nz, int sign) {
+    if (sign < 0) {
+        or_axis_pass(a, nx, ny, nz, 0, -1);
+        or_axis_pass(a, nx, ny, nz, 1, -1);
+        or_axis_pass(a, nx, ny, nz, 2, -1);
+    } else {
+        or_axis_pass(a, nx, ny, nz, 2, +1);
+        or_axis_pass(a, nx, ny, nz, 1, +1);
+        or_axis_pass(a, nx, ny, nz, 0, +1);
+        double s = 1.0 / ((double)nx * (double)ny * (double)nz);
+        int64_t N = nx * ny * nz;
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < 2 * N; ++i) a[i] *= s;
+    }
+}
+
+/* The 3D definition P:91-96 as a triple sum over the input for every output, O(N²). */
+void or_dft3d_naive(const double* a, int64_t nx, int64_t ny, int64_t nz, int sign, double* out) {
+    for (int64_t kz = 0; kz < nz; ++kz)
+        for (int64_t ky = 0; ky < ny; ++ky)
+            for (int64_t kx = 0; kx < nx; ++kx) {
+                long double sr = 0, si = 0;
+                for (int64_t z = 0; z < nz; ++z)
+                    for (int64_t y = 0; y < ny; ++y)
+                        for (int64_t x = 0; x < nx; ++x) {
+                            long double ph = (long double)sign * 2.0L * OR_PI_L *
+                                ((long double)((kx * x) % nx) / nx + (long double)((ky * y) % ny) / ny +
+                                 (long double)((kz * z) % nz) / nz);
+                            long double c = cosl(ph), s = sinl(ph);
+                            const double* v = a + 2 * (x + nx * (y + ny * z));
+                            sr += v[0] * c - v[1] * s;
+                            si += v[0] * s + v[1] * c;
+                        }
+                out[2 * (kx + nx * (ky + ny * kz))] = (double)sr;
+                out[2 * (kx + nx * (ky + ny * kz)) + 1] = (double)si;
+            }
+}
+
+/* R2C: c2c of (x + 0i), keep kx ∈ [0, nx/2] -> out is (nx/2+1, ny, nz) complex. */
+void or_rfft3d(const double* real, int64_t nx, int64_t ny, int64_t nz, double* out) {
+    int64_t N = nx * ny * nz, nxc = nx / 2 + 1;
+    double* a = (double*)malloc(sizeof(double) * 2 * (size_t)N);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < N; ++i) {
+        a[2 * i] = real[i];
+        a[2 * i + 1] = 0.0;
+    }
+    or_fft3d(a, nx, ny, nz, -1);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t z = 0; z < nz; ++z)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t x = 0; x < nxc; ++x) {
+                out[2 * (x + nxc * (y + ny * z))] = a[2 * (x + nx * (y + ny * z))];
+                out[2 * (x + nxc * (y + ny * z)) + 1] = a[2 * (x + nx * (y + ny * z)) + 1];
+            }
+    free(a);
+}
+
+/*
+ * C2R (reading R8): Hermitian-extend the (nx/2+1, ny, nz) half spectrum along x,
+ * X[nx-kx, (ny-ky)%ny, (nz-kz)%nz] = conj X[kx, ky, kz] for 1 <= kx < nx/2, run the full
+ * c2c inverse (×1/N) and keep the real part.  Bins kx = 0 and kx = nx/2 are used as given.
+ */
+void or_irfft3d(const double* half, int64_t nx, int64_t ny, int64_t nz, double* real_out) {
+    int64_t N = nx * ny * nz, nxc = nx / 2 + 1;
+    double* a = (double*)malloc(sizeof(double) * 2 * (size_t)N);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t z = 0; z < nz; ++z)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t x = 0; x < nx; ++x) {
+                double re, im;
+                if (x < nxc) {
+                    re = half[2 * (x + nxc * (y + ny * z))];
+                    im = half[2 * (x + nxc * (y + ny * z)) + 1];
+                } else {
+                    int64_t sx = nx - x, sy = (ny - y) % ny, sz = (nz - z) % nz;
+                    re = half[2 * (sx + nxc * (sy + ny * sz))];
+                    im = -half[2 * (sx + nxc * (sy + ny * sz)) + 1];
+                }
+                a[2 * (x + nx * (y + ny * z))] = re;
+                a[2 * (x + nx * (y + ny * z)) + 1] = im;
+            }
+    or_fft3d(a, nx, ny, nz, +1);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < N; ++i) real_out[i] = a[2 * i];
+    free(a);
+}
+
+/* ------------------------------------------------------------------ sampled bins */
+
+/*
+ * One output bin of the forward definition for the seeded generator input, with
+ * the input regenerated on the fly (no N-sized memory):
+ *   X(kx,ky,kz) = Σ_z w_nz^{kz z} Σ_y w_ny^{ky y} Σ_x w_nx^{kx x} A(x,y,z).
+ * real_input != 0 takes the R2C input (re part, im = 0).  O(N) work per bin.
+ */
+void or_dft3d_bin_seeded(uint64_t seed, int64_t nx, int64_t ny, int64_t nz, int round_f32,
+                         int real_input, int64_t kx, int64_t ky, int64_t kz, double out[2]) {
+    double* wx = (double*)malloc(sizeof(double) * 2 * (size_t)nx);
+    double* wy = (double*)malloc(sizeof(double) * 2 * (size_t)ny);
+    double* wz = (double*)malloc(sizeof(double) * 2 * (size_t)nz);
+    or_twiddles(nx, -1, wx);
+    or_twiddles(ny, -1, wy);
+    or_twiddles(nz, -1, wz);
+    double tr = 0, ti = 0;
+#pragma omp parallel for reduction(+ : tr, ti) schedule(static)
+    for (int64_t z = 0; z < nz; ++z) {
+        double zr = 0, zi = 0;
+        for (int64_t y = 0; y < ny; ++y) {
+            double yr = 0, yi = 0;
+            for (int64_t x = 0; x < nx; ++x) {
+                int64_t g = x + nx * (y + ny * z);
+                double ar = or_uniform(seed, g, 0, round_f32);
+                double ai = real_input ? 0.0 : or_uniform(seed, g, 1, round_f32);
+                int64_t e = (kx * x) % nx;
+                yr += ar * wx[2 * e] - ai * wx[2 * e + 1];
+                yi += ar * wx[2 * e + 1] + ai * wx[2 * e];
+            }
+            int64_t e = (ky * y) % ny;
+            zr += yr * wy[2 * e] - yi * wy[2 * e + 1];
+            zi += yr * wy[2 * e + 1] + yi * wy[2 * e];
+        }
+        int64_t e = (kz * z) % nz;
+        tr += zr * wz[2 * e] - zi * wz[2 * e + 1];
+        ti += zr * wz[2 * e + 1] + zi * wz[2 * e];
+    }
+    out[0] = tr;
+    out[1] = ti;
+    free(wx);
+    free(wy);
+    free(wz);
+}
+
+/* ------------------------------------------------------------------ error metrics */
+
+/* Σ|a-b|² and Σ|b|² over n doubles (complex arrays pass 2n), Kahan-compensated. */
+void or_err_sums(const double* a, const double* b, int64_t n, double out[2]) {
+    double se = 0, ce = 0, sr = 0, cr = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double d = a[i] - b[i];
+        double y = d * d - ce;
+        double t = se + y;
+        ce = (t - se) - y;
+        se = t;
+        y = b[i] * b[i] - cr;
+        t = sr + y;
+        cr = (t - sr) - y;
+        sr = t;
+    }
+    out[0] = se;
+    out[1] = sr;
+}
+
+int or_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

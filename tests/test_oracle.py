@@ -1,0 +1,223 @@
+"""Pins for the CPU oracle (``oracle/``) — things other than the oracle itself fix its values.
+
+PAPER.md prints no worked numeric example, so the pins are: closed forms
+(tests/golden/), brute-force O(N^2) sums on tiny inputs, an independent library (numpy's
+pocketfft), and invariants (Parseval, round trip, linearity, Hermitian symmetry).  Each is
+chosen so that a plausible oracle bug (dropped term, wrong sign, transposed axis, wrong
+twiddle index, missing 1/N) fails at least one of them.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import inputs
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _parse_vec(s):
+    out = []
+    for pair in s.split(";"):
+        re, im = pair.split(",")
+        out.append(complex(float(re), float(im)))
+    return np.array(out)
+
+
+def _golden_1d():
+    rows = []
+    with open(os.path.join(GOLDEN, "closed_forms_1d.txt")) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            name, x, X = [t.strip() for t in line.split("|")]
+            rows.append((name, _parse_vec(x), _parse_vec(X)))
+    return rows
+
+
+# --------------------------------------------------------------------- generator
+
+def test_splitmix64_known_value():
+    # splitmix64 (Steele, Lea, Flood 2014) seeded with 0 emits 0xE220A8397B1DCDAF first;
+    # our mixer applied to state 0 is exactly that first output.
+    z = inputs._splitmix64(np.array([0], dtype=np.uint64))[0]
+    assert int(z) == 0xE220A8397B1DCDAF
+
+
+def test_generator_oracle_matches_numpy_bits(oracle_mod):
+    g = (12, 10, 6)
+    lo, n = (3, 2, 1), (7, 5, 4)
+    for f32 in (False, True):
+        a = oracle_mod.gen_complex(77, g, lo, n, f32=f32)
+        b = inputs.gen_complex_np(77, g, lo, n, f32=f32).astype(np.complex128)
+        assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+        r1 = oracle_mod.gen_real(77, g, lo, n, f32=f32)
+        r2 = inputs.gen_real_np(77, g, lo, n, f32=f32).astype(np.float64)
+        assert np.array_equal(r1, r2)
+    a = oracle_mod.gen_complex(5, (64, 64, 64))
+    assert a.real.min() >= -1 and a.real.max() < 1
+    assert abs(a.real.mean()) < 0.01 and abs(a.imag.var() - 1 / 3) < 0.01
+
+
+# --------------------------------------------------------------------- 1D
+
+@pytest.mark.parametrize("row", _golden_1d(), ids=lambda r: r[0])
+def test_1d_closed_forms(oracle_mod, row):
+    _, x, X = row
+    np.testing.assert_allclose(oracle_mod.dft1d_naive(x), X, atol=1e-14)
+    np.testing.assert_allclose(oracle_mod.fft1d(x), X, atol=1e-14)
+    # inverse kernel (sign +1, unscaled) maps X back to n*x
+    np.testing.assert_allclose(oracle_mod.fft1d(X, +1), len(x) * x, atol=1e-13)
+
+
+LENGTHS = list(range(1, 33)) + [48, 64, 96, 97, 128, 192, 256, 384, 512, 768, 1024]
+
+
+@pytest.mark.parametrize("n", LENGTHS)
+def test_1d_fast_vs_bruteforce_and_numpy(oracle_mod, n):
+    rng = np.random.default_rng(n)
+    x = rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)
+    naive = oracle_mod.dft1d_naive(x)
+    fast = oracle_mod.fft1d(x)
+    ref = np.fft.fft(x)  # independent library (pocketfft)
+    scale = np.sqrt(n)
+    assert np.abs(naive - ref).max() < 1e-13 * scale * max(1, np.log2(n))
+    assert np.abs(fast - naive).max() < 1e-13 * scale * max(1, np.log2(n))
+    inv = oracle_mod.fft1d(fast, +1) / n
+    assert np.abs(inv - x).max() < 1e-14 * max(1, np.log2(n))
+
+
+@pytest.mark.parametrize("n", [5, 16, 24, 1024])
+def test_1d_plane_wave_every_bin(oracle_mod, n):
+    # exp(+2 pi i m t / n) -> n at k = m, 0 elsewhere: a misplaced bin is an O(1) error
+    t = np.arange(n)
+    for m in sorted({0, 1, n // 3, n - 1}):
+        x = np.exp(2j * np.pi * ((m * t) % n) / n)  # exact phase reduction
+        X = oracle_mod.fft1d(x)
+        e = np.zeros(n, complex)
+        e[m] = n
+        assert np.abs(X - e).max() < 1e-11
+
+
+# --------------------------------------------------------------------- 3D vs brute force
+
+@pytest.mark.parametrize("shape", [(2, 2, 2), (4, 4, 4), (8, 8, 8), (16, 8, 4), (4, 6, 12), (8, 5, 3), (7, 3, 2)])
+def test_3d_fast_vs_triple_sum(oracle_mod, shape):
+    nx, ny, nz = shape
+    a = oracle_mod.gen_complex(11, shape)
+    naive = oracle_mod.dft3d_naive(a)
+    fast = oracle_mod.fft3d(a, -1)
+    assert oracle_mod.rel_l2(fast, naive) < 1e-14
+    inv_naive = oracle_mod.dft3d_naive(naive, +1) / a.size
+    inv_fast = oracle_mod.fft3d(fast, +1)
+    assert oracle_mod.rel_l2(inv_fast, inv_naive) < 1e-14
+    assert oracle_mod.rel_l2(inv_fast, a) < 1e-14
+
+
+def test_3d_axis_order_non_cubic(oracle_mod):
+    # a transposed-axis bug passes on cubes; a plane wave with distinct (mx,my,mz) on a
+    # non-cubic grid lands on exactly one bin
+    nx, ny, nz = 12, 8, 6
+    mx, my, mz = 5, 3, 1
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    a = np.exp(2j * np.pi * ((mx * x) % nx / nx + (my * y) % ny / ny + (mz * z) % nz / nz))
+    X = oracle_mod.fft3d(a, -1)
+    e = np.zeros_like(X)
+    e[mz, my, mx] = a.size
+    assert np.abs(X - e).max() < 1e-10
+
+
+# --------------------------------------------------------------------- closed forms at config sizes
+
+@pytest.mark.parametrize("shape", [(64, 64, 64), (96, 64, 48)])
+def test_3d_closed_forms(oracle_mod, shape):
+    nx, ny, nz = shape
+    N = nx * ny * nz
+    # delta at origin -> all ones
+    a = np.zeros((nz, ny, nx), complex)
+    a[0, 0, 0] = 1
+    assert np.abs(oracle_mod.fft3d(a) - 1).max() < 1e-13
+    # delta at (ax, ay, az) -> pure phase exp(-2 pi i (kx ax/nx + ky ay/ny + kz az/nz))
+    ax, ay, az = 3, 5, 7
+    a = np.zeros((nz, ny, nx), complex)
+    a[az, ay, ax] = 1
+    kz, ky, kx = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    ph = np.exp(-2j * np.pi * ((kx * ax) % nx / nx + (ky * ay) % ny / ny + (kz * az) % nz / nz))
+    assert np.abs(oracle_mod.fft3d(a) - ph).max() < 1e-12
+    # constant c -> c*N at DC only
+    c = 0.25 - 0.5j
+    X = oracle_mod.fft3d(np.full((nz, ny, nx), c))
+    assert abs(X[0, 0, 0] - c * N) < 1e-9
+    X[0, 0, 0] = 0
+    assert np.abs(X).max() < 1e-9
+    # inverse of all-ones -> delta (the 1/N is applied)
+    d = oracle_mod.fft3d(np.ones((nz, ny, nx), complex), +1)
+    e = np.zeros_like(d)
+    e[0, 0, 0] = 1
+    assert np.abs(d - e).max() < 1e-14
+
+
+def test_3d_invariants_and_numpy(oracle_mod):
+    shape = (64, 32, 48)
+    a = oracle_mod.gen_complex(3, shape)
+    b = oracle_mod.gen_complex(4, shape)
+    A = oracle_mod.fft3d(a)
+    B = oracle_mod.fft3d(b)
+    N = a.size
+    # Parseval: sum |X|^2 = N sum |x|^2
+    assert abs(np.vdot(A, A).real / (N * np.vdot(a, a).real) - 1) < 1e-13
+    # linearity
+    alpha, beta = 0.7 - 0.2j, -1.3 + 0.4j
+    assert oracle_mod.rel_l2(oracle_mod.fft3d(alpha * a + beta * b), alpha * A + beta * B) < 1e-14
+    # round trip
+    assert oracle_mod.rel_l2(oracle_mod.fft3d(A, +1), a) < 1e-15
+    # independent library: numpy axes (z, y, x) == our (nz, ny, nx) storage
+    assert oracle_mod.rel_l2(A, np.fft.fftn(a)) < 1e-14
+    assert oracle_mod.rel_l2(oracle_mod.fft3d(a, +1), np.fft.ifftn(a)) < 1e-14
+
+
+# --------------------------------------------------------------------- R2C / C2R
+
+def test_r2c_relations(oracle_mod):
+    nx, ny, nz = 12, 8, 6
+    r = oracle_mod.gen_real(9, (nx, ny, nz))
+    H = oracle_mod.rfft3d(r)
+    assert H.shape == (nz, ny, nx // 2 + 1)
+    full = oracle_mod.fft3d(r.astype(complex))
+    assert oracle_mod.rel_l2(H, full[:, :, : nx // 2 + 1]) < 1e-15
+    # Hermitian symmetry of the spectrum of a real input
+    sym = np.conj(full[(-np.arange(nz)) % nz][:, (-np.arange(ny)) % ny][:, :, (-np.arange(nx)) % nx])
+    assert oracle_mod.rel_l2(full, sym) < 1e-14
+    assert oracle_mod.rel_l2(H, np.fft.rfftn(r)) < 1e-14
+    assert oracle_mod.rel_l2(oracle_mod.irfft3d(H, nx), r) < 1e-15
+
+
+def test_c2r_arbitrary_input_matches_numpy(oracle_mod):
+    # reading R8: C2R on arbitrary (non-Hermitian) input = numpy irfftn convention
+    nx, ny, nz = 10, 8, 6
+    rng = np.random.default_rng(0)
+    h = rng.standard_normal((nz, ny, nx // 2 + 1)) + 1j * rng.standard_normal((nz, ny, nx // 2 + 1))
+    ref = np.fft.irfftn(h, s=(nz, ny, nx), axes=(0, 1, 2))
+    assert np.abs(oracle_mod.irfft3d(h, nx) - ref).max() < 1e-15
+
+
+# --------------------------------------------------------------------- sampled bins
+
+def test_sampled_bins_match_full_transform(oracle_mod):
+    for shape, real in (((16, 12, 8), False), ((64, 64, 64), False), ((24, 16, 12), True)):
+        a = oracle_mod.gen_real(21, shape) if real else oracle_mod.gen_complex(21, shape)
+        X = oracle_mod.rfft3d(a) if real else oracle_mod.fft3d(a)
+        rng = np.random.default_rng(1)
+        for _ in range(6):
+            kx = int(rng.integers(0, X.shape[2]))
+            ky, kz = int(rng.integers(0, shape[1])), int(rng.integers(0, shape[2]))
+            v = oracle_mod.dft3d_bin_seeded(21, shape, (kx, ky, kz), real_input=real)
+            assert abs(v - X[kz, ky, kx]) < 1e-10 * np.sqrt(a.size)
+
+
+def test_err_sums(oracle_mod):
+    y = np.array([1 + 1j, 2, 3j])
+    ref = np.array([1, 2 + 1j, 3j])
+    e, r = oracle_mod.err_sums(y, ref)
+    assert e == pytest.approx(2.0) and r == pytest.approx(1 + 5 + 9)
