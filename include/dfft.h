@@ -1,0 +1,165 @@
+/*
+ * dfft.h — C ABI of libdfft.so, the B200-native distributed 3D FFT (DaggerFFT's hot path).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n (arXiv 2601.12209), with its section.
+ * No C++ or torch types cross this boundary: plain pointers (device or host, as stated),
+ * int64 sizes, enums.  All functions return a dfft_status_t; none aborts or throws.  On
+ * failure dfft_last_error() returns a thread-local human-readable detail.
+ *
+ * The operation (§III-A): the unnormalised forward 3D DFT
+ *     X(kx,ky,kz) = Σ_x Σ_y Σ_z A(x,y,z) · exp(-2πi (kx x/Nx + ky y/Ny + kz z/Nz))
+ * evaluated as three stages of batched 1D FFTs along x, y, z, each on its own
+ * stage-owned decomposition D1/D2/D3 (Alg. 1), with a pack → exchange →
+ * unpack redistribution between stages.  The inverse applies the same sequence
+ * mirrored, z then y then x (§IV-A), with the conjugate kernel and a 1/(Nx·Ny·Nz)
+ * scale (reading R1).  R2C/C2R halve the x axis: Nx/2+1 bins.
+ *
+ * Decompositions (readings R4-R6), rank r = i·P2 + j (row-major process grid):
+ *   PENCIL P1×P2:  D1 = x whole, y split by i over P1, z split by j over P2   (input, forward)
+ *                  D2 = x split by i, y whole, z split by j                    (internal)
+ *                  D3 = x split by i, y split by j, z whole                    (output, forward)
+ *   SLAB (p1 = P, p2 = 1):  D1 = z-slabs (x, y whole), D3 = y-slabs (x, z whole): "the first
+ *                  two transforms are performed locally on each slab before a single global
+ *                  transpose".  Internally identical to PENCIL with grid 1×P.
+ *   Splits are balanced blocks: part q of n over p has n/p + (q < n%p) elements, lowest
+ *   indices first.  For R2C the split x extent is Nx/2+1.
+ *   Every user-visible box is stored dense, x fastest: element (x,y,z) of a box with origin lo
+ *   and extents n is at ((z-lo_z)·n_y + (y-lo_y))·n_x + (x-lo_x).  Complex = interleaved
+ *   (re, im) = torch.complex64 / complex128.
+ */
+#ifndef DFFT_H_
+#define DFFT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFFT_VERSION 100 /* 1.0.0 */
+
+typedef struct dfft_comm_s* dfft_comm_t;
+typedef struct dfft_plan_s* dfft_plan_t;
+
+typedef enum {
+  DFFT_SUCCESS = 0,
+  DFFT_ERR_INVALID_VALUE = 1,     /* bad argument: sizes <= 0, p1*p2 != nranks, null/misaligned ptr, in == out */
+  DFFT_ERR_INFEASIBLE_DECOMP = 2, /* some rank would own an empty block in some layout */
+  DFFT_ERR_UNSUPPORTED = 3,       /* axis length with a prime factor outside {2,3,5,7}, > 4096, odd Nx for R2C */
+  DFFT_ERR_ALLOC = 4,             /* cudaMalloc failed */
+  DFFT_ERR_CUDA = 5,              /* a CUDA runtime call failed (detail in dfft_last_error) */
+  DFFT_ERR_NCCL = 6,              /* an NCCL call failed or the communicator reported an async error */
+  DFFT_ERR_INTERNAL = 7
+} dfft_status_t;
+
+typedef enum { DFFT_SLAB = 1, DFFT_PENCIL = 2 } dfft_decomp_t;
+
+/* Transform type and precision.  R2C with direction INVERSE is the C2R transform. */
+typedef enum { DFFT_C2C_F32 = 1, DFFT_C2C_F64 = 2, DFFT_R2C_F32 = 3, DFFT_R2C_F64 = 4 } dfft_type_t;
+
+/* Sign of the exponent: FORWARD = -1, INVERSE = +1 with the 1/N scale. */
+typedef enum { DFFT_FORWARD = -1, DFFT_INVERSE = 1 } dfft_direction_t;
+
+/*
+ * flags (bit field, 0 = defaults):
+ *   bits 0-7  DFFT_FLAG_CHUNKS(k): pipeline chunk count K (0 = automatic).  The stage-1/2
+ *             work and both exchanges are split into K chunks along the axis no exchange
+ *             touches (z forward, x inverse) and run as a two-stream pipeline (P:115-126,
+ *             Fig. 1 "progressive per-chunk pipelining"; Alg. 2 phases 3/5).
+ *   DFFT_FLAG_NO_OVERLAP: one stream, each exchange completes before the next stage starts
+ *             (the "SimpleMPIFFT" static-barrier ablation of P:438).  Results are bitwise
+ *             identical to the pipelined schedule.
+ */
+#define DFFT_FLAG_CHUNKS(k) ((uint64_t)((k) & 0xff))
+#define DFFT_FLAG_NO_OVERLAP ((uint64_t)1 << 8)
+
+int dfft_version(void);
+const char* dfft_status_string(dfft_status_t status);
+/* Thread-local detail of the last failure on this thread ("" if none).  Valid until the next call. */
+const char* dfft_last_error(void);
+
+/* ------------------------------------------------------------------ communicators
+ * One process per GPU.  Rank 0 calls dfft_get_unique_id and the caller broadcasts the
+ * 128 bytes (e.g. over a torch.distributed process group); every rank then calls
+ * dfft_comm_init collectively.  nranks == 1 needs no id (pass NULL) and creates no NCCL
+ * communicator.  The comm must outlive its plans.
+ */
+dfft_status_t dfft_get_unique_id(unsigned char id[128]);
+dfft_status_t dfft_comm_init(dfft_comm_t* comm, int nranks, int rank, const unsigned char id[128],
+                             int cuda_device);
+/*
+ * Simulated communicator (test/diagnostic): all `nranks` ranks live in this process on one
+ * GPU.  Plans created on it hold every rank's buffers; dfft_execute_sim runs every rank's
+ * stage kernels and performs the exchange with device-to-device copies of exactly the
+ * blocks NCCL would move.  Used to validate P = 8 layouts when fewer GPUs are available.
+ */
+dfft_status_t dfft_comm_init_sim(dfft_comm_t* comm, int nranks, int cuda_device);
+dfft_status_t dfft_comm_destroy(dfft_comm_t comm);
+
+/* ------------------------------------------------------------------ plans
+ * Collective over comm (every rank calls it with the same arguments).  Builds the stage
+ * geometry, twiddle tables, per-stage address tables, work buffers, sub-communicators
+ * (row = ranks with the same j, column = same i), streams and events once; execution
+ * reuses them ("plan creation is performed only once per distinct transform
+ * configuration", §V-B; "persistent workspaces and buffer reuse").
+ * proc grid: PENCIL takes p1 × p2; SLAB requires p2 == 1 and p1 == nranks.
+ */
+dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, int64_t ny, int64_t nz,
+                               dfft_decomp_t decomp, int p1, int p2, dfft_type_t type,
+                               dfft_direction_t direction, uint64_t flags);
+
+/* This rank's input (which = 0) or output (which = 1) box, x,y,z order.  For a simulated
+ * comm use dfft_plan_box_rank. */
+dfft_status_t dfft_plan_box(dfft_plan_t plan, int which, int64_t lo[3], int64_t n[3]);
+dfft_status_t dfft_plan_box_rank(dfft_plan_t plan, int rank, int which, int64_t lo[3], int64_t n[3]);
+
+/* Bytes of this rank's input box, output box, and plan-owned device workspace. */
+dfft_status_t dfft_plan_bytes(dfft_plan_t plan, size_t* in_bytes, size_t* out_bytes, size_t* workspace_bytes);
+
+/* Pure geometry (no GPU needed): the input (which = 0) or output (which = 1) box of `rank`
+ * for these plan arguments, with the same validation as dfft_plan_create. */
+dfft_status_t dfft_decomp_box(int64_t nx, int64_t ny, int64_t nz, dfft_decomp_t decomp, int p1, int p2,
+                              dfft_type_t type, dfft_direction_t direction, int rank, int which, int64_t lo[3],
+                              int64_t n[3]);
+
+/* Chunk count K actually used. */
+dfft_status_t dfft_plan_chunks(dfft_plan_t plan, int* chunks);
+
+/*
+ * Execute on device buffers.  `in` is this rank's input box (forward: D1; inverse: D3),
+ * `out` its output box (forward: D3; inverse: D1), both device pointers on the plan's
+ * GPU, 16-byte aligned, dense as described above, non-overlapping; `in` is never written.
+ * Stream-ordered and asynchronous: work is enqueued after everything already on `stream`
+ * and `stream` waits for its completion; no host synchronisation; capturable in a CUDA
+ * graph.  Collective: all ranks execute matching plans in the same order.
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ */
+dfft_status_t dfft_execute(dfft_plan_t plan, const void* in, void* out, void* stream);
+
+/*
+ * Same, with host pointers (pageable or pinned): copies `in` to a plan-owned device staging
+ * buffer, executes, copies the result back to `out`, and synchronises `stream` before
+ * returning.  This is the end-to-end entry point (host → device → host).
+ */
+dfft_status_t dfft_execute_host(dfft_plan_t plan, const void* in_host, void* out_host, void* stream);
+
+/* Simulated comm only: ins[r] / outs[r] are rank r's device boxes, r < nranks. */
+dfft_status_t dfft_execute_sim(dfft_plan_t plan, const void* const* ins, void* const* outs, void* stream);
+
+/* Synchronises the plan's internal streams, then frees everything the plan owns. */
+dfft_status_t dfft_destroy(dfft_plan_t plan);
+
+/* ------------------------------------------------------------------ diagnostics
+ * Batched 1D transform of `howmany` contiguous lines of length n (device pointers), in the
+ * same kernels the 3D path uses (stage-1 contiguous kernel, c2c only).  Used by parity tests
+ * of the per-length radix schedules.  sign = -1 forward, +1 inverse (unscaled).
+ */
+dfft_status_t dfft_fft1d(const void* in, void* out, int64_t n, int64_t howmany, int f64, int sign,
+                         void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DFFT_H_ */

@@ -1,0 +1,441 @@
+// fft_kernels.cuh — sm_100a batched 1D FFT kernels of the distributed 3D FFT.
+//
+// Each stage of the paper's pipeline is "independent 1D FFTs" along one axis (P:101-105,
+// §III-A; Alg. 1 stages 1-3).  Two kernel families compute a batch of length-N
+// lines with a mixed-radix Stockham autosort FFT (radix 16/8/4/2 first, then 3/5/7):
+//   * contig  — the FFT axis is unit stride on the read side (stage-1 x lines, and the
+//               inverse's last x stage).  LPC lines per CTA, T threads per line.
+//   * strided — the FFT axis is strided; W adjacent unit-stride columns per CTA so every
+//               row access is a 64-128 B coalesced segment (stages 2-3, y and z).
+// Pass p (radix R, Ns = product of earlier radices) maps butterfly b < N/R:
+//     v[r] = X[b + r·N/R] · w_{Ns·R}^{(b mod Ns)·r},  V = DFT_R(v),
+//     Y[(b/Ns)·Ns·R + (b mod Ns) + r·Ns] = V[r]
+// so the first pass reads and the last pass writes consecutive addresses across threads
+// (coalesced straight from/to HBM, no staging pass); the passes in between exchange through
+// padded shared memory (conflict-free layouts chosen with tools/bank_sim.py).  Twiddles
+// come from per-pass tables in HBM (long-double generated, [r-1][m] layout so a warp's
+// loads coalesce), never from recurrences.
+//
+// The pack / unpack of the redistribution (Alg. 2 phases 3-5) is fused into
+// the global side of the first and last pass through a SideMap: element t of line
+// (l0, l1) lives at  base + toff(t) + Lidx·lstr(t) + c0  where (toff, lstr) come either
+// from a closed form (unsegmented side) or from a per-t table (segmented side: t ranges
+// owned by different peers land in different send blocks / buffers).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dfft {
+
+// --------------------------------------------------------------------------------- types
+template <typename Real> struct CT;
+template <> struct CT<float> { using type = float2; };
+template <> struct CT<double> { using type = double2; };
+
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return {a.x + b.x, a.y + b.y}; }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { return {a.x - b.x, a.y - b.y}; }
+template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+// a · (DIR·i):  forward (DIR=-1) multiplies by -i, inverse by +i
+template <int DIR, typename C> __device__ __forceinline__ C mul_i(C a) {
+  if (DIR < 0) return {a.y, -a.x};
+  return {-a.y, a.x};
+}
+
+// --------------------------------------------------------------------------------- schedule
+constexpr int kMaxPass = 8;
+struct Sched {
+  int n, npass, T;
+  int rad[kMaxPass];
+};
+// radix-16 passes first, then the 2^k remainder, then 3, 5, 7.
+constexpr Sched make_sched(int n) {
+  Sched s{n, 0, 1, {0, 0, 0, 0, 0, 0, 0, 0}};
+  int m = n, odd[kMaxPass] = {0, 0, 0, 0, 0, 0, 0, 0}, nodd = 0;
+  for (int p = 7; p >= 3; p -= 2)
+    while (m % p == 0) { odd[nodd++] = p; m /= p; }
+  while (m % 16 == 0) { s.rad[s.npass++] = 16; m /= 16; }
+  if (m > 1) s.rad[s.npass++] = m;  // 2, 4 or 8
+  for (int q = nodd - 1; q >= 0; --q) s.rad[s.npass++] = odd[q];
+  int rmax = 1;
+  for (int p = 0; p < s.npass; ++p) rmax = s.rad[p] > rmax ? s.rad[p] : rmax;
+  s.T = n / rmax;
+  return s;
+}
+constexpr int sched_ns(const Sched& s, int p) {
+  int ns = 1;
+  for (int q = 0; q < p; ++q) ns *= s.rad[q];
+  return ns;
+}
+// offset (in complex elements) of pass p's twiddle table: Σ_{1<=q<p} (R_q - 1)·Ns_q
+constexpr int sched_twoff(const Sched& s, int p) {
+  int off = 0;
+  for (int q = 1; q < p; ++q) off += (s.rad[q] - 1) * sched_ns(s, q);
+  return off;
+}
+constexpr int sched_twlen(const Sched& s) { return sched_twoff(s, s.npass); }
+
+// --------------------------------------------------------------------------------- butterflies
+// exp(-2πi m/16) constants: cos and sin of 2πm/16 for m = 0..3 (the rest by symmetry)
+#define DFFT_C16_1 0.92387953251128675613
+#define DFFT_S16_1 0.38268343236508977173
+#define DFFT_SQH 0.70710678118654752440
+
+// a · w_R^m with w_R = exp(DIR·2πi/R), R ∈ {2,4,8,16}; m is a compile-time constant after
+// unrolling, so every branch folds.
+template <int DIR, int R, typename C>
+__device__ __forceinline__ C twc(C a, int m) {
+  using Real = decltype(a.x);
+  int q = (m * (16 / R)) & 15;  // index in 16ths of a turn
+  if (q == 0) return a;
+  if (q == 8) return {-a.x, -a.y};
+  if (q == 4) return mul_i<DIR>(a);
+  if (q == 12) return mul_i<-DIR>(a);
+  // cos/sin of 2πq/16 for the remaining q
+  Real c, s;
+  int q4 = q & 3;
+  Real cb = q4 == 1 ? (Real)DFFT_C16_1 : q4 == 2 ? (Real)DFFT_SQH : (Real)DFFT_S16_1;
+  Real sb = q4 == 1 ? (Real)DFFT_S16_1 : q4 == 2 ? (Real)DFFT_SQH : (Real)DFFT_C16_1;
+  if (q < 4) { c = cb; s = sb; }
+  else if (q < 8) { c = -sb; s = cb; }
+  else if (q < 12) { c = -cb; s = -sb; }
+  else { c = sb; s = -cb; }
+  // w = c + DIR·i·s
+  Real ws = DIR < 0 ? -s : s;
+  return {a.x * c - a.y * ws, a.x * ws + a.y * c};
+}
+
+template <int DIR, typename C> __device__ __forceinline__ void dft2(C& a, C& b) {
+  C t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+
+template <int DIR, typename C> __device__ __forceinline__ void dft4(C& a0, C& a1, C& a2, C& a3) {
+  C t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = mul_i<DIR>(csub(a1, a3));
+  a0 = cadd(t0, t2);
+  a2 = csub(t0, t2);
+  a1 = cadd(t1, t3);
+  a3 = csub(t1, t3);
+}
+
+// odd prime radix by the symmetric-pair form:
+//   X_k = a0 + Σ_m cos θ (a_m + a_{R-m}) + DIR·i Σ_m sin θ (a_m - a_{R-m}),  θ = 2π m k / R
+// cos(2πq/R) and sin(2πq/R) for R ∈ {3,5,7}, q ∈ [0, R)
+__host__ __device__ constexpr double odd_cos(int R, int q) {
+  return q == 0 ? 1.0
+       : R == 3 ? -0.5
+       : R == 5 ? ((q == 1 || q == 4) ? 0.30901699437494742410 : -0.80901699437494742410)
+       : ((q == 1 || q == 6) ? 0.62348980185873353053
+          : (q == 2 || q == 5) ? -0.22252093395631440429 : -0.90096886790241912624);
+}
+__host__ __device__ constexpr double odd_sin(int R, int q) {
+  return q == 0 ? 0.0
+       : (2 * q > R ? -1.0 : 1.0) *
+         (R == 3 ? 0.86602540378443864676
+          : R == 5 ? ((q == 1 || q == 4) ? 0.95105651629515357212 : 0.58778525229247312917)
+          : ((q == 1 || q == 6) ? 0.78183148246802980871
+             : (q == 2 || q == 5) ? 0.97492791218182360702 : 0.43388373911755812048));
+}
+
+template <int DIR, int R, typename C> __device__ __forceinline__ void dft_odd(C* v) {
+  using Real = decltype(v[0].x);
+  constexpr int H = (R - 1) / 2;
+  C sp[H + 1], sm[H + 1];
+#pragma unroll
+  for (int m = 1; m <= H; ++m) {
+    sp[m] = cadd(v[m], v[R - m]);
+    sm[m] = csub(v[m], v[R - m]);
+  }
+  C x0 = v[0];
+  C sum = x0;
+#pragma unroll
+  for (int m = 1; m <= H; ++m) sum = cadd(sum, sp[m]);
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    C re = x0, im = {0, 0};
+#pragma unroll
+    for (int m = 1; m <= H; ++m) {
+      const Real c = (Real)odd_cos(R, (m * k) % R), s = (Real)odd_sin(R, (m * k) % R);
+      re.x += c * sp[m].x;
+      re.y += c * sp[m].y;
+      im.x += s * sm[m].x;
+      im.y += s * sm[m].y;
+    }
+    // DIR·i·im
+    C t = mul_i<DIR>(im);
+    v[k] = cadd(re, t);
+    v[R - k] = csub(re, t);
+  }
+  v[0] = sum;
+}
+
+// DFT_R in registers, in place, natural order in and out.
+template <int DIR, int R, typename C> __device__ __forceinline__ void dft(C* v) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
+    dft2<DIR>(v[0], v[1]);
+  } else if constexpr (R == 4) {
+    dft4<DIR>(v[0], v[1], v[2], v[3]);
+  } else if constexpr (R == 8) {
+    // 8 = 2 (A) × 4 (B): n = 4 n1 + n2, k = k1 + 2 k2
+    dft2<DIR>(v[0], v[4]);
+    dft2<DIR>(v[1], v[5]);
+    dft2<DIR>(v[2], v[6]);
+    dft2<DIR>(v[3], v[7]);
+    // Y[n2][k1] at v[n2 + 4 k1]; twiddle w8^{n2 k1}
+    v[5] = twc<DIR, 8>(v[5], 1);
+    v[6] = twc<DIR, 8>(v[6], 2);
+    v[7] = twc<DIR, 8>(v[7], 3);
+    dft4<DIR>(v[0], v[1], v[2], v[3]);  // k1 = 0 -> X[0,2,4,6]
+    dft4<DIR>(v[4], v[5], v[6], v[7]);  // k1 = 1 -> X[1,3,5,7]
+    C t[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t[i] = v[i];
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      v[2 * k2] = t[k2];
+      v[2 * k2 + 1] = t[4 + k2];
+    }
+  } else if constexpr (R == 16) {
+    // 16 = 4 (A) × 4 (B): n = 4 n1 + n2, k = k1 + 4 k2
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4<DIR>(v[n2], v[n2 + 4], v[n2 + 8], v[n2 + 12]);
+    // now v[n2 + 4 k1] = Y[n2][k1]; twiddle w16^{n2 k1}
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2)
+#pragma unroll
+      for (int k1 = 1; k1 < 4; ++k1) v[n2 + 4 * k1] = twc<DIR, 16>(v[n2 + 4 * k1], n2 * k1);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4<DIR>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+    // v[4 k1 + k2] = X[k1 + 4 k2]: transpose 4x4
+    C t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = v[i];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+  } else {
+    static_assert(R == 3 || R == 5 || R == 7, "unsupported radix");
+    dft_odd<DIR, R>(v);
+  }
+}
+
+// --------------------------------------------------------------------------------- side maps
+// Where element t of a line lives on the global side of a pass (input of the first pass or
+// output of the last pass).  Unsegmented: toff = t·tstride, lstr = lstride.  Segmented: a
+// per-t table {toff, lstr} built at plan time (send-block routing = the fused pack/unpack).
+struct SideMap {
+  void* base;             // unsegmented: the side's pointer; segmented: base of entries with sel 0
+  void* base1;            // segmented: base of entries with sel 1 (e.g. the user's output buffer)
+  const longlong2* ttab;  // nullptr => unsegmented; else per t: {sel<<62 | offset, line stride}
+  long long tstride;
+  long long lstride;
+};
+
+template <typename C>
+__device__ __forceinline__ C* side_ptr(const SideMap& m, int t, long long lidx) {
+  const longlong2 e = __ldg(m.ttab + t);
+  C* b = reinterpret_cast<C*>((e.x >> 62) ? m.base1 : m.base);
+  return b + ((e.x & ((1LL << 62) - 1)) + lidx * e.y);
+}
+
+// Kernel arguments shared by both families.
+struct PassArgs {
+  SideMap in, out;
+  const void* tw;  // per-pass twiddle tables (complex), sched_twoff layout
+  long long L0, L1;  // line grid: lines (l0, l1), l0 < L0, l1 < L1
+  // contig: Lidx = l0·l0s + l1·l1s for the in/out side; strided: Lidx = l1, l0 is unit stride
+  long long in_l0s, in_l1s, out_l0s, out_l1s;
+  double scale;  // applied to the outputs of the last pass (1 = none)
+};
+
+// --------------------------------------------------------------------------------- Stockham core
+// One thread's part of the passes of one line.  IO supplies the global side:
+//   C load(int t)  and  void store(int t, C v); SM maps t to a shared-memory slot.
+template <typename C, int N, int DIR, int P, class IO, class SM>
+__device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, const C* __restrict__ tw, int j,
+                                              bool active) {
+  constexpr Sched S = make_sched(N);
+  constexpr int R = S.rad[P];
+  constexpr int NR = N / R;
+  constexpr int Ns = sched_ns(S, P);
+  constexpr int NB = (NR + S.T - 1) / S.T;
+  constexpr bool EXACT = (NR % S.T) == 0;
+  constexpr bool LAST = (P == S.npass - 1);
+  C v[NB][R];
+  // ---- gather inputs
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int b = j + S.T * u;
+    if (EXACT || b < NR) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if constexpr (P == 0) {
+          v[u][r] = active ? io.load(b + r * NR) : C{0, 0};
+        } else {
+          v[u][r] = smem[sm(b + r * NR)];
+        }
+      }
+    }
+  }
+  // every read of this pass is done before anything is overwritten (also makes a single-pass
+  // transform safe in place)
+  if constexpr (P > 0 || LAST) __syncthreads();
+  // ---- twiddle, butterfly, scatter
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int b = j + S.T * u;
+    if (EXACT || b < NR) {
+      const int m = b % Ns;
+      if constexpr (P > 0) {
+        const C* twp = tw + sched_twoff(S, P);
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], __ldg(twp + (r - 1) * Ns + m));
+      }
+      dft<DIR, R>(v[u]);
+      const int d = (b / Ns) * Ns * R + m;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if constexpr (LAST) {
+          if (active) io.store(d + r * Ns, v[u][r]);
+        } else {
+          smem[sm(d + r * Ns)] = v[u][r];
+        }
+      }
+    }
+  }
+  if constexpr (!LAST) {
+    __syncthreads();
+    stockham_pass<C, N, DIR, P + 1>(io, sm, smem, tw, j, active);
+  }
+}
+
+// ------------------------------------------------------------------ contiguous-axis family
+template <typename C> struct ContigIO {
+  const C* __restrict__ in;
+  C* __restrict__ out;
+  const SideMap* mi;
+  const SideMap* mo;
+  long long lin, lout;
+  decltype(C{}.x) scale;
+  __device__ __forceinline__ C load(int t) const {
+    if (mi->ttab == nullptr) return in[(long long)t + lin];
+    return *side_ptr<const C>(*mi, t, lin);
+  }
+  __device__ __forceinline__ void store(int t, C v) const {
+    if (scale != 1) { v.x *= scale; v.y *= scale; }
+    if (mo->ttab == nullptr) out[(long long)t + lout] = v;
+    else *side_ptr<C>(*mo, t, lout) = v;
+  }
+};
+
+struct ContigSM {
+  int base;
+  __device__ __forceinline__ int operator()(int t) const { return base + t + (t >> 4); }
+};
+
+template <int N> struct ContigCfg {
+  static constexpr Sched S = make_sched(N);
+  static constexpr int LPC = S.T >= 256 ? 1 : 256 / S.T;  // lines per CTA
+  static constexpr int THREADS = S.T * LPC;
+  static constexpr int LS = N + (N >> 4);  // padded line stride in smem
+};
+
+template <typename Real, int N, int DIR>
+__global__ void __launch_bounds__(ContigCfg<N>::THREADS)
+fft_contig_kernel(const PassArgs a) {
+  using C = typename CT<Real>::type;
+  using Cfg = ContigCfg<N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* smem = reinterpret_cast<C*>(smem_raw);
+  const int li = threadIdx.x / Cfg::S.T;
+  const int j = threadIdx.x % Cfg::S.T;
+  const long long line = (long long)blockIdx.x * Cfg::LPC + li;
+  const bool active = line < a.L0 * a.L1;
+  const long long l1 = active ? line / a.L0 : 0;
+  const long long l0 = active ? line - l1 * a.L0 : 0;
+  ContigIO<C> io;
+  io.in = reinterpret_cast<const C*>(a.in.base);
+  io.out = reinterpret_cast<C*>(a.out.base);
+  io.mi = &a.in;
+  io.mo = &a.out;
+  const long long lin = l0 * a.in_l0s + l1 * a.in_l1s;
+  const long long lout = l0 * a.out_l0s + l1 * a.out_l1s;
+  io.lin = a.in.ttab == nullptr ? lin * a.in.lstride : lin;
+  io.lout = a.out.ttab == nullptr ? lout * a.out.lstride : lout;
+  io.scale = (Real)a.scale;
+  ContigSM sm{li * Cfg::LS};
+  stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
+}
+
+// ------------------------------------------------------------------ strided-axis family
+template <typename Real, int N> struct StridedCfg {
+  static constexpr Sched S = make_sched(N);
+  static constexpr int ES = (int)sizeof(Real) * 2;
+  // W adjacent columns per CTA: 64-128 B row segments, at least 256 threads for short
+  // lines, smem tile capped at 96 KB.
+  static constexpr int W0 = ES == 8 ? 8 : 4;
+  static constexpr int Wthr = S.T * W0 >= 256 ? W0 : 256 / S.T;
+  static constexpr int Wcap = (96 * 1024) / (N * ES) >= 1 ? (96 * 1024) / (N * ES) : 1;
+  static constexpr int W = Wthr < Wcap ? Wthr : (Wcap >= 8 ? 8 : Wcap >= 4 ? 4 : Wcap >= 2 ? 2 : 1);
+  static constexpr int THREADS = S.T * W;
+  // pad W/2 slots per R0 rows when a row is narrower than 128 B (tools/bank_sim.py)
+  static constexpr int PAD = (W * ES < 128) ? (W / 2 > 0 ? W / 2 : 1) : 0;
+  static constexpr int R0 = S.rad[0];
+  static constexpr int SMEM_ELEMS = N * W + (N / R0) * PAD;
+};
+
+template <typename C> struct StridedIO {
+  const C* __restrict__ in;
+  C* __restrict__ out;
+  const SideMap* mi;
+  const SideMap* mo;
+  long long cin, cout;  // unsegmented: column offset incl. l1·lstride; segmented: l0
+  long long l1;
+  decltype(C{}.x) scale;
+  __device__ __forceinline__ C load(int t) const {
+    if (mi->ttab == nullptr) return in[(long long)t * mi->tstride + cin];
+    return side_ptr<const C>(*mi, t, l1)[cin];
+  }
+  __device__ __forceinline__ void store(int t, C v) const {
+    if (scale != 1) { v.x *= scale; v.y *= scale; }
+    if (mo->ttab == nullptr) out[(long long)t * mo->tstride + cout] = v;
+    else side_ptr<C>(*mo, t, l1)[cout] = v;
+  }
+};
+
+template <int W, int R0, int PAD> struct StridedSM {
+  int c;
+  __device__ __forceinline__ int operator()(int t) const { return t * W + c + (t / R0) * PAD; }
+};
+
+template <typename Real, int N, int DIR>
+__global__ void __launch_bounds__(StridedCfg<Real, N>::THREADS)
+fft_strided_kernel(const PassArgs a) {
+  using C = typename CT<Real>::type;
+  using Cfg = StridedCfg<Real, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* smem = reinterpret_cast<C*>(smem_raw);
+  const int c = threadIdx.x % Cfg::W;
+  const int j = threadIdx.x / Cfg::W;
+  const long long ntile = (a.L0 + Cfg::W - 1) / Cfg::W;
+  const long long l1 = blockIdx.x / ntile;
+  const long long l0 = (blockIdx.x - l1 * ntile) * Cfg::W + c;
+  const bool active = l0 < a.L0;
+  StridedIO<C> io;
+  io.in = reinterpret_cast<const C*>(a.in.base);
+  io.out = reinterpret_cast<C*>(a.out.base);
+  io.mi = &a.in;
+  io.mo = &a.out;
+  io.l1 = l1;
+  io.cin = a.in.ttab == nullptr ? l0 + l1 * a.in.lstride : l0;
+  io.cout = a.out.ttab == nullptr ? l0 + l1 * a.out.lstride : l0;
+  io.scale = (Real)a.scale;
+  StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
+  stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
+}
+
+}  // namespace dfft

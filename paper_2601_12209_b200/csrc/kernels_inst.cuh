@@ -1,0 +1,46 @@
+// kernels_inst.cuh — instantiation + registration of the FFT kernels for one precision.
+// Included by kernels_f32.cu / kernels_f64.cu with DFFT_REAL and DFFT_LOOKUP defined.
+#include "registry.h"
+
+namespace dfft {
+
+namespace {
+template <typename Real, int N, int DIR>
+KernelInfo make_contig() {
+  using Cfg = ContigCfg<N>;
+  KernelInfo k;
+  k.fn = (const void*)&fft_contig_kernel<Real, N, DIR>;
+  k.threads = Cfg::THREADS;
+  k.per_cta = Cfg::LPC;
+  k.smem = Cfg::S.npass > 1 ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
+  k.twlen = sched_twlen(Cfg::S);
+  return k;
+}
+template <typename Real, int N, int DIR>
+KernelInfo make_strided() {
+  using Cfg = StridedCfg<Real, N>;
+  KernelInfo k;
+  k.fn = (const void*)&fft_strided_kernel<Real, N, DIR>;
+  k.threads = Cfg::THREADS;
+  k.per_cta = Cfg::W;
+  k.smem = Cfg::S.npass > 1 ? (size_t)Cfg::SMEM_ELEMS * sizeof(Real) * 2 : 0;
+  k.twlen = sched_twlen(Cfg::S);
+  return k;
+}
+}  // namespace
+
+bool DFFT_LOOKUP(int family, int n, int dir, KernelInfo* out) {
+#define DFFT_CASE(N)                                                                             \
+  case N:                                                                                        \
+    if (family == kContig) *out = dir < 0 ? make_contig<DFFT_REAL, N, -1>() : make_contig<DFFT_REAL, N, 1>(); \
+    else *out = dir < 0 ? make_strided<DFFT_REAL, N, -1>() : make_strided<DFFT_REAL, N, 1>();    \
+    return true;
+  switch (n) {
+    DFFT_LENGTHS(DFFT_CASE)
+    default:
+      return false;
+  }
+#undef DFFT_CASE
+}
+
+}  // namespace dfft

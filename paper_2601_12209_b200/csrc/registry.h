@@ -1,0 +1,34 @@
+// registry.h — host-side lookup of the instantiated FFT kernels (one per family × length ×
+// precision × direction), with their launch shapes.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "fft_kernels.cuh"
+
+namespace dfft {
+
+enum Family { kContig = 0, kStrided = 1 };
+
+struct KernelInfo {
+  const void* fn = nullptr;
+  int threads = 0;       // CTA size
+  int per_cta = 0;       // contig: lines per CTA; strided: columns per CTA (W)
+  size_t smem = 0;       // dynamic shared memory bytes
+  int twlen = 0;         // twiddle table length (complex elements)
+};
+
+// Supported axis lengths: 2^a (2..4096), 3·2^a (3..3072), and the paper's
+// GPU shapes 480/720/840 with radix 5 and 7.
+#define DFFT_LENGTHS(X) \
+  X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096) \
+  X(3) X(6) X(12) X(24) X(48) X(96) X(192) X(384) X(768) X(1536) X(3072) \
+  X(5) X(7) X(480) X(720) X(840)
+
+bool lookup_kernel_f32(int family, int n, int dir, KernelInfo* out);
+bool lookup_kernel_f64(int family, int n, int dir, KernelInfo* out);
+bool length_supported(long long n);
+// radix schedule of length n (for twiddle generation): returns npass, fills rad[]
+int length_schedule(int n, int rad[kMaxPass]);
+
+}  // namespace dfft

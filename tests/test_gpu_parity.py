@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Gates (BASELINE.json north_star): rel-L2 <= 2e-5 (fp32), <= 1e-12 (fp64) vs the fp64 oracle
+fed bit-identical inputs (fp32 plans: inputs rounded to float on both sides).  Tighter
+QUALITY bounds catch precision bugs the gate is blind to.
+"""
+import numpy as np
+import pytest
+
+from helpers import GATE, LENGTHS, QUALITY, box_slice, rel_l2
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import inputs  # noqa: E402
+import paper_2601_12209_b200 as dfft  # noqa: E402
+
+CDT = {"f32": torch.complex64, "f64": torch.complex128}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _t(a, prec):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(CDT[prec]).cuda()
+
+
+# ------------------------------------------------------------------------------ generator bits
+def test_cuda_generator_matches_numpy_bits():
+    g, lo, n = (24, 20, 12), (3, 5, 2), (17, 9, 7)
+    for f32 in (False, True):
+        t = torch.empty((n[2], n[1], n[0]), dtype=torch.complex64 if f32 else torch.complex128, device="cuda")
+        inputs.fill_box_cuda(t, 99, g, lo, n, True)
+        ref = inputs.gen_complex_np(99, g, lo, n, f32=f32)
+        assert np.array_equal(t.cpu().numpy().view(np.uint8), ref.view(np.uint8))
+        r = torch.empty((n[2], n[1], n[0]), dtype=torch.float32 if f32 else torch.float64, device="cuda")
+        inputs.fill_box_cuda(r, 99, g, lo, n, False)
+        assert np.array_equal(r.cpu().numpy(), inputs.gen_real_np(99, g, lo, n, f32=f32))
+
+
+# ------------------------------------------------------------------------------ 1D kernels
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("n", LENGTHS)
+def test_fft1d_every_length(oracle_mod, n, prec):
+    batch = 37  # ragged against lines-per-CTA
+    x = inputs.gen_complex_np(7, (n, batch, 1), f32=(prec == "f32"))[0]  # (batch, n)
+    xt = _t(x, prec)
+    for sign in (-1, 1):
+        y = torch.empty_like(xt)
+        dfft.fft1d(xt, y, sign)
+        torch.cuda.synchronize()
+        ref = np.stack([oracle_mod.fft1d(row.astype(np.complex128), sign) for row in x])
+        e = rel_l2(y.cpu().numpy(), ref)
+        assert e <= GATE[prec], (n, sign, e)
+        assert e <= QUALITY[prec], (n, sign, e)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("n", [8, 64, 384, 480, 720, 768, 840, 1024, 4096])
+def test_fft1d_plane_waves_exact_bins(n, prec):
+    # exp(+2πi m t/n) -> n at k = m only: a misplaced bin is an O(1) error (pin independent of the oracle)
+    ms = [0, 1, n // 3, n // 2, n - 1]
+    t = np.arange(n)
+    x = np.stack([np.exp(2j * np.pi * ((m * t) % n) / n) for m in ms])
+    y = torch.empty((len(ms), n), dtype=CDT[prec], device="cuda")
+    dfft.fft1d(_t(x, prec), y, -1)
+    torch.cuda.synchronize()
+    e = np.zeros((len(ms), n), complex)
+    e[np.arange(len(ms)), ms] = n
+    tol = (2e-4 if prec == "f32" else 1e-11) * n
+    assert np.abs(y.cpu().numpy() - e).max() < tol
+
+
+# ------------------------------------------------------------------------------ 3D, one GPU
+def _run_single(oracle_mod, shape, decomp, prec, seed=3):
+    comm = dfft.Comm.create(nranks=1, rank=0, device=0)
+    dt = "c2c_" + prec
+    fwd = dfft.Plan(comm, shape, decomp, (1, 1), dt, dfft.FORWARD)
+    inv = dfft.Plan(comm, shape, decomp, (1, 1), dt, dfft.INVERSE)
+    x = fwd.alloc_in()
+    inputs.fill_box_cuda(x, seed, shape, (0, 0, 0), shape, True)
+    y = fwd.alloc_out()
+    z = inv.alloc_out()
+    fwd.execute(x, y)
+    inv.execute(y, z)
+    torch.cuda.synchronize()
+    a = oracle_mod.gen_complex(seed, shape, f32=(prec == "f32"))
+    A = oracle_mod.fft3d(a, -1)
+    ef = oracle_mod.rel_l2(y.cpu().numpy(), A)
+    er = oracle_mod.rel_l2(z.cpu().numpy(), a)
+    # inverse alone against the oracle's inverse of the same (GPU-produced) spectrum
+    B = oracle_mod.fft3d(y.cpu().numpy().astype(np.complex128), +1)
+    ei = oracle_mod.rel_l2(z.cpu().numpy(), B)
+    return ef, er, ei
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape", [(64, 64, 64), (8, 8, 8), (16, 12, 8), (6, 24, 48), (480, 3, 7), (2, 4, 4096),
+                                   (1024, 8, 6), (5, 768, 2), (840, 4, 2), (4, 720, 3)])
+def test_3d_single_gpu(oracle_mod, shape, prec):
+    ef, er, ei = _run_single(oracle_mod, shape, "pencil", prec)
+    assert ef <= GATE[prec] and er <= GATE[prec] and ei <= GATE[prec], (ef, er, ei)
+    assert ef <= QUALITY[prec] and ei <= QUALITY[prec], (ef, er, ei)
+
+
+def test_cfg1_64cubed_c128_slab(oracle_mod):
+    # BASELINE.json configs[0]: 64^3 complex128 c2c forward+inverse, single GPU, slab
+    ef, er, ei = _run_single(oracle_mod, (64, 64, 64), "slab", "f64", seed=260112209 + 1)
+    assert ef <= 1e-12 and er <= 1e-12 and ei <= 1e-12
+
+
+def test_closed_forms_3d_gpu():
+    shape = (64, 48, 32)
+    comm = dfft.Comm.create(nranks=1, rank=0, device=0)
+    fwd = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_f64", dfft.FORWARD)
+    x = fwd.alloc_in().zero_()
+    x[0, 0, 0] = 1
+    y = fwd.alloc_out()
+    fwd.execute(x, y)
+    assert (y - 1).abs().max().item() < 1e-14  # delta -> all ones
+    c = 0.25 - 0.5j
+    x.fill_(c)
+    fwd.execute(x, y)
+    yy = y.cpu().numpy()
+    assert abs(yy[0, 0, 0] - c * x.numel()) < 1e-9
+    yy[0, 0, 0] = 0
+    assert np.abs(yy).max() < 1e-9  # constant -> DC spike only
+
+
+# ------------------------------------------------------------------------------ simulated ranks
+def _run_sim(oracle_mod, shape, decomp, grid, prec, chunks, seed=5):
+    P = grid[0] * grid[1]
+    comm = dfft.Comm.simulated(P, 0)
+    dt = "c2c_" + prec
+    fwd = dfft.Plan(comm, shape, decomp, grid, dt, dfft.FORWARD, chunks=chunks)
+    inv = dfft.Plan(comm, shape, decomp, grid, dt, dfft.INVERSE, chunks=chunks)
+    xs, ys, zs = [], [], []
+    for r in range(P):
+        lo, n = fwd.box(0, r)
+        x = fwd.alloc_in(r)
+        inputs.fill_box_cuda(x, seed, shape, lo, n, True)
+        xs.append(x)
+        ys.append(fwd.alloc_out(r))
+        zs.append(inv.alloc_out(r))
+    fwd.execute_sim(xs, ys)
+    inv.execute_sim(ys, zs)
+    torch.cuda.synchronize()
+    a = oracle_mod.gen_complex(seed, shape, f32=(prec == "f32"))
+    A = oracle_mod.fft3d(a, -1)
+    Y = np.zeros_like(A)
+    Z = np.zeros_like(a)
+    for r in range(P):
+        lo, n = fwd.box(1, r)
+        box_slice(Y, lo, n)[...] = ys[r].cpu().numpy()
+        lo, n = inv.box(1, r)
+        box_slice(Z, lo, n)[...] = zs[r].cpu().numpy()
+    return oracle_mod.rel_l2(Y, A), oracle_mod.rel_l2(Z, a), Y
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,decomp,grid,chunks", [
+    ((32, 24, 16), "pencil", (2, 4), 1),
+    ((32, 24, 16), "pencil", (2, 4), 2),
+    ((32, 24, 16), "pencil", (2, 4), 3),
+    ((16, 16, 12), "slab", (4, 1), 2),
+    ((48, 12, 6), "pencil", (5, 2), 3),      # uneven splits on every axis
+    ((24, 96, 64), "pencil", (4, 2), 4),
+    ((64, 64, 64), "slab", (8, 1), 4),
+    ((12, 6, 8), "pencil", (3, 2), 2),
+])
+def test_simulated_ranks(oracle_mod, shape, decomp, grid, chunks, prec):
+    ef, er, _ = _run_sim(oracle_mod, shape, decomp, grid, prec, chunks)
+    assert ef <= GATE[prec] and er <= GATE[prec], (ef, er)
+    assert ef <= QUALITY[prec], ef
+
+
+def test_simulated_rank_invariance(oracle_mod):
+    # same kernels on every decomposition: identical arithmetic per line => identical bits
+    shape = (32, 24, 16)
+    _, _, Y1 = _run_sim(oracle_mod, shape, "pencil", (2, 4), "f64", 1)
+    _, _, Y2 = _run_sim(oracle_mod, shape, "pencil", (2, 4), "f64", 3)
+    _, _, Y3 = _run_sim(oracle_mod, shape, "pencil", (4, 2), "f64", 2)
+    _, _, Y4 = _run_sim(oracle_mod, shape, "slab", (8, 1), "f64", 2)
+    assert np.array_equal(Y1, Y2) and np.array_equal(Y1, Y3) and np.array_equal(Y1, Y4)
+
+
+# ------------------------------------------------------------------------------ full size
+def test_headline_1024cubed_c64_single_gpu(oracle_mod):
+    """BASELINE configs[3] at N=1 (the bench workload): sampled bins vs the oracle's direct sums,
+    round trip vs the regenerated input, Parseval — in the launch configuration bench.py times."""
+    shape = (1024, 1024, 1024)
+    seed = 260112209 + 4
+    comm = dfft.Comm.create(nranks=1, rank=0, device=0)
+    fwd = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_f32", dfft.FORWARD)
+    inv = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_f32", dfft.INVERSE)
+    x = fwd.alloc_in()
+    inputs.fill_box_cuda(x, seed, shape, (0, 0, 0), shape, True)
+    y = fwd.alloc_out()
+    fwd.execute(x, y)
+    rng = np.random.default_rng(0)
+    ks = [(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1), (1023, 1023, 1023), (512, 512, 512)]
+    ks += [tuple(int(v) for v in rng.integers(0, 1024, 3)) for _ in range(6)]
+    got = [complex(y[kz, ky, kx].item()) for kx, ky, kz in ks]
+    N = float(np.prod(shape))
+    err2 = 0.0
+    for (kx, ky, kz), g in zip(ks, got):
+        ref = oracle_mod.dft3d_bin_seeded(seed, shape, (kx, ky, kz), f32=True)
+        err2 += abs(g - ref) ** 2
+    # normalise by the expected bin magnitude sqrt(N * E|x|^2) = sqrt(2N/3) for uniform[-1,1) re/im
+    rms_rel = np.sqrt(err2 / len(ks)) / np.sqrt(2 * N / 3)
+    assert rms_rel <= GATE["f32"], rms_rel
+    # Parseval: sum|X|^2 = N sum|x|^2
+    sx = torch.sum(x.abs().double() ** 2).item()
+    sX = torch.sum(y.abs().double() ** 2).item()
+    assert abs(sX / (N * sx) - 1) < 1e-5
+    z = inv.alloc_out()
+    inv.execute(y, z)
+    del y
+    d = (z - x).abs().double().pow(2).sum().item()
+    assert np.sqrt(d / sx) <= GATE["f32"]
