@@ -180,7 +180,7 @@ struct RankPlan {
   size_t in_bytes = 0, out_bytes = 0, ws_bytes = 0;
   void* ws = nullptr;
   std::vector<Stage> A, B;  // per chunk
-  std::vector<Exchange> E1, E2;
+  std::vector<Exchange> E1, E2;  // first / second exchange (each names its comm group)
   Stage C;
 };
 
@@ -400,7 +400,8 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     }
     A.a.scale = 1.0;
     ST(finish_stage(pl, A, kStrided, (int)g.nz, xc, Y3n, nullptr, &at));
-    Exchange& E2 = rp.E2[k];
+    // first exchange of the inverse = T2⁻¹ on the column group
+    Exchange& E2 = rp.E1[k];
     E2.comm = 1;
     for (long long jp = 0; jp < g.P2; ++jp) {
       if (jp == j) continue;
@@ -422,7 +423,8 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     }
     B.a.scale = 1.0;
     ST(finish_stage(pl, B, kStrided, (int)g.ny, xc, Zn, nullptr, &bt));
-    Exchange& E1 = rp.E1[k];
+    // second exchange of the inverse = T1⁻¹ on the row group
+    Exchange& E1 = rp.E2[k];
     E1.comm = 0;
     for (long long ip = 0; ip < g.P1; ++ip) {
       if (ip == i) continue;

@@ -18,12 +18,12 @@ x = fwd.alloc_in()
 inputs.fill_box_cuda(x, 1, shape, (0, 0, 0), shape, True)
 y = fwd.alloc_out()
 z = inv.alloc_out()
-for _ in range(3):
+for _ in range(3 if n > 1 else 1):
     fwd.execute(x, y)
     inv.execute(y, z)
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-n = 10
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 s.record()
 for _ in range(n):
     fwd.execute(x, y)
