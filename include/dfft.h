@@ -147,6 +147,20 @@ dfft_status_t dfft_execute_host(dfft_plan_t plan, const void* in_host, void* out
 /* Simulated comm only: ins[r] / outs[r] are rank r's device boxes, r < nranks. */
 dfft_status_t dfft_execute_sim(dfft_plan_t plan, const void* const* ins, void* const* outs, void* stream);
 
+/* ------------------------------------------------------------------ per-phase profiling
+ * Phases (Fig. 9 breakdown analog): 0 stage-A FFT, 1 first exchange, 2 stage-B FFT,
+ * 3 second exchange, 4 stage-C FFT.  When enabled, every stage launch and exchange of
+ * dfft_execute is bracketed by CUDA timing events on the stream that runs it.
+ * dfft_plan_phase_times synchronises those events and returns the accumulated milliseconds
+ * and launch counts per phase (reset != 0 zeroes the accumulators afterwards).
+ * dfft_plan_stage_bytes returns the algorithmic bytes per execute of each phase: FFT stages
+ * read + write their local array once (2·elements·element size); exchanges count the bytes
+ * this rank sends to other ranks.
+ */
+dfft_status_t dfft_plan_set_profiling(dfft_plan_t plan, int on);
+dfft_status_t dfft_plan_phase_times(dfft_plan_t plan, double ms[5], long long launches[5], int reset);
+dfft_status_t dfft_plan_stage_bytes(dfft_plan_t plan, double bytes[5]);
+
 /* Synchronises the plan's internal streams, then frees everything the plan owns. */
 dfft_status_t dfft_destroy(dfft_plan_t plan);
 

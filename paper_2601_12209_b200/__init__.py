@@ -29,8 +29,9 @@ EXPORTS = [
     "dfft_version", "dfft_status_string", "dfft_last_error", "dfft_get_unique_id", "dfft_comm_init",
     "dfft_comm_init_sim", "dfft_comm_destroy", "dfft_plan_create", "dfft_plan_box", "dfft_plan_box_rank",
     "dfft_plan_bytes", "dfft_decomp_box", "dfft_plan_chunks", "dfft_execute", "dfft_execute_host", "dfft_execute_sim",
-    "dfft_destroy", "dfft_fft1d",
+    "dfft_destroy", "dfft_fft1d", "dfft_plan_set_profiling", "dfft_plan_phase_times", "dfft_plan_stage_bytes",
 ]
+PHASES = ["stage_A", "exchange_1", "stage_B", "exchange_2", "stage_C"]
 
 _lib = None
 _vp = ctypes.c_void_p
@@ -75,6 +76,9 @@ def lib():
         L.dfft_execute_sim.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]
         L.dfft_destroy.argtypes = [_vp]
         L.dfft_fft1d.argtypes = [_vp, _vp, _i64, _i64, _int, _int, _vp]
+        L.dfft_plan_set_profiling.argtypes = [_vp, _int]
+        L.dfft_plan_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), _int]
+        L.dfft_plan_stage_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
         for name in EXPORTS:
             if name not in ("dfft_version", "dfft_status_string", "dfft_last_error"):
                 getattr(L, name).restype = _int
@@ -247,6 +251,21 @@ class Plan:
         outs = (_vp * P)(*[y.data_ptr() for y in ys])
         _check(lib().dfft_execute_sim(self.h, ins, outs, _stream_ptr(stream, xs[0].device)), "dfft_execute_sim")
         return ys
+
+    # profiling ----------------------------------------------------------------------
+    def set_profiling(self, on: bool = True):
+        _check(lib().dfft_plan_set_profiling(self.h, int(on)), "dfft_plan_set_profiling")
+
+    def phase_times(self, reset: bool = True):
+        """{phase: (total ms, launches)} accumulated since the last reset (synchronises)."""
+        ms, n = (ctypes.c_double * 5)(), (ctypes.c_longlong * 5)()
+        _check(lib().dfft_plan_phase_times(self.h, ms, n, int(reset)), "dfft_plan_phase_times")
+        return {PHASES[q]: (ms[q], n[q]) for q in range(5)}
+
+    def stage_bytes(self):
+        b = (ctypes.c_double * 5)()
+        _check(lib().dfft_plan_stage_bytes(self.h, b), "dfft_plan_stage_bytes")
+        return {PHASES[q]: b[q] for q in range(5)}
 
     def destroy(self):
         if getattr(self, "h", None):

@@ -206,6 +206,14 @@ struct dfft_plan_s {
   std::vector<cudaEvent_t> evA, evE1, evB, evE2;
   void* stage_in = nullptr;  // dfft_execute_host staging buffers
   void* stage_out = nullptr;
+  // per-phase profiling (dfft_plan_set_profiling): timing events around every stage launch
+  // and exchange, on the stream that runs it; accumulated by dfft_plan_phase_times
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;                 // pool, pairs (start, stop)
+  std::vector<int> prof_phase;                      // phase id per recorded pair
+  size_t prof_used = 0;                             // pairs recorded since the last read
+  double prof_ms[5] = {0, 0, 0, 0, 0};
+  long long prof_n[5] = {0, 0, 0, 0, 0};
 };
 
 namespace {
@@ -513,17 +521,54 @@ dfft_status_t exchange_sim(dfft_plan_t pl, bool second, size_t k, const void* co
   return DFFT_SUCCESS;
 }
 
+// phases: 0 stage A, 1 exchange 1, 2 stage B, 3 exchange 2, 4 stage C
+dfft_status_t prof_begin(dfft_plan_t pl, int phase, cudaStream_t st, size_t* slot) {
+  if (!pl->prof) return DFFT_SUCCESS;
+  size_t i = pl->prof_used++;
+  while (pl->prof_ev.size() < 2 * pl->prof_used) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    pl->prof_ev.push_back(e);
+  }
+  if (pl->prof_phase.size() < pl->prof_used) pl->prof_phase.resize(pl->prof_used);
+  pl->prof_phase[i] = phase;
+  *slot = i;
+  CU(cudaEventRecord(pl->prof_ev[2 * i], st));
+  return DFFT_SUCCESS;
+}
+dfft_status_t prof_end(dfft_plan_t pl, size_t slot, cudaStream_t st) {
+  if (!pl->prof) return DFFT_SUCCESS;
+  CU(cudaEventRecord(pl->prof_ev[2 * slot + 1], st));
+  return DFFT_SUCCESS;
+}
+dfft_status_t launch_p(dfft_plan_t pl, int phase, const Stage& s, const void* in, void* out, void* ws,
+                       cudaStream_t st) {
+  if (s.empty) return DFFT_SUCCESS;
+  size_t slot = 0;
+  ST(prof_begin(pl, phase, st, &slot));
+  ST(launch(s, in, out, ws, st));
+  return prof_end(pl, slot, st);
+}
+dfft_status_t exchange_p(dfft_plan_t pl, int phase, const Exchange& x, const void* in, void* out, void* ws,
+                         cudaStream_t st) {
+  if (x.empty()) return DFFT_SUCCESS;
+  size_t slot = 0;
+  ST(prof_begin(pl, phase, st, &slot));
+  ST(exchange_nccl(pl, x, in, out, ws, st));
+  return prof_end(pl, slot, st);
+}
+
 dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream_t user) {
   RankPlan& rp = pl->ranks[0];
   const size_t K = rp.A.size();
   void* ws = rp.ws;
   if (!pl->overlap) {
     // static-barrier ablation: every step in program order on the user's stream
-    for (size_t k = 0; k < K; ++k) ST(launch(rp.A[k], in, out, ws, user));
-    for (size_t k = 0; k < K; ++k) ST(exchange_nccl(pl, rp.E1[k], in, out, ws, user));
-    for (size_t k = 0; k < K; ++k) ST(launch(rp.B[k], in, out, ws, user));
-    for (size_t k = 0; k < K; ++k) ST(exchange_nccl(pl, rp.E2[k], in, out, ws, user));
-    return launch(rp.C, in, out, ws, user);
+    for (size_t k = 0; k < K; ++k) ST(launch_p(pl, 0, rp.A[k], in, out, ws, user));
+    for (size_t k = 0; k < K; ++k) ST(exchange_p(pl, 1, rp.E1[k], in, out, ws, user));
+    for (size_t k = 0; k < K; ++k) ST(launch_p(pl, 2, rp.B[k], in, out, ws, user));
+    for (size_t k = 0; k < K; ++k) ST(exchange_p(pl, 3, rp.E2[k], in, out, ws, user));
+    return launch_p(pl, 4, rp.C, in, out, ws, user);
   }
   cudaStream_t sc = pl->s_comp, sm = pl->s_comm;
   CU(cudaEventRecord(pl->ev_fork, user));
@@ -532,11 +577,11 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
   // host issue order is a topological order of the chunk DAG, so every wait refers to the
   // record issued in this execute:  A0 E1_0 | A1 E1_1 B0 E2_0 | A2 E1_2 B1 E2_1 | ...
   auto do_A = [&](size_t k) -> dfft_status_t {
-    ST(launch(rp.A[k], in, out, ws, sc));
+    ST(launch_p(pl, 0, rp.A[k], in, out, ws, sc));
     if (!rp.E1[k].empty()) {
       CU(cudaEventRecord(pl->evA[k], sc));
       CU(cudaStreamWaitEvent(sm, pl->evA[k], 0));
-      ST(exchange_nccl(pl, rp.E1[k], in, out, ws, sm));
+      ST(exchange_p(pl, 1, rp.E1[k], in, out, ws, sm));
       CU(cudaEventRecord(pl->evE1[k], sm));
     }
     return DFFT_SUCCESS;
@@ -545,17 +590,17 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
   for (size_t k = 0; k < K; ++k) {
     if (k + 1 < K) ST(do_A(k + 1));
     if (!rp.E1[k].empty()) CU(cudaStreamWaitEvent(sc, pl->evE1[k], 0));
-    ST(launch(rp.B[k], in, out, ws, sc));
+    ST(launch_p(pl, 2, rp.B[k], in, out, ws, sc));
     if (!rp.E2[k].empty()) {
       CU(cudaEventRecord(pl->evB[k], sc));
       CU(cudaStreamWaitEvent(sm, pl->evB[k], 0));
-      ST(exchange_nccl(pl, rp.E2[k], in, out, ws, sm));
+      ST(exchange_p(pl, 3, rp.E2[k], in, out, ws, sm));
       CU(cudaEventRecord(pl->evE2[k], sm));
     }
   }
   // stage C needs every chunk of exchange 2 (same comm stream => the last record suffices)
   if (!rp.E2[K - 1].empty()) CU(cudaStreamWaitEvent(sc, pl->evE2[K - 1], 0));
-  ST(launch(rp.C, in, out, ws, sc));
+  ST(launch_p(pl, 4, rp.C, in, out, ws, sc));
   CU(cudaEventRecord(pl->ev_join_comp, sc));
   CU(cudaEventRecord(pl->ev_join_comm, sm));
   CU(cudaStreamWaitEvent(user, pl->ev_join_comp, 0));
@@ -593,6 +638,7 @@ void free_plan(dfft_plan_t pl) {
   }
   for (auto* v : {&pl->evA, &pl->evE1, &pl->evB, &pl->evE2})
     for (cudaEvent_t e : *v) cudaEventDestroy(e);
+  for (cudaEvent_t e : pl->prof_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : {pl->ev_fork, pl->ev_join_comp, pl->ev_join_comm})
     if (e) cudaEventDestroy(e);
   if (pl->s_comp) cudaStreamDestroy(pl->s_comp);
@@ -923,6 +969,59 @@ dfft_status_t dfft_execute_sim(dfft_plan_t pl, const void* const* ins, void* con
   ST(execute_sim(pl, ins, outs, (cudaStream_t)stream));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(DFFT_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t dfft_plan_set_profiling(dfft_plan_t pl, int on) {
+  if (!pl) return fail(DFFT_ERR_INVALID_VALUE, "null plan");
+  pl->prof = on != 0;
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t dfft_plan_phase_times(dfft_plan_t pl, double ms[5], long long launches[5], int reset) {
+  if (!pl || !ms) return fail(DFFT_ERR_INVALID_VALUE, "null argument");
+  for (size_t i = 0; i < pl->prof_used; ++i) {
+    CU(cudaEventSynchronize(pl->prof_ev[2 * i + 1]));
+    float t = 0;
+    CU(cudaEventElapsedTime(&t, pl->prof_ev[2 * i], pl->prof_ev[2 * i + 1]));
+    pl->prof_ms[pl->prof_phase[i]] += t;
+    pl->prof_n[pl->prof_phase[i]] += 1;
+  }
+  pl->prof_used = 0;
+  for (int q = 0; q < 5; ++q) {
+    ms[q] = pl->prof_ms[q];
+    if (launches) launches[q] = pl->prof_n[q];
+    if (reset) {
+      pl->prof_ms[q] = 0;
+      pl->prof_n[q] = 0;
+    }
+  }
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t dfft_plan_stage_bytes(dfft_plan_t pl, double bytes[5]) {
+  if (!pl || !bytes) return fail(DFFT_ERR_INVALID_VALUE, "null argument");
+  const RankPlan& rp = pl->ranks[0];
+  // algorithmic bytes per execute of each phase: every stage reads and writes its local
+  // array once; every exchange sends its off-rank blocks (the bytes that cross NVLink)
+  auto stage_b = [&](const Stage& s) {
+    if (s.empty) return 0.0;
+    double elems = (double)s.a.L0 * (double)s.a.L1 * (double)s.n;  // complex elements of the FFT
+    return 2.0 * elems * (double)pl->es;
+  };
+  auto xch_b = [&](const Exchange& x) {
+    double b = 0;
+    for (const Xfer& t : x.sends) b += (double)t.bytes;
+    return b;
+  };
+  for (int q = 0; q < 5; ++q) bytes[q] = 0;
+  for (size_t k = 0; k < rp.A.size(); ++k) {
+    bytes[0] += stage_b(rp.A[k]);
+    bytes[1] += xch_b(rp.E1[k]);
+    bytes[2] += stage_b(rp.B[k]);
+    bytes[3] += xch_b(rp.E2[k]);
+  }
+  bytes[4] = stage_b(rp.C);
   return DFFT_SUCCESS;
 }
 

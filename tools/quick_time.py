@@ -14,6 +14,7 @@ prec = sys.argv[2] if len(sys.argv) > 2 else "f32"
 comm = dfft.Comm.create(nranks=1, rank=0, device=0)
 fwd = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_" + prec, dfft.FORWARD)
 inv = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_" + prec, dfft.INVERSE)
+n = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 x = fwd.alloc_in()
 inputs.fill_box_cuda(x, 1, shape, (0, 0, 0), shape, True)
 y = fwd.alloc_out()
@@ -23,7 +24,6 @@ for _ in range(3 if n > 1 else 1):
     inv.execute(y, z)
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-n = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 s.record()
 for _ in range(n):
     fwd.execute(x, y)
