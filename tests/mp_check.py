@@ -37,7 +37,7 @@ def main():
     comm = dfft.Comm.create()
     grids = {2: [("pencil", (1, 2)), ("pencil", (2, 1)), ("slab", (2, 1))],
              4: [("pencil", (2, 2)), ("pencil", (1, 4)), ("pencil", (4, 1)), ("slab", (4, 1))]}[P]
-    shapes = [(32, 24, 16), (48, 20, 12), (64, 64, 64)]
+    shapes = [(32, 24, 16), (48, 12, 6), (64, 64, 64)]
     cases = [(d, g, s, p) for d, g in grids for s in shapes for p in ("f32", "f64")]
     import oracle
 
