@@ -17,7 +17,7 @@ import os
 from typing import Sequence
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libdfft.so")
+LIB_PATH = os.environ.get("DFFT_LIB", os.path.join(PKG, "libdfft.so"))  # DFFT_LIB: dev A/B builds only
 
 FORWARD, INVERSE = -1, 1
 SLAB, PENCIL = 1, 2

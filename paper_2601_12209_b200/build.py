@@ -41,7 +41,11 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, defines=(), lib_name: str = "libdfft.so") -> str:
+    """defines / lib_name: dev A/B variants (e.g. -DDFFT_STRIDED_W0=128 -> libdfft_w16.so)."""
+    global BUILD
+    if defines:
+        BUILD = os.path.join(ROOT, "build", lib_name.replace(".so", ""))
     os.makedirs(BUILD, exist_ok=True)
     nccl = nccl_dir()
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
@@ -54,13 +58,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
             obj = os.path.join(BUILD, u.replace(".cu", ".o"))
             objs.append(obj)
             if force or _stale(obj, [src] + headers):
-                cmd = [NVCC] + CFLAGS + ["-I" + os.path.join(nccl, "include"), "-Xptxas", "-v", "-c", src, "-o", obj]
+                cmd = [NVCC] + CFLAGS + list(defines) + ["-I" + os.path.join(nccl, "include"), "-Xptxas", "-v", "-c",
+                                                         src, "-o", obj]
                 jobs.append(ex.submit(_run, cmd))
         for j in jobs:
             out = j.result()
             if verbose:
                 print(out)
-    lib = os.path.join(PKG, "libdfft.so")
+    lib = os.path.join(PKG, lib_name)
     if force or _stale(lib, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", lib] + objs +
              ["-L" + os.path.join(nccl, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nccl, "lib")])
@@ -72,4 +77,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    names = [a for a in sys.argv[1:] if a.endswith(".so")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, defines=defs,
+                lib_name=names[0] if names else "libdfft.so"))

@@ -11,6 +11,8 @@
 // and the self block is written straight into its final place (Alg. 2 phase 4 elided).
 // The K chunks run on a compute stream and a comm stream linked by events, so chunk k's
 // exchange overlaps chunk k+1's FFT (Fig. 1 "progressive per-chunk pipelining").
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -138,11 +140,35 @@ dfft_status_t get_twiddles(int n, bool f64, int dir, int dev, const void** out) 
   return DFFT_SUCCESS;
 }
 
+bool g_use_tma = getenv("DFFT_NO_TMA") == nullptr;  // env switch for the A/B ablation
+CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                     : getenv("DFFT_TMA_PROMO128") ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                                   : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+bool g_oop_z = getenv("DFFT_OOP_Z") != nullptr;  // dev: P=1 forward z-stage out of place
+bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
+
 dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
   bool ok = f64 ? lookup_kernel_f64(family, n, dir, k) : lookup_kernel_f32(family, n, dir, k);
   if (!ok) return fail(DFFT_ERR_UNSUPPORTED, "axis length %d not instantiated", n);
   if (k->smem > 48 * 1024) CU(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->smem));
+  if (k->tma_fn && k->tma_smem > 48 * 1024) {
+    CU(cudaFuncSetAttribute(k->tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
+    CU(cudaFuncSetAttribute(k->tma_st_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
+  }
   return DFFT_SUCCESS;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
 }
 
 // ------------------------------------------------------------------------------ plan data
@@ -153,13 +179,14 @@ struct Ref {
 };
 
 struct Stage {
-  int family = 0, n = 0;
+  int family = 0, n = 0, es = 8;
   KernelInfo k;
   PassArgs a{};
   Ref in, in1, out, out1;
   void* in_tab = nullptr;  // device longlong2[n] or null
   void* out_tab = nullptr;
   long long grid = 0;
+  long long tma_grid = 0;  // persistent grid of the TMA variant (0 = not usable)
   bool empty = false;
 };
 
@@ -233,10 +260,30 @@ inline longlong2 tent(int sel, long long off, long long lstr) {
   return e;
 }
 
+// A segmented side whose table is a single affine segment (one owner, e.g. P2 == 1) becomes an
+// unsegmented side: base += toff(0), tstride = toff(1) - toff(0), lstride = lstr.
+bool linearize(const std::vector<longlong2>& tab, Ref& base, const Ref& base1, SideMap& m, long long es, bool unit_t) {
+  const long long mask = (1LL << 62) - 1;
+  const long long sel = tab[0].x >> 62, off0 = tab[0].x & mask, lstr = tab[0].y;
+  const long long ts = tab.size() > 1 ? (tab[1].x & mask) - off0 : 1;
+  if (unit_t && ts != 1) return false;
+  for (size_t t = 0; t < tab.size(); ++t)
+    if ((tab[t].x >> 62) != sel || (tab[t].x & mask) != off0 + (long long)t * ts || tab[t].y != lstr) return false;
+  Ref b = sel ? base1 : base;
+  b.off += off0 * es;
+  base = b;
+  m.tstride = ts;
+  m.lstride = lstr;
+  return true;
+}
+
 dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long long L0, long long L1,
                            const std::vector<longlong2>* in_tab, const std::vector<longlong2>* out_tab) {
+  if (in_tab && linearize(*in_tab, s.in, s.in1, s.a.in, (long long)pl->es, family == kContig)) in_tab = nullptr;
+  if (out_tab && linearize(*out_tab, s.out, s.out1, s.a.out, (long long)pl->es, family == kContig)) out_tab = nullptr;
   s.family = family;
   s.n = n;
+  s.es = (int)pl->es;
   s.a.L0 = L0;
   s.a.L1 = L1;
   if (L0 <= 0 || L1 <= 0) {
@@ -252,6 +299,18 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   if (family == kContig) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
   else s.grid = ((L0 + s.k.per_cta - 1) / s.k.per_cta) * L1;
   if (s.grid >= (1LL << 31)) return fail(DFFT_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", s.grid);
+  if (family == kStrided && s.k.tma_fn && g_use_tma && !in_tab && tensor_map_encoder()) {
+    const long long es = (long long)pl->es;
+    bool ok = (s.a.in.tstride * es) % 16 == 0 && (L1 == 1 || (s.a.in.lstride * es) % 16 == 0) &&
+              2 * L0 < (1LL << 32) && L1 < (1LL << 31);
+    if (ok) {
+      int occ = 0, dev = pl->comm->device, sms = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, s.k.tma_fn, s.k.tma_threads, s.k.tma_smem));
+      CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      long long tiles = ((L0 + s.k.tma_w - 1) / s.k.tma_w) * L1;
+      if (occ > 0) s.tma_grid = std::min<long long>(tiles, (long long)sms * occ);
+    }
+  }
   return DFFT_SUCCESS;
 }
 
@@ -282,6 +341,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long R1 = S1 + S1n, R1n = g.ny * Zn * Xn;
   const long long S2 = R1 + R1n, S2n = Zn * Xn * (g.ny - Y3n);
   rp.ws_bytes = (size_t)(S2 + S2n) * es;
+  if (g_oop_z && g.P1 == 1 && g.P2 == 1) rp.ws_bytes = std::max<size_t>(rp.ws_bytes, (size_t)(g.nxc * g.ny * g.nz * es));
   auto s1off = [&](long long k, long long ip) {
     long long acc = 0;
     for (long long q = 0; q < ip; ++q)
@@ -295,6 +355,9 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     return S2 + Xn * (g.z0(j, k) * (g.ny - Y3n) + g.zc(j, k) * acc);
   };
   const long long in_es = pl->r2c ? es / 2 : es;  // bytes of one input element
+  // P = 1 variant: A writes the transposed buffer into `out`, B writes natural order into the
+  // workspace, C runs out of place workspace -> `out` (dev switch DFFT_OOP_Z)
+  const bool oop = g_oop_z && g.P1 == 1 && g.P2 == 1;
   rp.A.resize(K);
   rp.B.resize(K);
   rp.E1.resize(K);
@@ -308,7 +371,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     A.a.in.lstride = pl->r2c ? g.nx / 2 : g.nx;
     A.a.in_l0s = 1;
     A.a.in_l1s = Y1n;
-    A.out = {kWs, 0};
+    A.out = {oop ? kUserOut : kWs, 0};
     A.a.out_l0s = zc;  // Lidx = y·zc + zz
     A.a.out_l1s = 1;
     std::vector<longlong2> ot(g.nxc);
@@ -330,11 +393,11 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     }
     // ---- stage B: y-FFT of columns (x, zz) of recv1 chunk k; out segmented by y-owner j'
     Stage& B = rp.B[k];
-    B.in = {kWs, (R1 + g.ny * z0 * Xn) * es};
+    B.in = {oop ? kUserOut : kWs, (R1 + g.ny * z0 * Xn) * es};
     B.a.in.tstride = zc * Xn;
     B.a.in.lstride = Xn;
     B.out = {kWs, 0};
-    B.out1 = {kUserOut, 0};
+    B.out1 = {oop ? kWs : kUserOut, 0};
     std::vector<longlong2> bt(g.ny);
     for (long long t = 0; t < g.ny; ++t) {
       long long jp = owner(t, g.ny, g.P2), tl = t - g.Y3lo(jp);
@@ -355,12 +418,85 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   }
   // ---- stage C: z-FFT in place on `out`
   Stage& C = rp.C;
-  C.in = {kUserOut, 0};
+  C.in = {oop ? kWs : kUserOut, 0};
   C.out = {kUserOut, 0};
   C.a.in.tstride = C.a.out.tstride = Y3n * Xn;
   C.a.in.lstride = C.a.out.lstride = Xn;
   C.a.scale = 1.0;
   ST(finish_stage(pl, C, kStrided, (int)g.nz, Xn, Y3n, nullptr, nullptr));
+  return DFFT_SUCCESS;
+}
+
+// Single GPU (P = 1, any decomposition): no exchange, so the axis order is free (the 3D DFT is
+// separable).  Order the stages so every stage writes at a small stride (large-stride stores
+// throttle a pass; large-stride loads do not — r01 measurements):
+//   forward: x (in -> out, natural), z (out -> ws as [y][z][x]), y (ws -> out, natural)
+//   inverse: y (in -> out, natural), z (out -> ws as [y][z][x]), x (ws -> out, natural, ×1/N)
+dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
+  const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
+  rp.ws_bytes = (size_t)(nxc * ny * nz * es);
+  rp.A.resize(1);
+  rp.B.resize(1);
+  rp.E1.resize(1);
+  rp.E2.resize(1);
+  Stage &A = rp.A[0], &B = rp.B[0], &C = rp.C;
+  // z-pass: natural [z][y][x] -> ws [y][z][x]
+  auto zpass = [&](Stage& Z) -> dfft_status_t {
+    Z.in = {kUserOut, 0};
+    Z.a.in.tstride = ny * nxc;
+    Z.a.in.lstride = nxc;
+    Z.out = {kWs, 0};
+    Z.a.out.tstride = nxc;
+    Z.a.out.lstride = nz * nxc;
+    Z.a.scale = 1.0;
+    return finish_stage(pl, Z, kStrided, (int)nz, nxc, ny, nullptr, nullptr);
+  };
+  if (pl->dir == DFFT_FORWARD) {
+    A.in = {kUserIn, 0};
+    A.a.in.tstride = 1;
+    A.a.in.lstride = pl->r2c ? nx / 2 : nx;
+    A.a.in_l0s = 1;
+    A.a.in_l1s = ny;
+    A.out = {kUserOut, 0};
+    A.a.out.tstride = 1;
+    A.a.out.lstride = nxc;
+    A.a.out_l0s = 1;
+    A.a.out_l1s = ny;
+    A.a.scale = 1.0;
+    ST(finish_stage(pl, A, kContig, (int)(pl->r2c ? nx / 2 : nx), ny, nz, nullptr, nullptr));
+    ST(zpass(B));
+    C.in = {kWs, 0};
+    C.a.in.tstride = nz * nxc;
+    C.a.in.lstride = nxc;
+    C.out = {kUserOut, 0};
+    C.a.out.tstride = nxc;
+    C.a.out.lstride = ny * nxc;
+    C.a.scale = 1.0;
+    ST(finish_stage(pl, C, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
+  } else {
+    if (pl->r2c) return fail(DFFT_ERR_UNSUPPORTED, "C2R single-GPU path not built yet");
+    A.in = {kUserIn, 0};
+    A.a.in.tstride = nxc;
+    A.a.in.lstride = ny * nxc;
+    A.out = {kUserOut, 0};
+    A.a.out.tstride = nxc;
+    A.a.out.lstride = ny * nxc;
+    A.a.scale = 1.0;
+    ST(finish_stage(pl, A, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
+    ST(zpass(B));
+    C.in = {kWs, 0};
+    C.a.in.tstride = 1;
+    C.a.in.lstride = nxc;
+    C.a.in_l0s = nz;  // line (y, z) of ws [y][z][x] is y·nz + z
+    C.a.in_l1s = 1;
+    C.out = {kUserOut, 0};
+    C.a.out.tstride = 1;
+    C.a.out.lstride = pl->r2c ? nx / 2 : nx;
+    C.a.out_l0s = 1;
+    C.a.out_l1s = ny;
+    C.a.scale = 1.0 / ((double)nx * (double)ny * (double)nz);
+    ST(finish_stage(pl, C, kContig, (int)(pl->r2c ? nx / 2 : nx), ny, nz, nullptr, nullptr));
+  }
   return DFFT_SUCCESS;
 }
 
@@ -478,6 +614,32 @@ dfft_status_t launch(const Stage& s, const void* in, void* out, void* ws, cudaSt
   a.in.base1 = resolve(s.in1, in, out, ws);
   a.out.base = resolve(s.out, in, out, ws);
   a.out.base1 = resolve(s.out1, in, out, ws);
+  if (s.tma_grid > 0 && ((uintptr_t)a.in.base & 15) == 0) {
+    // 3D views in reals: (2·L0, n, L1) with strides (tstride, lstride) elements
+    const bool f64 = s.es == 16;
+    const cuuint64_t esz = f64 ? 8 : 4, ces = 2 * esz;
+    auto encode = [&](CUtensorMap* tm, void* base, long long tstride, long long lstride) {
+      cuuint64_t dims[3] = {(cuuint64_t)(2 * a.L0), (cuuint64_t)s.n, (cuuint64_t)a.L1};
+      cuuint64_t strides[2] = {(cuuint64_t)tstride * ces,
+                               (cuuint64_t)(a.L1 > 1 ? lstride * ces : 16 * ((tstride * ces * s.n + 15) / 16))};
+      cuuint32_t box[3] = {(cuuint32_t)(2 * s.k.tma_w), (cuuint32_t)s.k.tma_boxr, 1};
+      cuuint32_t estr[3] = {1, 1, 1};
+      return tensor_map_encoder()(tm, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  g_tma_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    CUtensorMap tin, tout;
+    if (encode(&tin, a.in.base, a.in.tstride, a.in.lstride)) {
+      bool use_st = g_tma_store && a.out.ttab == nullptr && ((uintptr_t)a.out.base & 15) == 0 &&
+                (a.out.tstride * (long long)ces) % 16 == 0 && (a.L1 == 1 || (a.out.lstride * (long long)ces) % 16 == 0) &&
+                encode(&tout, a.out.base, a.out.tstride, a.out.lstride);
+      if (!use_st) tout = tin;  // unused by the non-TST variant
+      void* targs[] = {&tin, &tout, &a};
+      CU(cudaLaunchKernel(use_st ? s.k.tma_st_fn : s.k.tma_fn, dim3((unsigned)s.tma_grid), dim3(s.k.tma_threads), targs,
+                          s.k.tma_smem, st));
+      return DFFT_SUCCESS;
+    }
+  }
   void* args[] = {&a};
   CU(cudaLaunchKernel(s.k.fn, dim3((unsigned)s.grid), dim3(s.k.threads), args, s.k.smem, st));
   return DFFT_SUCCESS;
@@ -864,7 +1026,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       memcpy(rp.out_n, d3n, sizeof d3n);
       rp.in_bytes = d1b;
       rp.out_bytes = d3b;
-      ST(build_forward(pl, g, rp));
+      ST(P == 1 ? build_single(pl, g, rp) : build_forward(pl, g, rp));
     } else {
       memcpy(rp.in_lo, d3lo, sizeof d3lo);
       memcpy(rp.in_n, d3n, sizeof d3n);
@@ -872,7 +1034,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       memcpy(rp.out_n, d1n, sizeof d1n);
       rp.in_bytes = d3b;
       rp.out_bytes = d1b;
-      ST(build_inverse(pl, g, rp));
+      ST(P == 1 ? build_single(pl, g, rp) : build_inverse(pl, g, rp));
     }
     if (rp.ws_bytes) {
       cudaError_t e = cudaMalloc(&rp.ws, rp.ws_bytes);

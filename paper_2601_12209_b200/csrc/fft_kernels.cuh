@@ -22,6 +22,7 @@
 // from a closed form (unsegmented side) or from a per-t table (segmented side: t ranges
 // owned by different peers land in different send blocks / buffers).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -242,6 +243,15 @@ __device__ __forceinline__ C* side_ptr(const SideMap& m, int t, long long lidx) 
   return b + ((e.x & ((1LL << 62) - 1)) + lidx * e.y);
 }
 
+// Global store of one complex value from the last pass (DFFT_STORE_CS: streaming hint, dev A/B).
+template <typename C> __device__ __forceinline__ void st_out(C* p, C v) {
+#ifdef DFFT_STORE_CS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
+
 // Kernel arguments shared by both families.
 struct PassArgs {
   SideMap in, out;
@@ -283,7 +293,8 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
   }
   // every read of this pass is done before anything is overwritten (also makes a single-pass
   // transform safe in place)
-  if constexpr (P > 0 || LAST) __syncthreads();
+  if constexpr (P > 0 || LAST || IO::kSyncAfterLoad) __syncthreads();
+  if constexpr (P == 0 && IO::kSyncAfterLoad) io.after_load();  // e.g. refill the drained TMA stage
   // ---- twiddle, butterfly, scatter
 #pragma unroll
   for (int u = 0; u < NB; ++u) {
@@ -315,6 +326,8 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
 
 // ------------------------------------------------------------------ contiguous-axis family
 template <typename C> struct ContigIO {
+  static constexpr bool kSyncAfterLoad = false;
+  __device__ __forceinline__ void after_load() {}
   const C* __restrict__ in;
   C* __restrict__ out;
   const SideMap* mi;
@@ -377,18 +390,24 @@ template <typename Real, int N> struct StridedCfg {
   static constexpr int ES = (int)sizeof(Real) * 2;
   // W adjacent columns per CTA: 64-128 B row segments, at least 256 threads for short
   // lines, smem tile capped at 96 KB.
-  static constexpr int W0 = ES == 8 ? 8 : 4;
+#ifndef DFFT_STRIDED_W0
+#define DFFT_STRIDED_W0 64
+#endif
+  static constexpr int W0 = DFFT_STRIDED_W0 / ES;  // row segment bytes / element size
   static constexpr int Wthr = S.T * W0 >= 256 ? W0 : 256 / S.T;
   static constexpr int Wcap = (96 * 1024) / (N * ES) >= 1 ? (96 * 1024) / (N * ES) : 1;
   static constexpr int W = Wthr < Wcap ? Wthr : (Wcap >= 8 ? 8 : Wcap >= 4 ? 4 : Wcap >= 2 ? 2 : 1);
   static constexpr int THREADS = S.T * W;
-  // pad W/2 slots per R0 rows when a row is narrower than 128 B (tools/bank_sim.py)
-  static constexpr int PAD = (W * ES < 128) ? (W / 2 > 0 ? W / 2 : 1) : 0;
+  // pad W slots per R0 rows when a row is narrower than 128 B: 64-bit shared accesses resolve
+  // conflicts per half-warp, so rows b and b+1 must land 64 B apart mod 128 (tools/bank_sim.py)
+  static constexpr int PAD = (W * ES < 128) ? W : 0;
   static constexpr int R0 = S.rad[0];
   static constexpr int SMEM_ELEMS = N * W + (N / R0) * PAD;
 };
 
 template <typename C> struct StridedIO {
+  static constexpr bool kSyncAfterLoad = false;
+  __device__ __forceinline__ void after_load() {}
   const C* __restrict__ in;
   C* __restrict__ out;
   const SideMap* mi;
@@ -402,8 +421,8 @@ template <typename C> struct StridedIO {
   }
   __device__ __forceinline__ void store(int t, C v) const {
     if (scale != 1) { v.x *= scale; v.y *= scale; }
-    if (mo->ttab == nullptr) out[(long long)t * mo->tstride + cout] = v;
-    else side_ptr<C>(*mo, t, l1)[cout] = v;
+    if (mo->ttab == nullptr) st_out(out + ((long long)t * mo->tstride + cout), v);
+    else st_out(side_ptr<C>(*mo, t, l1) + cout, v);
   }
 };
 
@@ -436,6 +455,184 @@ fft_strided_kernel(const PassArgs a) {
   io.scale = (Real)a.scale;
   StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
   stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
+}
+
+// ------------------------------------------------------------------ strided family, TMA-staged
+// Persistent CTAs; each tile (W columns × N rows) is brought into shared memory by TMA
+// (cp.async.bulk.tensor, 3D box: 2W reals × BOXR rows × 1) into one of NS stages, completion
+// tracked by an mbarrier with expect_tx.  Pass 0 reads the stage, the stage is refilled with the
+// tile NS steps ahead right after (one elected thread), and the remaining passes run in a padded
+// work buffer — HBM reads stay in flight while the CTA computes.  Stores go from registers
+// through the SideMap (fused pack) as in the plain strided kernel.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const void* tmap, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tmap), "r"(c0),
+               "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+constexpr int largest_divisor_le(int n, int cap) {
+  for (int d = cap; d >= 1; --d)
+    if (n % d == 0) return d;
+  return 1;
+}
+
+template <typename Real, int N> struct TmaCfg {
+  static constexpr Sched S = make_sched(N);
+  static constexpr int ES = (int)sizeof(Real) * 2;
+  static constexpr int W0 = ES == 8 ? 8 : 4;  // 64 B row segments
+  static constexpr int W = S.T * W0 >= 256 ? W0 : 256 / S.T;
+  static constexpr int THREADS = S.T * W;
+  static constexpr int NS = 2;
+  static constexpr int BOXR = largest_divisor_le(N, 256);
+  static constexpr int NBOX = N / BOXR;
+  static constexpr int R0 = S.rad[0];
+  static constexpr int PAD = (W * ES < 128) ? W : 0;
+  static constexpr int STAGE_ELEMS = N * W;
+  static constexpr int WORK_ELEMS = N * W + (N / R0) * PAD;
+  static constexpr size_t SMEM = (size_t)(NS * STAGE_ELEMS + WORK_ELEMS) * ES + NS * 8 + 16;
+  static constexpr bool OK = S.npass >= 2 && THREADS <= 1024 && SMEM <= 227 * 1024 && 2 * W <= 256;
+};
+
+template <typename C, int W, bool TST> struct TmaIO : StridedIO<C> {
+  static constexpr bool kSyncAfterLoad = true;
+  const C* stage;  // this tile's stage buffer, dense [t][W]
+  C* obuf;         // TST: dense [t][W] output tile, written to HBM by a TMA store
+  int c;
+  // refill: thread 0 issues the TMA for the tile NS steps ahead into the drained stage
+  const void* tmap;
+  uint64_t* bar;
+  C* stage_ptr;
+  int next_c0, next_l1, nbox, boxr;
+  uint32_t bytes;
+  bool refill;
+  __device__ __forceinline__ C load(int t) const { return stage[t * W + c]; }
+  __device__ __forceinline__ void store(int t, C v) const {
+    if constexpr (TST) {
+      if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
+      obuf[t * W + c] = v;
+    } else {
+      StridedIO<C>::store(t, v);
+    }
+  }
+  __device__ __forceinline__ void after_load() {
+    if (refill && threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar, bytes);
+      for (int q = 0; q < nbox; ++q)
+        tma_load_3d(stage_ptr + q * boxr * W, tmap, next_c0, q * boxr, next_l1, bar);
+    }
+  }
+};
+
+// TST: the output side is unsegmented and written by TMA stores (omap) from the work buffer —
+// issuing 64 B row stores at a large stride from the SMs throttles the LSU (r01 ncu: lg_throttle).
+template <typename Real, int N, int DIR, bool TST>
+__global__ void __launch_bounds__(TmaCfg<Real, N>::THREADS)
+fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
+                       const PassArgs a) {
+  using C = typename CT<Real>::type;
+  using Cfg = TmaCfg<Real, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* stages = reinterpret_cast<C*>(smem_raw);
+  C* work = stages + Cfg::NS * Cfg::STAGE_ELEMS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(work + Cfg::WORK_ELEMS);
+  const int c = threadIdx.x % Cfg::W;
+  const int j = threadIdx.x / Cfg::W;
+  const long long ntile = (a.L0 + Cfg::W - 1) / Cfg::W;
+  const long long total = ntile * a.L1;
+  constexpr uint32_t kBytes = (uint32_t)(Cfg::STAGE_ELEMS * Cfg::ES);
+  // TMA coordinates are in reals: column c -> 2c
+  auto issue = [&](long long tile, int s) {
+    const long long l1 = tile / ntile;
+    const int c0 = (int)((tile - l1 * ntile) * Cfg::W * 2);
+    mbar_expect_tx(&bars[s], kBytes);
+    for (int q = 0; q < Cfg::NBOX; ++q)
+      tma_load_3d(stages + s * Cfg::STAGE_ELEMS + q * Cfg::BOXR * Cfg::W, &tmap, c0, q * Cfg::BOXR, (int)l1, &bars[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::NS; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < Cfg::NS; ++s) {
+      long long tile = blockIdx.x + (long long)s * gridDim.x;
+      if (tile < total) issue(tile, s);
+    }
+  }
+  __syncthreads();
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+    const int s = it % Cfg::NS;
+    const uint32_t parity = (uint32_t)((it / Cfg::NS) & 1);
+    const long long l1 = tile / ntile;
+    const long long l0 = (tile - l1 * ntile) * Cfg::W + c;
+    const bool active = l0 < a.L0;
+    if (TST && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
+    TmaIO<C, Cfg::W, TST> io;
+    io.obuf = work;
+    io.out = reinterpret_cast<C*>(a.out.base);
+    io.mo = &a.out;
+    io.l1 = l1;
+    io.cout = a.out.ttab == nullptr ? l0 + l1 * a.out.lstride : l0;
+    io.scale = (Real)a.scale;
+    io.stage = stages + s * Cfg::STAGE_ELEMS;
+    io.c = c;
+    const long long next = tile + (long long)Cfg::NS * gridDim.x;
+    io.refill = next < total;
+    io.tmap = &tmap;
+    io.bar = &bars[s];
+    io.stage_ptr = stages + s * Cfg::STAGE_ELEMS;
+    {
+      const long long nl1 = next / ntile;
+      io.next_l1 = (int)nl1;
+      io.next_c0 = (int)((next - nl1 * ntile) * Cfg::W * 2);
+    }
+    io.nbox = Cfg::NBOX;
+    io.boxr = Cfg::BOXR;
+    io.bytes = kBytes;
+    mbar_wait(&bars[s], parity);
+    StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
+    stockham_pass<C, N, DIR, 0>(io, sm, work, reinterpret_cast<const C*>(a.tw), j, active);
+    if constexpr (TST) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int c0 = (int)((tile - l1 * ntile) * Cfg::W * 2);
+        for (int q = 0; q < Cfg::NBOX; ++q) tma_store_3d(&omap, c0, q * Cfg::BOXR, (int)l1, work + q * Cfg::BOXR * Cfg::W);
+        bulk_commit();
+      }
+    }
+  }
+  if (TST && threadIdx.x == 0) bulk_wait0();
 }
 
 }  // namespace dfft

@@ -25,6 +25,15 @@ KernelInfo make_strided() {
   k.per_cta = Cfg::W;
   k.smem = Cfg::S.npass > 1 ? (size_t)Cfg::SMEM_ELEMS * sizeof(Real) * 2 : 0;
   k.twlen = sched_twlen(Cfg::S);
+  using TC = TmaCfg<Real, N>;
+  if constexpr (TC::OK) {
+    k.tma_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, false>;
+    k.tma_st_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, true>;
+    k.tma_threads = TC::THREADS;
+    k.tma_w = TC::W;
+    k.tma_boxr = TC::BOXR;
+    k.tma_smem = TC::SMEM;
+  }
   return k;
 }
 }  // namespace

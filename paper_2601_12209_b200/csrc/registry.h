@@ -16,6 +16,11 @@ struct KernelInfo {
   int per_cta = 0;       // contig: lines per CTA; strided: columns per CTA (W)
   size_t smem = 0;       // dynamic shared memory bytes
   int twlen = 0;         // twiddle table length (complex elements)
+  // strided family only: persistent TMA-staged variant (null if not instantiable for n)
+  const void* tma_fn = nullptr;
+  const void* tma_st_fn = nullptr;  // same, with TMA stores (unsegmented output side)
+  int tma_threads = 0, tma_w = 0, tma_boxr = 0;
+  size_t tma_smem = 0;
 };
 
 // Supported axis lengths: 2^a (2..4096), 3·2^a (3..3072), and the paper's

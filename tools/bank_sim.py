@@ -23,11 +23,19 @@ def schedule(n, dp):
 
 
 def wavefronts(words_per_lane):
-    banks = {}
-    for ws in words_per_lane:
-        for w in ws:
-            banks.setdefault(w % 32, set()).add(w)
-    return max(len(s) for s in banks.values())
+    """Accesses wider than 4 B are split into phases of 128 B worth of lanes (half-warps for
+    8 B, quarter-warps for 16 B, as measured by ncu on B200); within a phase the wavefront count
+    is the max number of distinct words on one bank."""
+    per = len(words_per_lane[0]) if words_per_lane else 1
+    lanes_per_phase = 32 // per
+    tot = 0
+    for p0 in range(0, len(words_per_lane), lanes_per_phase):
+        banks = {}
+        for ws in words_per_lane[p0:p0 + lanes_per_phase]:
+            for w in ws:
+                banks.setdefault(w % 32, set()).add(w)
+        tot += max(len(s) for s in banks.values())
+    return tot
 
 
 def sim(n, dp, fam, W=None, padshift=None):
@@ -66,7 +74,7 @@ def sim(n, dp, fam, W=None, padshift=None):
                             lanes.append([e * es // 4 + q for q in range(es // 4)])
                         if not lanes: continue
                         tot += wavefronts(lanes)
-                        ideal += max(1, len(lanes) * es // 128)
+                        ideal += max(1, (len(lanes) * es + 127) // 128)
         Ns *= R
     return tot / max(ideal, 1), rads, T
 
@@ -78,6 +86,6 @@ if __name__ == "__main__":
             for ps in (3, 4, 5):
                 res.append(("c%d" % ps, round(sim(n, dp, "contig", padshift=ps)[0], 2)))
             for W in ((4, 8) if dp else (8, 16)):
-                for pad in (0, W // 2, W):
+                for pad in (0, W // 2, W, 2 * W):
                     res.append(("s%d/%d" % (W, pad), round(sim(n, dp, "strided", W=W, padshift=pad)[0], 2)))
             print("dp" if dp else "sp", n, schedule(n, dp), res)

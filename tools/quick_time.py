@@ -42,3 +42,13 @@ es = 8 if prec == "f32" else 16
 hbm = 6 * N * es
 print(f"{shape} {prec}: fwd {tf:.3f} ms ({hbm / tf / 1e6:.0f} GB/s eff), fwd+inv {tfi:.3f} ms, "
       f"roundtrip err {((z - x).abs().pow(2).sum() / x.abs().pow(2).sum()).sqrt().item():.2e}")
+fwd.set_profiling(True)
+inv.set_profiling(True)
+fwd.phase_times()
+inv.phase_times()
+for _ in range(3):
+    fwd.execute(x, y)
+    inv.execute(y, z)
+pf, pi = fwd.phase_times(), inv.phase_times()
+print("  fwd " + " ".join(f"{k}={v[0] / 3:.3f}" for k, v in pf.items() if v[1]) +
+      " | inv " + " ".join(f"{k}={v[0] / 3:.3f}" for k, v in pi.items() if v[1]))
