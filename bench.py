@@ -45,6 +45,9 @@ def parse():
     p.add_argument("--grid-p", default="", help="process grid P1,P2 (default by N)")
     p.add_argument("--chunks", type=int, default=0)
     p.add_argument("--no-overlap", action="store_true")
+    p.add_argument("--exchange", default="ce", choices=["ce", "p2p", "nccl"],
+                   help="ce: copy engines into peers' IPC windows; p2p: FFT epilogues store into the windows; "
+                        "nccl: grouped send/recv")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=260112209 + 4)
@@ -205,9 +208,9 @@ def main():
     es = 8 if args.precision == "f32" else 16
     comm = dfft.Comm.create(nranks=world, rank=rank, device=local)
     fwd = dfft.Plan(comm, shape, args.strategy, grid, dt, dfft.FORWARD, chunks=args.chunks,
-                    overlap=not args.no_overlap)
+                    overlap=not args.no_overlap, exchange=args.exchange)
     inv = dfft.Plan(comm, shape, args.strategy, grid, dt, dfft.INVERSE, chunks=args.chunks,
-                    overlap=not args.no_overlap)
+                    overlap=not args.no_overlap, exchange=args.exchange)
     lo, n = fwd.box(0)
     x = fwd.alloc_in()
     inputs.fill_box_cuda(x, args.seed, shape, lo, n, True)
@@ -341,6 +344,7 @@ def main():
             "config": {"workload": f"{shape[0]}x{shape[1]}x{shape[2]} complex{'64' if es == 8 else '128'} c2c "
                                    f"{args.strategy} {grid[0]}x{grid[1]} fwd+inv",
                        "grid": list(shape), "proc_grid": list(grid), "chunks": fwd.chunks(),
+                       "exchange": args.exchange if world > 1 else "none",
                        "overlap": not args.no_overlap,
                        "l2": f"inputs larger than L2 ({Nloc * es / 2**30:.2f} GiB per GPU)"
                              if Nloc * es > 2 * 126e6 else "inputs L2-resident (flagged)",

@@ -70,9 +70,21 @@ typedef enum { DFFT_FORWARD = -1, DFFT_INVERSE = 1 } dfft_direction_t;
  *   DFFT_FLAG_NO_OVERLAP: one stream, each exchange completes before the next stage starts
  *             (the "SimpleMPIFFT" static-barrier ablation of P:438).  Results are bitwise
  *             identical to the pipelined schedule.
+ *   Exchange transport for P > 1 (same kernels and bitwise-identical results in every mode):
+ *     default:  the FFT epilogue packs each off-rank block into a local send block and the
+ *               copy engine of the comm stream writes it into the receiving peer's workspace
+ *               (a CUDA IPC window exchanged at plan creation) over NVLink; flag words in the
+ *               windows (system-scope release stores, cuStreamWaitValue32) order producer and
+ *               consumer per chunk.  No SM time is spent on transfers.
+ *     DFFT_FLAG_FUSED_STORE: the FFT epilogue stores each off-rank element straight into the
+ *               peer's window (no send block; the exchange is inside the FFT kernel).
+ *     DFFT_FLAG_NCCL: grouped ncclSend/ncclRecv of the send blocks (baseline/ablation).
+ *   Env DFFT_EXCHANGE=ce|p2p|nccl overrides.
  */
 #define DFFT_FLAG_CHUNKS(k) ((uint64_t)((k) & 0xff))
 #define DFFT_FLAG_NO_OVERLAP ((uint64_t)1 << 8)
+#define DFFT_FLAG_NCCL ((uint64_t)1 << 9)
+#define DFFT_FLAG_FUSED_STORE ((uint64_t)1 << 10)
 
 int dfft_version(void);
 const char* dfft_status_string(dfft_status_t status);

@@ -144,7 +144,6 @@ bool g_use_tma = getenv("DFFT_NO_TMA") == nullptr;  // env switch for the A/B ab
 CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
                                      : getenv("DFFT_TMA_PROMO128") ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
-bool g_oop_z = getenv("DFFT_OOP_Z") != nullptr;  // dev: P=1 forward z-stage out of place
 bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
 
 dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
@@ -172,17 +171,19 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // ------------------------------------------------------------------------------ plan data
-enum RefKind { kNone = 0, kUserIn = 1, kUserOut = 2, kWs = 3 };
+enum RefKind { kNone = 0, kUserIn = 1, kUserOut = 2, kWs = 3, kPeer = 4 };
 struct Ref {
   int kind = kNone;
   long long off = 0;  // bytes
+  int peer = -1;      // kPeer: global rank whose workspace (IPC window) this points into
 };
 
 struct Stage {
   int family = 0, n = 0, es = 8;
   KernelInfo k;
   PassArgs a{};
-  Ref in, in1, out, out1;
+  Ref in, out;
+  std::vector<Ref> in_bases, out_bases;  // table selector -> base (segmented sides)
   void* in_tab = nullptr;  // device longlong2[n] or null
   void* out_tab = nullptr;
   long long grid = 0;
@@ -194,11 +195,15 @@ struct Xfer {
   int peer;
   Ref ref;
   size_t bytes;
+  Ref remote;  // CE mode (sends): the receiver's address, a kPeer reference into its window
+  // CE mode: 2D copy (height rows of width bytes; source / destination pitches), height 1 = 1D
+  size_t width = 0, height = 1, spitch = 0, dpitch = 0;
 };
 struct Exchange {
   int comm = 0;  // 0 = row (P1 group), 1 = column (P2 group)
-  std::vector<Xfer> sends, recvs;
-  bool empty() const { return sends.empty() && recvs.empty(); }
+  std::vector<Xfer> sends, recvs;     // NCCL mode: the blocks to move
+  std::vector<int> peers;             // P2P mode: global ranks of the other group members
+  bool empty() const { return sends.empty() && recvs.empty() && peers.empty(); }
 };
 
 struct RankPlan {
@@ -233,6 +238,13 @@ struct dfft_plan_s {
   std::vector<cudaEvent_t> evA, evE1, evB, evE2;
   void* stage_in = nullptr;  // dfft_execute_host staging buffers
   void* stage_out = nullptr;
+  // P2P exchange (default for P > 1): every rank's workspace is an IPC window; the FFT epilogues
+  // store straight into the peers' receive regions over NVLink; flags in the windows order it
+  bool p2p = false;
+  bool ce = false;                   // copy-engine exchange (cudaMemcpyAsync into the peers' windows)
+  std::vector<void*> peer_ws;        // by global rank (own rank = own workspace), null if not a peer
+  size_t flag_off = 0;               // byte offset of the flag block in every workspace
+  unsigned int epoch = 0;            // executes so far (flag values)
   // per-phase profiling (dfft_plan_set_profiling): timing events around every stage launch
   // and exchange, on the stream that runs it; accumulated by dfft_plan_phase_times
   bool prof = false;
@@ -252,35 +264,65 @@ dfft_status_t upload_table(const std::vector<longlong2>& h, void** d) {
   return DFFT_SUCCESS;
 }
 
-// table entry: {sel<<62 | element offset, line stride}
-inline longlong2 tent(int sel, long long off, long long lstr) {
-  longlong2 e;
-  e.x = ((long long)sel << 62) | off;
-  e.y = lstr;
-  return e;
+// Affine segment of a side: t ∈ [tlo, tlo+tn) lives at bases[sel] + off0 + (t−tlo)·ts + l0·s0 + l1·s1.
+struct Seg {
+  int sel;
+  long long tlo, tn, off0, ts, s0, s1;
+};
+using Segs = std::vector<Seg>;
+
+// per-t table {sel<<56 | off(t), s0 | s1<<32} (the kernel's SegEnt)
+std::vector<longlong2> seg_table(const Segs& segs, long long n) {
+  std::vector<longlong2> tab(n);
+  for (const Seg& q : segs)
+    for (long long t = q.tlo; t < q.tlo + q.tn; ++t) {
+      longlong2 e;
+      e.x = ((long long)q.sel << 56) | (q.off0 + (t - q.tlo) * q.ts);
+      e.y = (long long)((unsigned long long)(unsigned int)q.s0 | ((unsigned long long)(unsigned int)q.s1 << 32));
+      tab[t] = e;
+    }
+  return tab;
 }
 
-// A segmented side whose table is a single affine segment (one owner, e.g. P2 == 1) becomes an
-// unsegmented side: base += toff(0), tstride = toff(1) - toff(0), lstride = lstr.
-bool linearize(const std::vector<longlong2>& tab, Ref& base, const Ref& base1, SideMap& m, long long es, bool unit_t) {
-  const long long mask = (1LL << 62) - 1;
-  const long long sel = tab[0].x >> 62, off0 = tab[0].x & mask, lstr = tab[0].y;
-  const long long ts = tab.size() > 1 ? (tab[1].x & mask) - off0 : 1;
-  if (unit_t && ts != 1) return false;
-  for (size_t t = 0; t < tab.size(); ++t)
-    if ((tab[t].x >> 62) != sel || (tab[t].x & mask) != off0 + (long long)t * ts || tab[t].y != lstr) return false;
-  Ref b = sel ? base1 : base;
-  b.off += off0 * es;
+// One segment covering all t (one owner, e.g. P2 == 1), or adjacent segments that happen to be
+// one affine map, make the side unsegmented: no table, closed-form addressing.
+bool linearize(const Segs& segs, long long n, Ref& base, const std::vector<Ref>& bases, SideMap& m, long long es) {
+  if (segs.empty()) return false;
+  const Seg& f = segs[0];
+  for (const Seg& q : segs)
+    if (q.sel != f.sel || q.s0 != f.s0 || q.s1 != f.s1 || q.ts != f.ts || q.off0 != f.off0 + (q.tlo - f.tlo) * f.ts)
+      return false;
+  (void)n;
+  Ref b = bases[f.sel];
+  b.off += (f.off0 - f.tlo * f.ts) * es;
   base = b;
-  m.tstride = ts;
-  m.lstride = lstr;
+  m.tstride = f.ts;
+  m.s0 = f.s0;
+  m.s1 = f.s1;
   return true;
 }
 
+inline void set_side(SideMap& m, long long ts, long long s0, long long s1) {
+  m.tstride = ts;
+  m.s0 = s0;
+  m.s1 = s1;
+}
+
 dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long long L0, long long L1,
-                           const std::vector<longlong2>* in_tab, const std::vector<longlong2>* out_tab) {
-  if (in_tab && linearize(*in_tab, s.in, s.in1, s.a.in, (long long)pl->es, family == kContig)) in_tab = nullptr;
-  if (out_tab && linearize(*out_tab, s.out, s.out1, s.a.out, (long long)pl->es, family == kContig)) out_tab = nullptr;
+                           const Segs* in_segs, const Segs* out_segs) {
+  if (s.in_bases.empty()) s.in_bases = {s.in};
+  if (s.out_bases.empty()) s.out_bases = {s.out};
+  if (s.in_bases.size() > (size_t)kMaxBases || s.out_bases.size() > (size_t)kMaxBases)
+    return fail(DFFT_ERR_UNSUPPORTED, "more than %d segment bases", kMaxBases);
+  if (in_segs && linearize(*in_segs, n, s.in, s.in_bases, s.a.in, (long long)pl->es)) in_segs = nullptr;
+  if (out_segs && linearize(*out_segs, n, s.out, s.out_bases, s.a.out, (long long)pl->es)) out_segs = nullptr;
+  if (family == kContig && ((!in_segs && s.a.in.tstride != 1) || (!out_segs && s.a.out.tstride != 1)))
+    return fail(DFFT_ERR_INTERNAL, "contig stage with a non-unit t-stride side");
+  std::vector<longlong2> in_tab_h, out_tab_h;
+  if (in_segs) in_tab_h = seg_table(*in_segs, n);
+  if (out_segs) out_tab_h = seg_table(*out_segs, n);
+  const std::vector<longlong2>* in_tab = in_segs ? &in_tab_h : nullptr;
+  const std::vector<longlong2>* out_tab = out_segs ? &out_tab_h : nullptr;
   s.family = family;
   s.n = n;
   s.es = (int)pl->es;
@@ -294,14 +336,14 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw));
   if (in_tab) ST(upload_table(*in_tab, &s.in_tab));
   if (out_tab) ST(upload_table(*out_tab, &s.out_tab));
-  s.a.in.ttab = (const longlong2*)s.in_tab;
-  s.a.out.ttab = (const longlong2*)s.out_tab;
+  s.a.in.ttab = (const SegEnt*)s.in_tab;
+  s.a.out.ttab = (const SegEnt*)s.out_tab;
   if (family == kContig) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
   else s.grid = ((L0 + s.k.per_cta - 1) / s.k.per_cta) * L1;
   if (s.grid >= (1LL << 31)) return fail(DFFT_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", s.grid);
   if (family == kStrided && s.k.tma_fn && g_use_tma && !in_tab && tensor_map_encoder()) {
     const long long es = (long long)pl->es;
-    bool ok = (s.a.in.tstride * es) % 16 == 0 && (L1 == 1 || (s.a.in.lstride * es) % 16 == 0) &&
+    bool ok = s.a.in.s0 == 1 && (s.a.in.tstride * es) % 16 == 0 && (L1 == 1 || (s.a.in.s1 * es) % 16 == 0) &&
               2 * L0 < (1LL << 32) && L1 < (1LL << 31);
     if (ok) {
       int occ = 0, dev = pl->comm->device, sms = 0;
@@ -332,170 +374,252 @@ struct Geo {
   long long x0(long long i, long long k) const { return blo(Xn(i), K, k); }
 };
 
-// Forward plan of one rank (all offsets in complex elements unless named *_b).
+// Group members as global ranks: row group = same j (index i'), column group = same i (index j').
+inline int row_rank(const Geo& g, long long ip, long long j) { return (int)(ip * g.P2 + j); }
+inline int col_rank(const Geo& g, long long i, long long jp) { return (int)(i * g.P2 + jp); }
+
+// Flag block at the end of every workspace (CE / fused modes): uint32 ready[2][K][P], done[2][K][P].
+// ready[e][k][src] is written by src into the consumer's window once its chunk-k blocks have
+// landed there; done[e][k][dst] is written by the consumer dst into the producer's window once
+// it has finished reading (so the next execute may overwrite).
+inline size_t flag_bytes(const Geo& g) { return (size_t)4 * 2 * 2 * g.K * g.P1 * g.P2; }
+
+// Workspace layouts (complex elements) of rank (i, j); every rank can compute any other rank's
+// layout, which is how senders address the receivers' windows.
+//   forward  NCCL: [S1 send1 | R1 recv1 [y][zc][x] per chunk | S2 send2]     (E2 lands in `out`)
+//            CE:   [S1 send1 | R1 recv1 [zc][y][x] per chunk | S2 send2 | R2 [y'][z][x]]
+//            P2P:  [R1 recv1 [zc][y][x] per chunk | R2 [y'][z][x]]           (no send blocks)
+//   inverse  NCCL/CE: [S2' | R2' [y][z][xc] per chunk | S1' | R1' blocks by (source row, chunk)]
+//            P2P:  [R2' | R1']
+// CE/P2P layouts put the FFT axis of the *consumer* at a small stride, so no stage both reads
+// and writes at a large stride (such a stage ran at 2.3 TB/s vs 4.6-6 TB/s).
+struct FwdLayout {
+  long long S1, R1, S2, R2, end;
+};
+FwdLayout fwd_layout(const Geo& g, long long i, long long j, int mode /*0 nccl 1 ce 2 p2p*/) {
+  FwdLayout L{};
+  const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
+  const long long S1n = mode == 2 ? 0 : Y1n * Zn * (g.nxc - Xn);
+  const long long S2n = mode == 2 ? 0 : Zn * Xn * (g.ny - Y3n);
+  L.S1 = 0;
+  L.R1 = S1n;
+  L.S2 = L.R1 + g.ny * Zn * Xn;
+  L.R2 = L.S2 + S2n;
+  L.end = L.R2 + (mode == 0 ? 0 : g.nz * Y3n * Xn);
+  return L;
+}
+struct InvLayout {
+  long long S2, R2, S1, R1, end;
+};
+InvLayout inv_layout(const Geo& g, long long i, long long j, int mode) {
+  InvLayout L{};
+  const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
+  L.S2 = 0;
+  L.R2 = mode == 2 ? 0 : Y3n * Xn * (g.nz - Zn);
+  L.S1 = L.R2 + g.ny * Zn * Xn;
+  L.R1 = L.S1 + (mode == 2 ? 0 : Zn * Xn * (g.ny - Y1n));
+  L.end = L.R1 + g.nxc * Y1n * Zn;
+  return L;
+}
+
+int exch_mode(dfft_plan_t pl) { return pl->p2p ? 2 : pl->ce ? 1 : 0; }
+
+void add_flags(dfft_plan_t pl, const Geo& g, RankPlan& rp, long long end_elems) {
+  rp.ws_bytes = (size_t)end_elems * pl->es;
+  if (pl->p2p || pl->ce) {
+    pl->flag_off = (rp.ws_bytes + 255) / 256 * 256;
+    rp.ws_bytes = pl->flag_off + flag_bytes(g);
+  }
+}
+
+// Forward plan of one rank: x-FFT (D1 in) → T1 → y-FFT → T2 → z-FFT (D3 out).
 dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long i = rp.i, j = rp.j, K = g.K, es = (long long)pl->es;
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
-  // workspace: [S1 send1][R1 recv1][S2 send2]
-  const long long S1 = 0, S1n = Y1n * Zn * (g.nxc - Xn);
-  const long long R1 = S1 + S1n, R1n = g.ny * Zn * Xn;
-  const long long S2 = R1 + R1n, S2n = Zn * Xn * (g.ny - Y3n);
-  rp.ws_bytes = (size_t)(S2 + S2n) * es;
-  if (g_oop_z && g.P1 == 1 && g.P2 == 1) rp.ws_bytes = std::max<size_t>(rp.ws_bytes, (size_t)(g.nxc * g.ny * g.nz * es));
-  auto s1off = [&](long long k, long long ip) {
+  const int mode = exch_mode(pl);
+  const bool nccl = mode == 0, ce = mode == 1, p2p = mode == 2;
+  const FwdLayout L = fwd_layout(g, i, j, mode);
+  add_flags(pl, g, rp, L.end);
+  auto s1off = [&](long long k, long long ip) {  // send1 block (k, i'): [zz][y][x_i'] (NCCL: [y][zz][x])
     long long acc = 0;
     for (long long q = 0; q < ip; ++q)
       if (q != i) acc += g.Xn(q);
-    return S1 + Y1n * (g.z0(j, k) * (g.nxc - Xn) + g.zc(j, k) * acc);
+    return L.S1 + Y1n * (g.z0(j, k) * (g.nxc - Xn) + g.zc(j, k) * acc);
   };
-  auto s2off = [&](long long k, long long jp) {
+  auto s2off = [&](long long k, long long jp) {  // send2 block (k, j'): NCCL [zz][y'][x], CE [y'][zz][x]
     long long acc = 0;
     for (long long q = 0; q < jp; ++q)
       if (q != j) acc += g.Y3n(q);
-    return S2 + Xn * (g.z0(j, k) * (g.ny - Y3n) + g.zc(j, k) * acc);
+    return L.S2 + Xn * (g.z0(j, k) * (g.ny - Y3n) + g.zc(j, k) * acc);
   };
-  const long long in_es = pl->r2c ? es / 2 : es;  // bytes of one input element
-  // P = 1 variant: A writes the transposed buffer into `out`, B writes natural order into the
-  // workspace, C runs out of place workspace -> `out` (dev switch DFFT_OOP_Z)
-  const bool oop = g_oop_z && g.P1 == 1 && g.P2 == 1;
+  const long long nxl = pl->r2c ? g.nx / 2 : g.nx;  // input line length in (complex) elements
+  const long long in_es = pl->r2c ? es / 2 : es;
   rp.A.resize(K);
   rp.B.resize(K);
   rp.E1.resize(K);
   rp.E2.resize(K);
   for (long long k = 0; k < K; ++k) {
     const long long zc = g.zc(j, k), z0 = g.z0(j, k);
-    // ---- stage A: x-FFT of lines (y, zz); out segmented by x-owner i'
+    // ---- stage A: x-FFT of lines (l0 = y, l1 = zz); out segmented by x-owner i'
     Stage& A = rp.A[k];
     A.in = {kUserIn, z0 * Y1n * g.nx * in_es};
-    A.a.in.tstride = 1;
-    A.a.in.lstride = pl->r2c ? g.nx / 2 : g.nx;
-    A.a.in_l0s = 1;
-    A.a.in_l1s = Y1n;
-    A.out = {oop ? kUserOut : kWs, 0};
-    A.a.out_l0s = zc;  // Lidx = y·zc + zz
-    A.a.out_l1s = 1;
-    std::vector<longlong2> ot(g.nxc);
-    for (long long t = 0; t < g.nxc; ++t) {
-      long long ip = owner(t, g.nxc, g.P1), tl = t - g.Xlo(ip);
-      if (ip == i) ot[t] = tent(0, R1 + g.ny * z0 * Xn + g.Y1lo(i) * zc * Xn + tl, Xn);
-      else ot[t] = tent(0, s1off(k, ip) + tl, g.Xn(ip));
+    set_side(A.a.in, 1, nxl, Y1n * nxl);
+    A.out = {kWs, 0};
+    A.out_bases.push_back({kWs, 0});
+    if (p2p)  // selector 1 + i' = rank (i', j)'s window (own window for i' == i)
+      for (long long ip = 0; ip < g.P1; ++ip) A.out_bases.push_back({kPeer, 0, row_rank(g, ip, j)});
+    Segs aseg;
+    for (long long ip = 0; ip < g.P1; ++ip) {
+      const long long xl = g.Xlo(ip), xn = g.Xn(ip);
+      if (p2p) {
+        const FwdLayout Lr = fwd_layout(g, ip, j, mode);
+        aseg.push_back({1 + (int)ip, xl, xn, Lr.R1 + g.ny * z0 * xn + g.Y1lo(i) * xn, 1, xn, g.ny * xn});
+      } else if (ip == i) {
+        if (nccl) aseg.push_back({0, xl, xn, L.R1 + g.ny * z0 * Xn + g.Y1lo(i) * zc * Xn, 1, zc * Xn, Xn});
+        else aseg.push_back({0, xl, xn, L.R1 + g.ny * z0 * Xn + g.Y1lo(i) * Xn, 1, Xn, g.ny * Xn});
+      } else {
+        if (nccl) aseg.push_back({0, xl, xn, s1off(k, ip), 1, zc * xn, xn});
+        else aseg.push_back({0, xl, xn, s1off(k, ip), 1, xn, Y1n * xn});
+      }
     }
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, kContig, (int)(pl->r2c ? g.nx / 2 : g.nx), Y1n, zc, nullptr, &ot));
+    ST(finish_stage(pl, A, kContig, (int)nxl, Y1n, zc, nullptr, &aseg));
     // ---- exchange 1 (row group)
     Exchange& E1 = rp.E1[k];
     E1.comm = 0;
     for (long long ip = 0; ip < g.P1; ++ip) {
       if (ip == i) continue;
-      E1.sends.push_back({(int)ip, {kWs, s1off(k, ip) * es}, (size_t)(Y1n * zc * g.Xn(ip) * es)});
-      E1.recvs.push_back({(int)ip, {kWs, (R1 + g.ny * z0 * Xn + g.Y1lo(ip) * zc * Xn) * es},
+      if (!nccl) E1.peers.push_back(row_rank(g, ip, j));
+      if (p2p) continue;
+      const long long xn = g.Xn(ip);
+      Xfer x{(int)ip, {kWs, s1off(k, ip) * es}, (size_t)(Y1n * zc * xn * es)};
+      if (ce) {  // zc rows of Y1n·xn elements into [zz][y][x] of the receiver
+        const FwdLayout Lr = fwd_layout(g, ip, j, mode);
+        x.remote = {kPeer, (Lr.R1 + g.ny * z0 * xn + g.Y1lo(i) * xn) * es, row_rank(g, ip, j)};
+        x.width = (size_t)(Y1n * xn * es);
+        x.height = (size_t)zc;
+        x.spitch = x.width;
+        x.dpitch = (size_t)(g.ny * xn * es);
+      }
+      E1.sends.push_back(x);
+      E1.recvs.push_back({(int)ip, {kWs, (L.R1 + g.ny * z0 * Xn + g.Y1lo(ip) * zc * Xn) * es},
                           (size_t)(g.Y1n(ip) * zc * Xn * es)});
     }
-    // ---- stage B: y-FFT of columns (x, zz) of recv1 chunk k; out segmented by y-owner j'
+    // ---- stage B: y-FFT of columns (l0 = x, l1 = zz) of recv1 chunk k; out segmented by y-owner j'
     Stage& B = rp.B[k];
-    B.in = {oop ? kUserOut : kWs, (R1 + g.ny * z0 * Xn) * es};
-    B.a.in.tstride = zc * Xn;
-    B.a.in.lstride = Xn;
+    B.in = {kWs, (L.R1 + g.ny * z0 * Xn) * es};
+    if (nccl) set_side(B.a.in, zc * Xn, 1, Xn);
+    else set_side(B.a.in, Xn, 1, g.ny * Xn);
     B.out = {kWs, 0};
-    B.out1 = {oop ? kWs : kUserOut, 0};
-    std::vector<longlong2> bt(g.ny);
-    for (long long t = 0; t < g.ny; ++t) {
-      long long jp = owner(t, g.ny, g.P2), tl = t - g.Y3lo(jp);
-      if (jp == j) bt[t] = tent(1, (g.Zlo(j) + z0) * Y3n * Xn + tl * Xn, Y3n * Xn);
-      else bt[t] = tent(0, s2off(k, jp) + tl * Xn, g.Y3n(jp) * Xn);
+    B.out_bases.push_back({kWs, 0});
+    B.out_bases.push_back({kUserOut, 0});
+    if (p2p)  // selector 2 + j' = rank (i, j')'s window
+      for (long long jp = 0; jp < g.P2; ++jp) B.out_bases.push_back({kPeer, 0, col_rank(g, i, jp)});
+    Segs bseg;
+    for (long long jp = 0; jp < g.P2; ++jp) {
+      const long long yl = g.Y3lo(jp), yn = g.Y3n(jp);
+      if (p2p) {
+        const FwdLayout Lr = fwd_layout(g, i, jp, mode);
+        bseg.push_back({2 + (int)jp, yl, yn, Lr.R2 + (g.Zlo(j) + z0) * Xn, g.nz * Xn, 1, Xn});
+      } else if (jp == j) {
+        if (nccl) bseg.push_back({1, yl, yn, (g.Zlo(j) + z0) * Y3n * Xn, Xn, 1, Y3n * Xn});
+        else bseg.push_back({0, yl, yn, L.R2 + (g.Zlo(j) + z0) * Xn, g.nz * Xn, 1, Xn});
+      } else {
+        if (nccl) bseg.push_back({0, yl, yn, s2off(k, jp), Xn, 1, yn * Xn});
+        else bseg.push_back({0, yl, yn, s2off(k, jp), zc * Xn, 1, Xn});
+      }
     }
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, kStrided, (int)g.ny, Xn, zc, nullptr, &bt));
-    // ---- exchange 2 (column group): peers' chunk k lands in `out` at its z offset
+    ST(finish_stage(pl, B, kStrided, (int)g.ny, Xn, zc, nullptr, &bseg));
+    // ---- exchange 2 (column group)
     Exchange& E2 = rp.E2[k];
     E2.comm = 1;
     for (long long jp = 0; jp < g.P2; ++jp) {
       if (jp == j) continue;
-      E2.sends.push_back({(int)jp, {kWs, s2off(k, jp) * es}, (size_t)(zc * g.Y3n(jp) * Xn * es)});
+      if (!nccl) E2.peers.push_back(col_rank(g, i, jp));
+      if (p2p) continue;
+      const long long yn = g.Y3n(jp);
+      Xfer x{(int)jp, {kWs, s2off(k, jp) * es}, (size_t)(zc * yn * Xn * es)};
+      if (ce) {  // yn rows of zc·Xn elements into [y'][z][x] of the receiver
+        const FwdLayout Lr = fwd_layout(g, i, jp, mode);
+        x.remote = {kPeer, (Lr.R2 + (g.Zlo(j) + z0) * Xn) * es, col_rank(g, i, jp)};
+        x.width = (size_t)(zc * Xn * es);
+        x.height = (size_t)yn;
+        x.spitch = x.width;
+        x.dpitch = (size_t)(g.nz * Xn * es);
+      }
+      E2.sends.push_back(x);
       E2.recvs.push_back({(int)jp, {kUserOut, (g.Zlo(jp) + g.z0(jp, k)) * Y3n * Xn * es},
                           (size_t)(g.zc(jp, k) * Y3n * Xn * es)});
     }
   }
-  // ---- stage C: z-FFT in place on `out`
+  // ---- stage C: z-FFT of columns (l0 = x, l1 = y'): in place on `out` (NCCL), R2 -> `out` (CE/P2P)
   Stage& C = rp.C;
-  C.in = {oop ? kWs : kUserOut, 0};
   C.out = {kUserOut, 0};
-  C.a.in.tstride = C.a.out.tstride = Y3n * Xn;
-  C.a.in.lstride = C.a.out.lstride = Xn;
+  set_side(C.a.out, Y3n * Xn, 1, Xn);
+  if (nccl) {
+    C.in = {kUserOut, 0};
+    set_side(C.a.in, Y3n * Xn, 1, Xn);
+  } else {
+    C.in = {kWs, L.R2 * es};
+    set_side(C.a.in, Xn, 1, g.nz * Xn);
+  }
   C.a.scale = 1.0;
   ST(finish_stage(pl, C, kStrided, (int)g.nz, Xn, Y3n, nullptr, nullptr));
   return DFFT_SUCCESS;
 }
 
 // Single GPU (P = 1, any decomposition): no exchange, so the axis order is free (the 3D DFT is
-// separable).  Order the stages so every stage writes at a small stride (large-stride stores
-// throttle a pass; large-stride loads do not — r01 measurements):
+// separable).  Order the stages so no stage both reads and writes at a large stride:
 //   forward: x (in -> out, natural), z (out -> ws as [y][z][x]), y (ws -> out, natural)
 //   inverse: y (in -> out, natural), z (out -> ws as [y][z][x]), x (ws -> out, natural, ×1/N)
 dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
+  const long long nxl = pl->r2c ? nx / 2 : nx;
   rp.ws_bytes = (size_t)(nxc * ny * nz * es);
   rp.A.resize(1);
   rp.B.resize(1);
   rp.E1.resize(1);
   rp.E2.resize(1);
   Stage &A = rp.A[0], &B = rp.B[0], &C = rp.C;
-  // z-pass: natural [z][y][x] -> ws [y][z][x]
+  // z-pass, columns (l0 = x, l1 = y): natural [z][y][x] -> ws [y][z][x]
   auto zpass = [&](Stage& Z) -> dfft_status_t {
     Z.in = {kUserOut, 0};
-    Z.a.in.tstride = ny * nxc;
-    Z.a.in.lstride = nxc;
+    set_side(Z.a.in, ny * nxc, 1, nxc);
     Z.out = {kWs, 0};
-    Z.a.out.tstride = nxc;
-    Z.a.out.lstride = nz * nxc;
+    set_side(Z.a.out, nxc, 1, nz * nxc);
     Z.a.scale = 1.0;
     return finish_stage(pl, Z, kStrided, (int)nz, nxc, ny, nullptr, nullptr);
   };
   if (pl->dir == DFFT_FORWARD) {
-    A.in = {kUserIn, 0};
-    A.a.in.tstride = 1;
-    A.a.in.lstride = pl->r2c ? nx / 2 : nx;
-    A.a.in_l0s = 1;
-    A.a.in_l1s = ny;
+    A.in = {kUserIn, 0};  // lines (l0 = y, l1 = z)
+    set_side(A.a.in, 1, nxl, ny * nxl);
     A.out = {kUserOut, 0};
-    A.a.out.tstride = 1;
-    A.a.out.lstride = nxc;
-    A.a.out_l0s = 1;
-    A.a.out_l1s = ny;
+    set_side(A.a.out, 1, nxc, ny * nxc);
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, kContig, (int)(pl->r2c ? nx / 2 : nx), ny, nz, nullptr, nullptr));
+    ST(finish_stage(pl, A, kContig, (int)nxl, ny, nz, nullptr, nullptr));
     ST(zpass(B));
-    C.in = {kWs, 0};
-    C.a.in.tstride = nz * nxc;
-    C.a.in.lstride = nxc;
+    C.in = {kWs, 0};  // columns (l0 = x, l1 = z)
+    set_side(C.a.in, nz * nxc, 1, nxc);
     C.out = {kUserOut, 0};
-    C.a.out.tstride = nxc;
-    C.a.out.lstride = ny * nxc;
+    set_side(C.a.out, nxc, 1, ny * nxc);
     C.a.scale = 1.0;
     ST(finish_stage(pl, C, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
   } else {
     if (pl->r2c) return fail(DFFT_ERR_UNSUPPORTED, "C2R single-GPU path not built yet");
-    A.in = {kUserIn, 0};
-    A.a.in.tstride = nxc;
-    A.a.in.lstride = ny * nxc;
+    A.in = {kUserIn, 0};  // columns (l0 = x, l1 = z)
+    set_side(A.a.in, nxc, 1, ny * nxc);
     A.out = {kUserOut, 0};
-    A.a.out.tstride = nxc;
-    A.a.out.lstride = ny * nxc;
+    set_side(A.a.out, nxc, 1, ny * nxc);
     A.a.scale = 1.0;
     ST(finish_stage(pl, A, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
     ST(zpass(B));
-    C.in = {kWs, 0};
-    C.a.in.tstride = 1;
-    C.a.in.lstride = nxc;
-    C.a.in_l0s = nz;  // line (y, z) of ws [y][z][x] is y·nz + z
-    C.a.in_l1s = 1;
+    C.in = {kWs, 0};  // lines (l0 = y, l1 = z) of ws [y][z][x]
+    set_side(C.a.in, 1, nz * nxc, nxc);
     C.out = {kUserOut, 0};
-    C.a.out.tstride = 1;
-    C.a.out.lstride = pl->r2c ? nx / 2 : nx;
-    C.a.out_l0s = 1;
-    C.a.out_l1s = ny;
+    set_side(C.a.out, 1, nxl, ny * nxl);
     C.a.scale = 1.0 / ((double)nx * (double)ny * (double)nz);
-    ST(finish_stage(pl, C, kContig, (int)(pl->r2c ? nx / 2 : nx), ny, nz, nullptr, nullptr));
+    ST(finish_stage(pl, C, kContig, (int)nxl, ny, nz, nullptr, nullptr));
   }
   return DFFT_SUCCESS;
 }
@@ -504,116 +628,150 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
 dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long i = rp.i, j = rp.j, K = g.K, es = (long long)pl->es;
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
-  // workspace: [S2' send][R2' recv][S1' send][R1' recv]
-  const long long S2 = 0, S2n = Y3n * Xn * (g.nz - Zn);
-  const long long R2 = S2 + S2n, R2n = g.ny * Zn * Xn;
-  const long long S1 = R2 + R2n, S1n = Zn * Xn * (g.ny - Y1n);
-  const long long R1 = S1 + S1n, R1n = g.nxc * Y1n * Zn;
-  rp.ws_bytes = (size_t)(R1 + R1n) * es;
-  auto s2off = [&](long long k, long long jp) {
+  const int mode = exch_mode(pl);
+  const bool nccl = mode == 0, ce = mode == 1, p2p = mode == 2;
+  const InvLayout L = inv_layout(g, i, j, mode);
+  add_flags(pl, g, rp, L.end);
+  auto s2off = [&](long long k, long long jp) {  // send2' block (k, j'): [y'][z ∈ Z_j'][xc]
     long long acc = 0;
     for (long long q = 0; q < jp; ++q)
       if (q != j) acc += g.Zn(q);
-    return S2 + Y3n * (g.x0(i, k) * (g.nz - Zn) + g.xc(i, k) * acc);
+    return L.S2 + Y3n * (g.x0(i, k) * (g.nz - Zn) + g.xc(i, k) * acc);
   };
-  auto s1off = [&](long long k, long long ip) {
+  auto s1off = [&](long long k, long long ip) {  // send1' block (k, i'): [z][y ∈ Y1_i'][xc]
     long long acc = 0;
     for (long long q = 0; q < ip; ++q)
       if (q != i) acc += g.Y1n(q);
-    return S1 + Zn * (g.x0(i, k) * (g.ny - Y1n) + g.xc(i, k) * acc);
+    return L.S1 + Zn * (g.x0(i, k) * (g.ny - Y1n) + g.xc(i, k) * acc);
   };
-  // recv1' block of (source row is, chunk k): [z][y ∈ Y1_me][xc_k(is)]
-  auto r1off = [&](long long is, long long k) { return R1 + Zn * Y1n * (g.Xlo(is) + g.x0(is, k)); };
+  // recv1' block of (source row is, chunk k) on rank (ir, j): [z][y ∈ Y1_ir][xc_k(is)]
+  auto r1off = [&](const InvLayout& Lr, long long ir, long long is, long long k) {
+    return Lr.R1 + Zn * g.Y1n(ir) * (g.Xlo(is) + g.x0(is, k));
+  };
+  const long long nxl = pl->r2c ? g.nx / 2 : g.nx;
   rp.A.resize(K);
   rp.B.resize(K);
   rp.E1.resize(K);
   rp.E2.resize(K);
   for (long long k = 0; k < K; ++k) {
     const long long xc = g.xc(i, k), x0 = g.x0(i, k);
-    // ---- stage A: z-IFFT of columns (xx, y') of `in`; out segmented by z-owner j'
+    // ---- stage A: z-IFFT of columns (l0 = xx, l1 = y') of `in`; out segmented by z-owner j'
     Stage& A = rp.A[k];
     A.in = {kUserIn, x0 * es};
-    A.a.in.tstride = Y3n * Xn;
-    A.a.in.lstride = Xn;
+    set_side(A.a.in, Y3n * Xn, 1, Xn);
     A.out = {kWs, 0};
-    std::vector<longlong2> at(g.nz);
-    for (long long t = 0; t < g.nz; ++t) {
-      long long jp = owner(t, g.nz, g.P2), tl = t - g.Zlo(jp);
-      if (jp == j) at[t] = tent(0, R2 + g.ny * Zn * x0 + g.Y3lo(j) * Zn * xc + tl * xc, Zn * xc);
-      else at[t] = tent(0, s2off(k, jp) + tl * xc, g.Zn(jp) * xc);
+    A.out_bases.push_back({kWs, 0});
+    if (p2p)
+      for (long long jp = 0; jp < g.P2; ++jp) A.out_bases.push_back({kPeer, 0, col_rank(g, i, jp)});
+    Segs aseg;
+    for (long long jp = 0; jp < g.P2; ++jp) {
+      const long long zl = g.Zlo(jp), zn = g.Zn(jp);
+      if (p2p) {
+        const InvLayout Lr = inv_layout(g, i, jp, mode);
+        aseg.push_back({1 + (int)jp, zl, zn, Lr.R2 + g.ny * zn * x0 + g.Y3lo(j) * zn * xc, xc, 1, zn * xc});
+      } else if (jp == j) {
+        aseg.push_back({0, zl, zn, L.R2 + g.ny * Zn * x0 + g.Y3lo(j) * Zn * xc, xc, 1, Zn * xc});
+      } else {
+        aseg.push_back({0, zl, zn, s2off(k, jp), xc, 1, zn * xc});
+      }
     }
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, kStrided, (int)g.nz, xc, Y3n, nullptr, &at));
+    ST(finish_stage(pl, A, kStrided, (int)g.nz, xc, Y3n, nullptr, &aseg));
     // first exchange of the inverse = T2⁻¹ on the column group
-    Exchange& E2 = rp.E1[k];
-    E2.comm = 1;
+    Exchange& E1 = rp.E1[k];
+    E1.comm = 1;
     for (long long jp = 0; jp < g.P2; ++jp) {
       if (jp == j) continue;
-      E2.sends.push_back({(int)jp, {kWs, s2off(k, jp) * es}, (size_t)(Y3n * g.Zn(jp) * xc * es)});
-      E2.recvs.push_back({(int)jp, {kWs, (R2 + g.ny * Zn * x0 + g.Y3lo(jp) * Zn * xc) * es},
+      if (!nccl) E1.peers.push_back(col_rank(g, i, jp));
+      if (p2p) continue;
+      Xfer x{(int)jp, {kWs, s2off(k, jp) * es}, (size_t)(Y3n * g.Zn(jp) * xc * es)};
+      if (ce) {
+        const InvLayout Lr = inv_layout(g, i, jp, mode);
+        x.remote = {kPeer, (Lr.R2 + g.ny * g.Zn(jp) * x0 + g.Y3lo(j) * g.Zn(jp) * xc) * es, col_rank(g, i, jp)};
+      }
+      E1.sends.push_back(x);
+      E1.recvs.push_back({(int)jp, {kWs, (L.R2 + g.ny * Zn * x0 + g.Y3lo(jp) * Zn * xc) * es},
                           (size_t)(g.Y3n(jp) * Zn * xc * es)});
     }
-    // ---- stage B: y-IFFT of columns (xx, z) of recv2' chunk k; out segmented by y-owner i'
+    // ---- stage B: y-IFFT of columns (l0 = xx, l1 = z) of recv2' chunk k; out segmented by y-owner i'
     Stage& B = rp.B[k];
-    B.in = {kWs, (R2 + g.ny * Zn * x0) * es};
-    B.a.in.tstride = Zn * xc;
-    B.a.in.lstride = xc;
+    B.in = {kWs, (L.R2 + g.ny * Zn * x0) * es};
+    set_side(B.a.in, Zn * xc, 1, xc);
     B.out = {kWs, 0};
-    std::vector<longlong2> bt(g.ny);
-    for (long long t = 0; t < g.ny; ++t) {
-      long long ip = owner(t, g.ny, g.P1), tl = t - g.Y1lo(ip);
-      if (ip == i) bt[t] = tent(0, r1off(i, k) + tl * xc, Y1n * xc);
-      else bt[t] = tent(0, s1off(k, ip) + tl * xc, g.Y1n(ip) * xc);
+    B.out_bases.push_back({kWs, 0});
+    if (p2p)
+      for (long long ip = 0; ip < g.P1; ++ip) B.out_bases.push_back({kPeer, 0, row_rank(g, ip, j)});
+    Segs bseg;
+    for (long long ip = 0; ip < g.P1; ++ip) {
+      const long long yl = g.Y1lo(ip), yn = g.Y1n(ip);
+      if (p2p) {
+        const InvLayout Lr = inv_layout(g, ip, j, mode);
+        bseg.push_back({1 + (int)ip, yl, yn, r1off(Lr, ip, i, k), xc, 1, yn * xc});
+      } else if (ip == i) {
+        bseg.push_back({0, yl, yn, r1off(L, i, i, k), xc, 1, Y1n * xc});
+      } else {
+        bseg.push_back({0, yl, yn, s1off(k, ip), xc, 1, yn * xc});
+      }
     }
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, kStrided, (int)g.ny, xc, Zn, nullptr, &bt));
+    ST(finish_stage(pl, B, kStrided, (int)g.ny, xc, Zn, nullptr, &bseg));
     // second exchange of the inverse = T1⁻¹ on the row group
-    Exchange& E1 = rp.E2[k];
-    E1.comm = 0;
+    Exchange& E2 = rp.E2[k];
+    E2.comm = 0;
     for (long long ip = 0; ip < g.P1; ++ip) {
       if (ip == i) continue;
-      E1.sends.push_back({(int)ip, {kWs, s1off(k, ip) * es}, (size_t)(Zn * g.Y1n(ip) * xc * es)});
-      E1.recvs.push_back({(int)ip, {kWs, r1off(ip, k) * es}, (size_t)(Zn * Y1n * g.xc(ip, k) * es)});
+      if (!nccl) E2.peers.push_back(row_rank(g, ip, j));
+      if (p2p) continue;
+      Xfer x{(int)ip, {kWs, s1off(k, ip) * es}, (size_t)(Zn * g.Y1n(ip) * xc * es)};
+      if (ce) {
+        const InvLayout Lr = inv_layout(g, ip, j, mode);
+        x.remote = {kPeer, r1off(Lr, ip, i, k) * es, row_rank(g, ip, j)};
+      }
+      E2.sends.push_back(x);
+      E2.recvs.push_back({(int)ip, {kWs, r1off(L, i, ip, k) * es}, (size_t)(Zn * Y1n * g.xc(ip, k) * es)});
     }
   }
-  // ---- stage C: x-IFFT of lines (y, z); input segmented by (source row, chunk); ×1/N
+  // ---- stage C: x-IFFT of lines (l0 = y, l1 = z); input segmented by (source row, chunk); ×1/N
   Stage& C = rp.C;
   C.in = {kWs, 0};
-  C.a.in_l0s = 1;
-  C.a.in_l1s = Y1n;
-  std::vector<longlong2> ct(g.nxc);
-  for (long long t = 0; t < g.nxc; ++t) {
-    long long is = owner(t, g.nxc, g.P1), tl1 = t - g.Xlo(is);
-    long long k = owner(tl1, g.Xn(is), K), tl = tl1 - g.x0(is, k);
-    ct[t] = tent(0, r1off(is, k) + tl, g.xc(is, k));
-  }
+  Segs cseg;
+  for (long long is = 0; is < g.P1; ++is)
+    for (long long k = 0; k < K; ++k) {
+      const long long xcs = g.xc(is, k);
+      if (xcs > 0) cseg.push_back({0, g.Xlo(is) + g.x0(is, k), xcs, r1off(L, i, is, k), 1, xcs, Y1n * xcs});
+    }
   C.out = {kUserOut, 0};
-  C.a.out.tstride = 1;
-  C.a.out.lstride = pl->r2c ? g.nx / 2 : g.nx;
-  C.a.out_l0s = 1;
-  C.a.out_l1s = Y1n;
+  set_side(C.a.out, 1, nxl, Y1n * nxl);
   C.a.scale = 1.0 / ((double)g.nx * (double)g.ny * (double)g.nz);
-  ST(finish_stage(pl, C, kContig, (int)(pl->r2c ? g.nx / 2 : g.nx), Y1n, Zn, &ct, nullptr));
+  ST(finish_stage(pl, C, kContig, (int)nxl, Y1n, Zn, &cseg, nullptr));
   return DFFT_SUCCESS;
 }
 
 // ------------------------------------------------------------------------------ execution
-void* resolve(const Ref& r, const void* in, void* out, void* ws) {
+struct Ctx {
+  const void* in;
+  void* out;
+  void* ws;
+  void* const* peers;  // P2P: workspace windows by global rank
+};
+
+void* resolve(const Ref& r, const Ctx& c) {
   switch (r.kind) {
-    case kUserIn: return (char*)in + r.off;
-    case kUserOut: return (char*)out + r.off;
-    case kWs: return (char*)ws + r.off;
+    case kUserIn: return (char*)c.in + r.off;
+    case kUserOut: return (char*)c.out + r.off;
+    case kWs: return (char*)c.ws + r.off;
+    case kPeer: return c.peers ? (char*)c.peers[r.peer] + r.off : nullptr;
     default: return nullptr;
   }
 }
 
-dfft_status_t launch(const Stage& s, const void* in, void* out, void* ws, cudaStream_t st) {
+dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
   if (s.empty) return DFFT_SUCCESS;
   PassArgs a = s.a;
-  a.in.base = resolve(s.in, in, out, ws);
-  a.in.base1 = resolve(s.in1, in, out, ws);
-  a.out.base = resolve(s.out, in, out, ws);
-  a.out.base1 = resolve(s.out1, in, out, ws);
+  a.in.base = resolve(s.in, c);
+  a.out.base = resolve(s.out, c);
+  for (size_t q = 0; q < s.in_bases.size(); ++q) a.in.bases[q] = resolve(s.in_bases[q], c);
+  for (size_t q = 0; q < s.out_bases.size(); ++q) a.out.bases[q] = resolve(s.out_bases[q], c);
   if (s.tma_grid > 0 && ((uintptr_t)a.in.base & 15) == 0) {
     // 3D views in reals: (2·L0, n, L1) with strides (tstride, lstride) elements
     const bool f64 = s.es == 16;
@@ -629,10 +787,10 @@ dfft_status_t launch(const Stage& s, const void* in, void* out, void* ws, cudaSt
                                   g_tma_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
     CUtensorMap tin, tout;
-    if (encode(&tin, a.in.base, a.in.tstride, a.in.lstride)) {
-      bool use_st = g_tma_store && a.out.ttab == nullptr && ((uintptr_t)a.out.base & 15) == 0 &&
-                (a.out.tstride * (long long)ces) % 16 == 0 && (a.L1 == 1 || (a.out.lstride * (long long)ces) % 16 == 0) &&
-                encode(&tout, a.out.base, a.out.tstride, a.out.lstride);
+    if (encode(&tin, a.in.base, a.in.tstride, a.in.s1)) {
+      bool use_st = g_tma_store && a.out.ttab == nullptr && a.out.s0 == 1 && ((uintptr_t)a.out.base & 15) == 0 &&
+                    (a.out.tstride * (long long)ces) % 16 == 0 && (a.L1 == 1 || (a.out.s1 * (long long)ces) % 16 == 0) &&
+                    encode(&tout, a.out.base, a.out.tstride, a.out.s1);
       if (!use_st) tout = tin;  // unused by the non-TST variant
       void* targs[] = {&tin, &tout, &a};
       CU(cudaLaunchKernel(use_st ? s.k.tma_st_fn : s.k.tma_fn, dim3((unsigned)s.tma_grid), dim3(s.k.tma_threads), targs,
@@ -645,13 +803,12 @@ dfft_status_t launch(const Stage& s, const void* in, void* out, void* ws, cudaSt
   return DFFT_SUCCESS;
 }
 
-dfft_status_t exchange_nccl(dfft_plan_t pl, const Exchange& x, const void* in, void* out, void* ws,
-                            cudaStream_t st) {
-  if (x.empty()) return DFFT_SUCCESS;
+dfft_status_t exchange_nccl(dfft_plan_t pl, const Exchange& x, const Ctx& cx, cudaStream_t st) {
+  if (x.sends.empty() && x.recvs.empty()) return DFFT_SUCCESS;
   ncclComm_t c = x.comm == 0 ? pl->row : pl->col;
   NC(ncclGroupStart());
-  for (const Xfer& s : x.sends) NC(ncclSend(resolve(s.ref, in, out, ws), s.bytes, ncclUint8, s.peer, c, st));
-  for (const Xfer& r : x.recvs) NC(ncclRecv(resolve(r.ref, in, out, ws), r.bytes, ncclUint8, r.peer, c, st));
+  for (const Xfer& s : x.sends) NC(ncclSend(resolve(s.ref, cx), s.bytes, ncclUint8, s.peer, c, st));
+  for (const Xfer& r : x.recvs) NC(ncclRecv(resolve(r.ref, cx), r.bytes, ncclUint8, r.peer, c, st));
   NC(ncclGroupEnd());
   return DFFT_SUCCESS;
 }
@@ -675,8 +832,8 @@ dfft_status_t exchange_sim(dfft_plan_t pl, bool second, size_t k, const void* co
       if (!rv || rv->bytes != s.bytes)
         return fail(DFFT_ERR_INTERNAL, "sim exchange mismatch %d->%d (%zu vs %zu bytes)", r, q, s.bytes,
                     rv ? rv->bytes : 0);
-      void* sp = resolve(s.ref, ins[r], outs[r], src.ws);
-      void* dp = resolve(rv->ref, ins[q], outs[q], dst.ws);
+      void* sp = resolve(s.ref, Ctx{ins[r], outs[r], src.ws, nullptr});
+      void* dp = resolve(rv->ref, Ctx{ins[q], outs[q], dst.ws, nullptr});
       CU(cudaMemcpyAsync(dp, sp, s.bytes, cudaMemcpyDeviceToDevice, st));
     }
   }
@@ -703,34 +860,174 @@ dfft_status_t prof_end(dfft_plan_t pl, size_t slot, cudaStream_t st) {
   CU(cudaEventRecord(pl->prof_ev[2 * slot + 1], st));
   return DFFT_SUCCESS;
 }
-dfft_status_t launch_p(dfft_plan_t pl, int phase, const Stage& s, const void* in, void* out, void* ws,
-                       cudaStream_t st) {
+dfft_status_t launch_p(dfft_plan_t pl, int phase, const Stage& s, const Ctx& c, cudaStream_t st) {
   if (s.empty) return DFFT_SUCCESS;
   size_t slot = 0;
   ST(prof_begin(pl, phase, st, &slot));
-  ST(launch(s, in, out, ws, st));
+  ST(launch(s, c, st));
   return prof_end(pl, slot, st);
 }
-dfft_status_t exchange_p(dfft_plan_t pl, int phase, const Exchange& x, const void* in, void* out, void* ws,
-                         cudaStream_t st) {
-  if (x.empty()) return DFFT_SUCCESS;
+dfft_status_t exchange_p(dfft_plan_t pl, int phase, const Exchange& x, const Ctx& c, cudaStream_t st) {
+  if (x.sends.empty() && x.recvs.empty()) return DFFT_SUCCESS;
   size_t slot = 0;
   ST(prof_begin(pl, phase, st, &slot));
-  ST(exchange_nccl(pl, x, in, out, ws, st));
+  ST(exchange_nccl(pl, x, c, st));
   return prof_end(pl, slot, st);
+}
+
+// ---- P2P exchange: stage kernels store into the peers' windows; flags order the stages.
+struct SignalArgs {
+  unsigned int* ptr[2 * kMaxBases];
+  int n;
+  unsigned int value;
+};
+
+__global__ void dfft_signal_kernel(const __grid_constant__ SignalArgs a) {
+  // stream order puts this after the stage kernel whose stores it publishes; the system-scope
+  // fence + release store make them visible to the peer that acquires the flag
+  if ((int)threadIdx.x < a.n) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.ptr[threadIdx.x]), "r"(a.value) : "memory");
+  }
+}
+
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitFn stream_wait_value32() {
+  static WaitFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<WaitFn>(p);
+  }();
+  return fn;
+}
+
+// flag word: arr 0 = ready, 1 = done; e = exchange (0 first, 1 second); k chunk; r writer/reader rank
+inline size_t flag_index(const dfft_plan_s* pl, int arr, int e, int k, int r) {
+  const size_t P = (size_t)pl->P1 * pl->P2, K = (size_t)pl->K;
+  return (((size_t)arr * 2 + e) * K + k) * P + r;
+}
+
+dfft_status_t p2p_signal(dfft_plan_t pl, int arr, int e, int k, const std::vector<int>& targets, unsigned value,
+                         cudaStream_t st) {
+  if (targets.empty()) return DFFT_SUCCESS;
+  SignalArgs a{};
+  a.n = (int)targets.size();
+  a.value = value;
+  const int me = pl->comm->rank;
+  for (size_t q = 0; q < targets.size(); ++q)
+    a.ptr[q] = reinterpret_cast<unsigned int*>((char*)pl->peer_ws[targets[q]] + pl->flag_off) +
+               flag_index(pl, arr, e, k, me);
+  void* args[] = {&a};
+  CU(cudaLaunchKernel((const void*)dfft_signal_kernel, dim3(1), dim3(32), args, 0, st));
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t p2p_wait(dfft_plan_t pl, int arr, int e, int k, const std::vector<int>& from, unsigned value,
+                       cudaStream_t st) {
+  unsigned int* flags = reinterpret_cast<unsigned int*>((char*)pl->ranks[0].ws + pl->flag_off);
+  for (int r : from) {
+    CUresult res = stream_wait_value32()((CUstream)st, (CUdeviceptr)(flags + flag_index(pl, arr, e, k, r)), value,
+                                         CU_STREAM_WAIT_VALUE_GEQ);
+    if (res != CUDA_SUCCESS) return fail(DFFT_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)res);
+  }
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t execute_p2p(dfft_plan_t pl, const Ctx& cx, cudaStream_t st) {
+  RankPlan& rp = pl->ranks[0];
+  const int K = (int)rp.A.size();
+  const unsigned ep = ++pl->epoch;
+  for (int k = 0; k < K; ++k) {
+    // my epoch-1 stores into the first-exchange peers were consumed
+    if (ep > 1) ST(p2p_wait(pl, 1, 0, k, rp.E1[k].peers, ep - 1, st));
+    ST(launch_p(pl, 0, rp.A[k], cx, st));
+    ST(p2p_signal(pl, 0, 0, k, rp.E1[k].peers, ep, st));
+  }
+  for (int k = 0; k < K; ++k) {
+    ST(p2p_wait(pl, 0, 0, k, rp.E1[k].peers, ep, st));
+    if (ep > 1) ST(p2p_wait(pl, 1, 1, k, rp.E2[k].peers, ep - 1, st));
+    ST(launch_p(pl, 2, rp.B[k], cx, st));
+    ST(p2p_signal(pl, 1, 0, k, rp.E1[k].peers, ep, st));  // done reading my first-exchange window
+    ST(p2p_signal(pl, 0, 1, k, rp.E2[k].peers, ep, st));  // ready: stored into the peers' second windows
+  }
+  for (int k = 0; k < K; ++k) ST(p2p_wait(pl, 0, 1, k, rp.E2[k].peers, ep, st));
+  ST(launch_p(pl, 4, rp.C, cx, st));
+  for (int k = 0; k < K; ++k) ST(p2p_signal(pl, 1, 1, k, rp.E2[k].peers, ep, st));
+  return DFFT_SUCCESS;
+}
+
+// ---- CE exchange: stage kernels pack into local send blocks (as for NCCL); the copy engine of
+// the comm stream moves each block into the receiver's window; flags order producer/consumer.
+dfft_status_t exchange_ce(dfft_plan_t pl, int e, int k, const Exchange& x, const Ctx& cx, unsigned ep,
+                          cudaStream_t st) {
+  if (x.peers.empty()) return DFFT_SUCCESS;
+  if (ep > 1) ST(p2p_wait(pl, 1, e, k, x.peers, ep - 1, st));  // receivers consumed epoch ep-1
+  for (const Xfer& t : x.sends) {
+    if (t.height > 1)
+      CU(cudaMemcpy2DAsync(resolve(t.remote, cx), t.dpitch, resolve(t.ref, cx), t.spitch, t.width, t.height,
+                           cudaMemcpyDeviceToDevice, st));
+    else
+      CU(cudaMemcpyAsync(resolve(t.remote, cx), resolve(t.ref, cx), t.bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  return p2p_signal(pl, 0, e, k, x.peers, ep, st);
+}
+
+dfft_status_t execute_ce(dfft_plan_t pl, const Ctx& cx, cudaStream_t user) {
+  RankPlan& rp = pl->ranks[0];
+  const size_t K = rp.A.size();
+  const unsigned ep = ++pl->epoch;
+  cudaStream_t sc = pl->s_comp, sm = pl->s_comm;
+  CU(cudaEventRecord(pl->ev_fork, user));
+  CU(cudaStreamWaitEvent(sc, pl->ev_fork, 0));
+  CU(cudaStreamWaitEvent(sm, pl->ev_fork, 0));
+  auto do_A = [&](size_t k) -> dfft_status_t {
+    ST(launch_p(pl, 0, rp.A[k], cx, sc));
+    CU(cudaEventRecord(pl->evA[k], sc));
+    CU(cudaStreamWaitEvent(sm, pl->evA[k], 0));
+    size_t slot = 0;
+    ST(prof_begin(pl, 1, sm, &slot));
+    ST(exchange_ce(pl, 0, (int)k, rp.E1[k], cx, ep, sm));
+    return prof_end(pl, slot, sm);
+  };
+  ST(do_A(0));
+  for (size_t k = 0; k < K; ++k) {
+    if (k + 1 < K) ST(do_A(k + 1));
+    ST(p2p_wait(pl, 0, 0, (int)k, rp.E1[k].peers, ep, sc));  // peers' blocks of chunk k have landed
+    ST(launch_p(pl, 2, rp.B[k], cx, sc));
+    ST(p2p_signal(pl, 1, 0, (int)k, rp.E1[k].peers, ep, sc));  // done reading my first receive region
+    CU(cudaEventRecord(pl->evB[k], sc));
+    CU(cudaStreamWaitEvent(sm, pl->evB[k], 0));
+    size_t slot = 0;
+    ST(prof_begin(pl, 3, sm, &slot));
+    ST(exchange_ce(pl, 1, (int)k, rp.E2[k], cx, ep, sm));
+    ST(prof_end(pl, slot, sm));
+  }
+  for (size_t k = 0; k < K; ++k) ST(p2p_wait(pl, 0, 1, (int)k, rp.E2[k].peers, ep, sc));
+  ST(launch_p(pl, 4, rp.C, cx, sc));
+  for (size_t k = 0; k < K; ++k) ST(p2p_signal(pl, 1, 1, (int)k, rp.E2[k].peers, ep, sc));
+  CU(cudaEventRecord(pl->ev_join_comp, sc));
+  CU(cudaEventRecord(pl->ev_join_comm, sm));
+  CU(cudaStreamWaitEvent(user, pl->ev_join_comp, 0));
+  CU(cudaStreamWaitEvent(user, pl->ev_join_comm, 0));
+  return DFFT_SUCCESS;
 }
 
 dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream_t user) {
   RankPlan& rp = pl->ranks[0];
   const size_t K = rp.A.size();
-  void* ws = rp.ws;
+  const Ctx cx{in, out, rp.ws, pl->peer_ws.empty() ? nullptr : pl->peer_ws.data()};
+  if (pl->p2p) return execute_p2p(pl, cx, user);
+  if (pl->ce) return execute_ce(pl, cx, user);
   if (!pl->overlap) {
     // static-barrier ablation: every step in program order on the user's stream
-    for (size_t k = 0; k < K; ++k) ST(launch_p(pl, 0, rp.A[k], in, out, ws, user));
-    for (size_t k = 0; k < K; ++k) ST(exchange_p(pl, 1, rp.E1[k], in, out, ws, user));
-    for (size_t k = 0; k < K; ++k) ST(launch_p(pl, 2, rp.B[k], in, out, ws, user));
-    for (size_t k = 0; k < K; ++k) ST(exchange_p(pl, 3, rp.E2[k], in, out, ws, user));
-    return launch_p(pl, 4, rp.C, in, out, ws, user);
+    for (size_t k = 0; k < K; ++k) ST(launch_p(pl, 0, rp.A[k], cx, user));
+    for (size_t k = 0; k < K; ++k) ST(exchange_p(pl, 1, rp.E1[k], cx, user));
+    for (size_t k = 0; k < K; ++k) ST(launch_p(pl, 2, rp.B[k], cx, user));
+    for (size_t k = 0; k < K; ++k) ST(exchange_p(pl, 3, rp.E2[k], cx, user));
+    return launch_p(pl, 4, rp.C, cx, user);
   }
   cudaStream_t sc = pl->s_comp, sm = pl->s_comm;
   CU(cudaEventRecord(pl->ev_fork, user));
@@ -739,11 +1036,11 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
   // host issue order is a topological order of the chunk DAG, so every wait refers to the
   // record issued in this execute:  A0 E1_0 | A1 E1_1 B0 E2_0 | A2 E1_2 B1 E2_1 | ...
   auto do_A = [&](size_t k) -> dfft_status_t {
-    ST(launch_p(pl, 0, rp.A[k], in, out, ws, sc));
-    if (!rp.E1[k].empty()) {
+    ST(launch_p(pl, 0, rp.A[k], cx, sc));
+    if (!rp.E1[k].sends.empty() || !rp.E1[k].recvs.empty()) {
       CU(cudaEventRecord(pl->evA[k], sc));
       CU(cudaStreamWaitEvent(sm, pl->evA[k], 0));
-      ST(exchange_p(pl, 1, rp.E1[k], in, out, ws, sm));
+      ST(exchange_p(pl, 1, rp.E1[k], cx, sm));
       CU(cudaEventRecord(pl->evE1[k], sm));
     }
     return DFFT_SUCCESS;
@@ -751,18 +1048,18 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
   ST(do_A(0));
   for (size_t k = 0; k < K; ++k) {
     if (k + 1 < K) ST(do_A(k + 1));
-    if (!rp.E1[k].empty()) CU(cudaStreamWaitEvent(sc, pl->evE1[k], 0));
-    ST(launch_p(pl, 2, rp.B[k], in, out, ws, sc));
-    if (!rp.E2[k].empty()) {
+    if (!rp.E1[k].sends.empty() || !rp.E1[k].recvs.empty()) CU(cudaStreamWaitEvent(sc, pl->evE1[k], 0));
+    ST(launch_p(pl, 2, rp.B[k], cx, sc));
+    if (!rp.E2[k].sends.empty() || !rp.E2[k].recvs.empty()) {
       CU(cudaEventRecord(pl->evB[k], sc));
       CU(cudaStreamWaitEvent(sm, pl->evB[k], 0));
-      ST(exchange_p(pl, 3, rp.E2[k], in, out, ws, sm));
+      ST(exchange_p(pl, 3, rp.E2[k], cx, sm));
       CU(cudaEventRecord(pl->evE2[k], sm));
     }
   }
   // stage C needs every chunk of exchange 2 (same comm stream => the last record suffices)
-  if (!rp.E2[K - 1].empty()) CU(cudaStreamWaitEvent(sc, pl->evE2[K - 1], 0));
-  ST(launch_p(pl, 4, rp.C, in, out, ws, sc));
+  if (!rp.E2[K - 1].sends.empty() || !rp.E2[K - 1].recvs.empty()) CU(cudaStreamWaitEvent(sc, pl->evE2[K - 1], 0));
+  ST(launch_p(pl, 4, rp.C, cx, sc));
   CU(cudaEventRecord(pl->ev_join_comp, sc));
   CU(cudaEventRecord(pl->ev_join_comm, sm));
   CU(cudaStreamWaitEvent(user, pl->ev_join_comp, 0));
@@ -773,12 +1070,12 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
 dfft_status_t execute_sim(dfft_plan_t pl, const void* const* ins, void* const* outs, cudaStream_t st) {
   const size_t P = pl->ranks.size(), K = pl->ranks[0].A.size();
   for (size_t k = 0; k < K; ++k)
-    for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].A[k], ins[r], outs[r], pl->ranks[r].ws, st));
+    for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].A[k], Ctx{ins[r], outs[r], pl->ranks[r].ws, nullptr}, st));
   for (size_t k = 0; k < K; ++k) ST(exchange_sim(pl, false, k, ins, outs, st));
   for (size_t k = 0; k < K; ++k)
-    for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].B[k], ins[r], outs[r], pl->ranks[r].ws, st));
+    for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].B[k], Ctx{ins[r], outs[r], pl->ranks[r].ws, nullptr}, st));
   for (size_t k = 0; k < K; ++k) ST(exchange_sim(pl, true, k, ins, outs, st));
-  for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].C, ins[r], outs[r], pl->ranks[r].ws, st));
+  for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].C, Ctx{ins[r], outs[r], pl->ranks[r].ws, nullptr}, st));
   return DFFT_SUCCESS;
 }
 
@@ -790,8 +1087,20 @@ void free_stage(Stage& s) {
 
 void free_plan(dfft_plan_t pl) {
   if (!pl) return;
+  if ((pl->p2p || pl->ce) && pl->epoch > 0 && pl->s_comp) {
+    // peers write their final `done` flags into this window after their last stage: wait for
+    // them so no peer store lands in freed memory
+    RankPlan& rp = pl->ranks[0];
+    for (int k = 0; k < (int)rp.A.size(); ++k) {
+      p2p_wait(pl, 1, 0, k, rp.E1[k].peers, pl->epoch, pl->s_comp);
+      p2p_wait(pl, 1, 1, k, rp.E2[k].peers, pl->epoch, pl->s_comp);
+    }
+  }
   if (pl->s_comp) cudaStreamSynchronize(pl->s_comp);
   if (pl->s_comm) cudaStreamSynchronize(pl->s_comm);
+  for (size_t r = 0; r < pl->peer_ws.size(); ++r)
+    if (pl->peer_ws[r] && (int)r != pl->comm->rank) cudaIpcCloseMemHandle(pl->peer_ws[r]);
+  pl->peer_ws.clear();
   for (RankPlan& rp : pl->ranks) {
     for (Stage& s : rp.A) free_stage(s);
     for (Stage& s : rp.B) free_stage(s);
@@ -955,7 +1264,16 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   int Kreq = (int)(flags & 0xff);
   bool overlap = !(flags & DFFT_FLAG_NO_OVERLAP);
   long long kmax = direction == DFFT_FORWARD ? nz / p2 : nxc / p1;
-  long long K = Kreq > 0 ? Kreq : (P > 1 ? 4 : 1);
+  // exchange transport for P > 1: copy engines into IPC windows (default),
+  // fused epilogue stores into the windows (DFFT_FLAG_FUSED_STORE), or NCCL (DFFT_FLAG_NCCL)
+  const char* exch_env = getenv("DFFT_EXCHANGE");
+  auto env_is = [&](const char* v) { return exch_env && strcmp(exch_env, v) == 0; };
+  const bool nccl_mode = comm->sim || P == 1 || (flags & DFFT_FLAG_NCCL) || env_is("nccl");
+  const bool p2p_mode = !nccl_mode && ((flags & DFFT_FLAG_FUSED_STORE) || env_is("p2p"));
+  const bool ce_mode = !nccl_mode && !p2p_mode;
+  // chunks pipeline the transfers against the FFTs; with fused stores the transfer happens
+  // inside the FFT kernels themselves, so one chunk is the default there
+  long long K = Kreq > 0 ? Kreq : (P > 1 && !p2p_mode ? 4 : 1);
   K = std::max<long long>(1, std::min<long long>(K, kmax));
   if (P == 1) K = 1;  // nothing to overlap
 
@@ -974,6 +1292,11 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   pl->r2c = r2c;
   pl->overlap = overlap;
   pl->es = f64 ? 16 : 8;
+  // exchange over NVLink peer memory unless asked for NCCL (flag or DFFT_EXCHANGE=nccl)
+  pl->p2p = p2p_mode;
+  pl->ce = ce_mode;
+  if ((pl->p2p || pl->ce) && !stream_wait_value32())
+    return fail(DFFT_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
   Geo g{nx, ny, nz, nxc, p1, p2, K};
 
   if (!comm->sim && P > 1) {
@@ -1039,6 +1362,28 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
     if (rp.ws_bytes) {
       cudaError_t e = cudaMalloc(&rp.ws, rp.ws_bytes);
       if (e != cudaSuccess) return fail(DFFT_ERR_ALLOC, "workspace of %zu bytes: %s", rp.ws_bytes, cudaGetErrorString(e));
+    }
+  }
+  if (pl->p2p || pl->ce) {
+    // every workspace becomes an IPC window; open the windows of the row and column peers
+    RankPlan& rp = pl->ranks[0];
+    CU(cudaMemset((char*)rp.ws + pl->flag_off, 0, flag_bytes(g)));
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, rp.ws));
+    char* d = nullptr;
+    CU(cudaMalloc(&d, sizeof(h) * (P + 1)));
+    CU(cudaMemcpy(d, &h, sizeof(h), cudaMemcpyHostToDevice));
+    NC(ncclAllGather(d, d + sizeof(h), sizeof(h), ncclUint8, comm->world, 0));
+    std::vector<cudaIpcMemHandle_t> all(P);
+    CU(cudaMemcpy(all.data(), d + sizeof(h), sizeof(h) * P, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    pl->peer_ws.assign(P, nullptr);
+    pl->peer_ws[comm->rank] = rp.ws;
+    for (int r = 0; r < P; ++r) {
+      int ri = r / p2, rj = r % p2;
+      if (r == comm->rank || (ri != rp.i && rj != rp.j)) continue;  // only row and column peers
+      cudaError_t e = cudaIpcOpenMemHandle(&pl->peer_ws[r], all[r], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return fail(DFFT_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
     }
   }
   CU(cudaStreamCreateWithFlags(&pl->s_comp, cudaStreamNonBlocking));
@@ -1203,10 +1548,8 @@ dfft_status_t dfft_fft1d(const void* in, void* out, int64_t n, int64_t howmany, 
   ST(get_twiddles((int)n, f64 != 0, sign, dev, &s.a.tw));
   s.a.in.base = const_cast<void*>(in);
   s.a.out.base = out;
-  s.a.in.tstride = s.a.out.tstride = 1;
-  s.a.in.lstride = s.a.out.lstride = n;
-  s.a.in_l0s = s.a.out_l0s = 1;
-  s.a.in_l1s = s.a.out_l1s = 0;
+  set_side(s.a.in, 1, n, 0);
+  set_side(s.a.out, 1, n, 0);
   s.a.L0 = howmany;
   s.a.L1 = 1;
   s.a.scale = 1.0;

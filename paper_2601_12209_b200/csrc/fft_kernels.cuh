@@ -228,19 +228,28 @@ template <int DIR, int R, typename C> __device__ __forceinline__ void dft(C* v) 
 // Where element t of a line lives on the global side of a pass (input of the first pass or
 // output of the last pass).  Unsegmented: toff = t·tstride, lstr = lstride.  Segmented: a
 // per-t table {toff, lstr} built at plan time (send-block routing = the fused pack/unpack).
+constexpr int kMaxBases = 16;
+// Element (t, l0, l1) of a side lives at  base + off(t) + l0·s0 + l1·s1  (complex elements):
+//   unsegmented: off(t) = t·tstride, (s0, s1) from the map;
+//   segmented:   a per-t table entry {sel<<56 | off(t), s0, s1} — t ranges owned by different
+//                peers live in different send blocks / windows with their own layouts.
+struct SegEnt {
+  long long off;  // sel << 56 | element offset of (t, 0, 0) relative to bases[sel]
+  int s0, s1;     // line strides of this segment
+};
 struct SideMap {
-  void* base;             // unsegmented: the side's pointer; segmented: base of entries with sel 0
-  void* base1;            // segmented: base of entries with sel 1 (e.g. the user's output buffer)
-  const longlong2* ttab;  // nullptr => unsegmented; else per t: {sel<<62 | offset, line stride}
-  long long tstride;
-  long long lstride;
+  void* base;                 // unsegmented: the side's pointer
+  void* bases[kMaxBases];     // segmented: base pointer per selector (local buffers, peers' windows)
+  const SegEnt* ttab;         // nullptr => unsegmented
+  long long tstride, s0, s1;  // unsegmented strides (elements)
 };
 
 template <typename C>
-__device__ __forceinline__ C* side_ptr(const SideMap& m, int t, long long lidx) {
-  const longlong2 e = __ldg(m.ttab + t);
-  C* b = reinterpret_cast<C*>((e.x >> 62) ? m.base1 : m.base);
-  return b + ((e.x & ((1LL << 62) - 1)) + lidx * e.y);
+__device__ __forceinline__ C* seg_ptr(const SideMap& m, int t, long long l0, long long l1) {
+  const longlong2 raw = __ldg(reinterpret_cast<const longlong2*>(m.ttab) + t);
+  const int s0 = (int)(raw.y & 0xffffffffLL), s1 = (int)(raw.y >> 32);
+  C* b = reinterpret_cast<C*>(m.bases[(unsigned long long)raw.x >> 56]);
+  return b + ((raw.x & ((1LL << 56) - 1)) + l0 * s0 + l1 * s1);
 }
 
 // Global store of one complex value from the last pass (DFFT_STORE_CS: streaming hint, dev A/B).
@@ -255,11 +264,9 @@ template <typename C> __device__ __forceinline__ void st_out(C* p, C v) {
 // Kernel arguments shared by both families.
 struct PassArgs {
   SideMap in, out;
-  const void* tw;  // per-pass twiddle tables (complex), sched_twoff layout
-  long long L0, L1;  // line grid: lines (l0, l1), l0 < L0, l1 < L1
-  // contig: Lidx = l0·l0s + l1·l1s for the in/out side; strided: Lidx = l1, l0 is unit stride
-  long long in_l0s, in_l1s, out_l0s, out_l1s;
-  double scale;  // applied to the outputs of the last pass (1 = none)
+  const void* tw;    // per-pass twiddle tables (complex), sched_twoff layout
+  long long L0, L1;  // line grid: lines (l0, l1), l0 < L0, l1 < L1 (strided: l0 = the column)
+  double scale;      // applied to the outputs of the last pass (1 = none)
 };
 
 // --------------------------------------------------------------------------------- Stockham core
@@ -325,23 +332,37 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
 }
 
 // ------------------------------------------------------------------ contiguous-axis family
-template <typename C> struct ContigIO {
+// Global side of a pass for one line (l0, l1): loads of the first pass, stores of the last.
+// UNIT_T: unsegmented sides have t-stride 1 (the contig family; the host guarantees it).
+template <typename C, bool UNIT_T = false> struct GIO {
   static constexpr bool kSyncAfterLoad = false;
   __device__ __forceinline__ void after_load() {}
   const C* __restrict__ in;
   C* __restrict__ out;
   const SideMap* mi;
   const SideMap* mo;
-  long long lin, lout;
+  long long l0, l1;
+  long long lin, lout;  // unsegmented sides: l0·s0 + l1·s1
   decltype(C{}.x) scale;
+  __device__ __forceinline__ void init(const SideMap& i, const SideMap& o, long long l0_, long long l1_, double sc) {
+    in = reinterpret_cast<const C*>(i.base);
+    out = reinterpret_cast<C*>(o.base);
+    mi = &i;
+    mo = &o;
+    l0 = l0_;
+    l1 = l1_;
+    lin = l0_ * i.s0 + l1_ * i.s1;
+    lout = l0_ * o.s0 + l1_ * o.s1;
+    scale = (decltype(C{}.x))sc;
+  }
   __device__ __forceinline__ C load(int t) const {
-    if (mi->ttab == nullptr) return in[(long long)t + lin];
-    return *side_ptr<const C>(*mi, t, lin);
+    if (mi->ttab == nullptr) return UNIT_T ? in[lin + t] : in[(long long)t * mi->tstride + lin];
+    return *seg_ptr<const C>(*mi, t, l0, l1);
   }
   __device__ __forceinline__ void store(int t, C v) const {
     if (scale != 1) { v.x *= scale; v.y *= scale; }
-    if (mo->ttab == nullptr) out[(long long)t + lout] = v;
-    else *side_ptr<C>(*mo, t, lout) = v;
+    if (mo->ttab == nullptr) st_out(out + (UNIT_T ? lout + t : (long long)t * mo->tstride + lout), v);
+    else st_out(seg_ptr<C>(*mo, t, l0, l1), v);
   }
 };
 
@@ -359,7 +380,7 @@ template <int N> struct ContigCfg {
 
 template <typename Real, int N, int DIR>
 __global__ void __launch_bounds__(ContigCfg<N>::THREADS)
-fft_contig_kernel(const PassArgs a) {
+fft_contig_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
   using Cfg = ContigCfg<N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -370,16 +391,8 @@ fft_contig_kernel(const PassArgs a) {
   const bool active = line < a.L0 * a.L1;
   const long long l1 = active ? line / a.L0 : 0;
   const long long l0 = active ? line - l1 * a.L0 : 0;
-  ContigIO<C> io;
-  io.in = reinterpret_cast<const C*>(a.in.base);
-  io.out = reinterpret_cast<C*>(a.out.base);
-  io.mi = &a.in;
-  io.mo = &a.out;
-  const long long lin = l0 * a.in_l0s + l1 * a.in_l1s;
-  const long long lout = l0 * a.out_l0s + l1 * a.out_l1s;
-  io.lin = a.in.ttab == nullptr ? lin * a.in.lstride : lin;
-  io.lout = a.out.ttab == nullptr ? lout * a.out.lstride : lout;
-  io.scale = (Real)a.scale;
+  GIO<C, true> io;
+  io.init(a.in, a.out, l0, l1, a.scale);
   ContigSM sm{li * Cfg::LS};
   stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
 }
@@ -405,27 +418,6 @@ template <typename Real, int N> struct StridedCfg {
   static constexpr int SMEM_ELEMS = N * W + (N / R0) * PAD;
 };
 
-template <typename C> struct StridedIO {
-  static constexpr bool kSyncAfterLoad = false;
-  __device__ __forceinline__ void after_load() {}
-  const C* __restrict__ in;
-  C* __restrict__ out;
-  const SideMap* mi;
-  const SideMap* mo;
-  long long cin, cout;  // unsegmented: column offset incl. l1·lstride; segmented: l0
-  long long l1;
-  decltype(C{}.x) scale;
-  __device__ __forceinline__ C load(int t) const {
-    if (mi->ttab == nullptr) return in[(long long)t * mi->tstride + cin];
-    return side_ptr<const C>(*mi, t, l1)[cin];
-  }
-  __device__ __forceinline__ void store(int t, C v) const {
-    if (scale != 1) { v.x *= scale; v.y *= scale; }
-    if (mo->ttab == nullptr) st_out(out + ((long long)t * mo->tstride + cout), v);
-    else st_out(side_ptr<C>(*mo, t, l1) + cout, v);
-  }
-};
-
 template <int W, int R0, int PAD> struct StridedSM {
   int c;
   __device__ __forceinline__ int operator()(int t) const { return t * W + c + (t / R0) * PAD; }
@@ -433,7 +425,7 @@ template <int W, int R0, int PAD> struct StridedSM {
 
 template <typename Real, int N, int DIR>
 __global__ void __launch_bounds__(StridedCfg<Real, N>::THREADS)
-fft_strided_kernel(const PassArgs a) {
+fft_strided_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
   using Cfg = StridedCfg<Real, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -444,15 +436,8 @@ fft_strided_kernel(const PassArgs a) {
   const long long l1 = blockIdx.x / ntile;
   const long long l0 = (blockIdx.x - l1 * ntile) * Cfg::W + c;
   const bool active = l0 < a.L0;
-  StridedIO<C> io;
-  io.in = reinterpret_cast<const C*>(a.in.base);
-  io.out = reinterpret_cast<C*>(a.out.base);
-  io.mi = &a.in;
-  io.mo = &a.out;
-  io.l1 = l1;
-  io.cin = a.in.ttab == nullptr ? l0 + l1 * a.in.lstride : l0;
-  io.cout = a.out.ttab == nullptr ? l0 + l1 * a.out.lstride : l0;
-  io.scale = (Real)a.scale;
+  GIO<C> io;
+  io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
   StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
   stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
 }
@@ -510,7 +495,10 @@ constexpr int largest_divisor_le(int n, int cap) {
 template <typename Real, int N> struct TmaCfg {
   static constexpr Sched S = make_sched(N);
   static constexpr int ES = (int)sizeof(Real) * 2;
-  static constexpr int W0 = ES == 8 ? 8 : 4;  // 64 B row segments
+#ifndef DFFT_TMA_ROWB
+#define DFFT_TMA_ROWB 64
+#endif
+  static constexpr int W0 = DFFT_TMA_ROWB / ES;  // row segment of a tile (bytes / element size)
   static constexpr int W = S.T * W0 >= 256 ? W0 : 256 / S.T;
   static constexpr int THREADS = S.T * W;
   static constexpr int NS = 2;
@@ -524,7 +512,7 @@ template <typename Real, int N> struct TmaCfg {
   static constexpr bool OK = S.npass >= 2 && THREADS <= 1024 && SMEM <= 227 * 1024 && 2 * W <= 256;
 };
 
-template <typename C, int W, bool TST> struct TmaIO : StridedIO<C> {
+template <typename C, int W, bool TST> struct TmaIO : GIO<C> {
   static constexpr bool kSyncAfterLoad = true;
   const C* stage;  // this tile's stage buffer, dense [t][W]
   C* obuf;         // TST: dense [t][W] output tile, written to HBM by a TMA store
@@ -542,7 +530,7 @@ template <typename C, int W, bool TST> struct TmaIO : StridedIO<C> {
       if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
       obuf[t * W + c] = v;
     } else {
-      StridedIO<C>::store(t, v);
+      GIO<C>::store(t, v);
     }
   }
   __device__ __forceinline__ void after_load() {
@@ -560,7 +548,7 @@ template <typename C, int W, bool TST> struct TmaIO : StridedIO<C> {
 template <typename Real, int N, int DIR, bool TST>
 __global__ void __launch_bounds__(TmaCfg<Real, N>::THREADS)
 fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
-                       const PassArgs a) {
+                       const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
   using Cfg = TmaCfg<Real, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -598,12 +586,8 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     const bool active = l0 < a.L0;
     if (TST && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
     TmaIO<C, Cfg::W, TST> io;
+    io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
     io.obuf = work;
-    io.out = reinterpret_cast<C*>(a.out.base);
-    io.mo = &a.out;
-    io.l1 = l1;
-    io.cout = a.out.ttab == nullptr ? l0 + l1 * a.out.lstride : l0;
-    io.scale = (Real)a.scale;
     io.stage = stages + s * Cfg::STAGE_ELEMS;
     io.c = c;
     const long long next = tile + (long long)Cfg::NS * gridDim.x;

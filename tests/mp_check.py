@@ -47,15 +47,19 @@ def main():
     n_ok = 0
     for decomp, grid, shape, prec in cases:
         results = []
-        for chunks, overlap in ((0, True), (1, True), (3, True), (2, False)):
-            fwd = dfft.Plan(comm, shape, decomp, grid, "c2c_" + prec, dfft.FORWARD, chunks=chunks, overlap=overlap)
-            inv = dfft.Plan(comm, shape, decomp, grid, "c2c_" + prec, dfft.INVERSE, chunks=chunks, overlap=overlap)
+        for chunks, overlap, exch in ((0, True, "ce"), (1, True, "ce"), (3, True, "ce"), (0, True, "p2p"),
+                                      (3, True, "p2p"), (0, True, "nccl"), (3, True, "nccl"), (2, False, "nccl")):
+            fwd = dfft.Plan(comm, shape, decomp, grid, "c2c_" + prec, dfft.FORWARD, chunks=chunks, overlap=overlap,
+                            exchange=exch)
+            inv = dfft.Plan(comm, shape, decomp, grid, "c2c_" + prec, dfft.INVERSE, chunks=chunks, overlap=overlap,
+                            exchange=exch)
             lo, n = fwd.box(0)
             x = fwd.alloc_in()
             inputs.fill_box_cuda(x, 11, shape, lo, n, True)
             y, z = fwd.alloc_out(), inv.alloc_out()
-            fwd.execute(x, y)
-            inv.execute(y, z)
+            for _ in range(2):  # twice: the second execute exercises the flag epochs / buffer reuse
+                fwd.execute(x, y)
+                inv.execute(y, z)
             torch.cuda.synchronize()
             results.append((gather(y, fwd, 1), gather(z, inv, 1)))
             fwd.destroy()
