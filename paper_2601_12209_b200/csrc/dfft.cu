@@ -146,6 +146,36 @@ CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP
                                                                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
 
+// R2C/C2R split twiddles: w^k = exp(dir·2πi·k/(2N)), k ∈ [0, N), long double once each.
+dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void** out) {
+  std::lock_guard<std::mutex> lk(g_tw_mu);
+  TwKey key{-N, f64 ? 1 : 0, dir, dev};  // negative n: the split table of length N
+  auto it = g_tw.find(key);
+  if (it != g_tw.end()) {
+    *out = it->second;
+    return DFFT_SUCCESS;
+  }
+  void* d = nullptr;
+  const size_t es = f64 ? 16 : 8;
+  CU(cudaMalloc(&d, (size_t)N * es));
+  std::vector<double> hd(2 * (size_t)N);
+  std::vector<float> hf(2 * (size_t)N);
+  for (int k = 0; k < N; ++k) {
+    long double a = 2.0L * 3.141592653589793238462643383279502884L * (long double)k / (2.0L * N);
+    hd[2 * k] = (double)cosl(a);
+    hd[2 * k + 1] = (double)((long double)dir * sinl(a));
+    hf[2 * k] = (float)cosl(a);
+    hf[2 * k + 1] = (float)((long double)dir * sinl(a));
+  }
+  if (f64) CU(cudaMemcpy(d, hd.data(), (size_t)N * es, cudaMemcpyHostToDevice));
+  else CU(cudaMemcpy(d, hf.data(), (size_t)N * es, cudaMemcpyHostToDevice));
+  g_tw[key] = d;
+  *out = d;
+  return DFFT_SUCCESS;
+}
+
+inline bool is_contig(int family) { return family != kStrided; }
+
 dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
   bool ok = f64 ? lookup_kernel_f64(family, n, dir, k) : lookup_kernel_f32(family, n, dir, k);
   if (!ok) return fail(DFFT_ERR_UNSUPPORTED, "axis length %d not instantiated", n);
@@ -273,6 +303,7 @@ using Segs = std::vector<Seg>;
 
 // per-t table {sel<<56 | off(t), s0 | s1<<32} (the kernel's SegEnt)
 std::vector<longlong2> seg_table(const Segs& segs, long long n) {
+  for (const Seg& q : segs) n = std::max(n, q.tlo + q.tn);  // R2C/C2R sides carry N+1 bins
   std::vector<longlong2> tab(n);
   for (const Seg& q : segs)
     for (long long t = q.tlo; t < q.tlo + q.tn; ++t) {
@@ -316,7 +347,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
     return fail(DFFT_ERR_UNSUPPORTED, "more than %d segment bases", kMaxBases);
   if (in_segs && linearize(*in_segs, n, s.in, s.in_bases, s.a.in, (long long)pl->es)) in_segs = nullptr;
   if (out_segs && linearize(*out_segs, n, s.out, s.out_bases, s.a.out, (long long)pl->es)) out_segs = nullptr;
-  if (family == kContig && ((!in_segs && s.a.in.tstride != 1) || (!out_segs && s.a.out.tstride != 1)))
+  if (is_contig(family) && ((!in_segs && s.a.in.tstride != 1) || (!out_segs && s.a.out.tstride != 1)))
     return fail(DFFT_ERR_INTERNAL, "contig stage with a non-unit t-stride side");
   std::vector<longlong2> in_tab_h, out_tab_h;
   if (in_segs) in_tab_h = seg_table(*in_segs, n);
@@ -334,11 +365,13 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   }
   ST(get_kernel(family, n, pl->f64, pl->dir, &s.k));
   ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw));
+  if (family == kContigR2C || family == kContigC2R)
+    ST(get_split_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw2));
   if (in_tab) ST(upload_table(*in_tab, &s.in_tab));
   if (out_tab) ST(upload_table(*out_tab, &s.out_tab));
   s.a.in.ttab = (const SegEnt*)s.in_tab;
   s.a.out.ttab = (const SegEnt*)s.out_tab;
-  if (family == kContig) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
+  if (is_contig(family)) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
   else s.grid = ((L0 + s.k.per_cta - 1) / s.k.per_cta) * L1;
   if (s.grid >= (1LL << 31)) return fail(DFFT_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", s.grid);
   if (family == kStrided && s.k.tma_fn && g_use_tma && !in_tab && tensor_map_encoder()) {
@@ -483,7 +516,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       }
     }
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, kContig, (int)nxl, Y1n, zc, nullptr, &aseg));
+    ST(finish_stage(pl, A, pl->r2c ? kContigR2C : kContig, (int)nxl, Y1n, zc, nullptr, &aseg));
     // ---- exchange 1 (row group)
     Exchange& E1 = rp.E1[k];
     E1.comm = 0;
@@ -576,7 +609,9 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
 dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
   const long long nxl = pl->r2c ? nx / 2 : nx;
-  rp.ws_bytes = (size_t)(nxc * ny * nz * es);
+  const long long W = nxc * ny * nz;
+  const bool c2r = pl->r2c && pl->dir == DFFT_INVERSE;  // the real `out` cannot hold a complex stage
+  rp.ws_bytes = (size_t)((c2r ? 2 : 1) * W * es);
   rp.A.resize(1);
   rp.B.resize(1);
   rp.E1.resize(1);
@@ -584,9 +619,9 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   Stage &A = rp.A[0], &B = rp.B[0], &C = rp.C;
   // z-pass, columns (l0 = x, l1 = y): natural [z][y][x] -> ws [y][z][x]
   auto zpass = [&](Stage& Z) -> dfft_status_t {
-    Z.in = {kUserOut, 0};
+    Z.in = c2r ? Ref{kWs, 0} : Ref{kUserOut, 0};
     set_side(Z.a.in, ny * nxc, 1, nxc);
-    Z.out = {kWs, 0};
+    Z.out = {kWs, c2r ? W * es : 0};
     set_side(Z.a.out, nxc, 1, nz * nxc);
     Z.a.scale = 1.0;
     return finish_stage(pl, Z, kStrided, (int)nz, nxc, ny, nullptr, nullptr);
@@ -597,7 +632,7 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     A.out = {kUserOut, 0};
     set_side(A.a.out, 1, nxc, ny * nxc);
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, kContig, (int)nxl, ny, nz, nullptr, nullptr));
+    ST(finish_stage(pl, A, pl->r2c ? kContigR2C : kContig, (int)nxl, ny, nz, nullptr, nullptr));
     ST(zpass(B));
     C.in = {kWs, 0};  // columns (l0 = x, l1 = z)
     set_side(C.a.in, nz * nxc, 1, nxc);
@@ -606,20 +641,19 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.a.scale = 1.0;
     ST(finish_stage(pl, C, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
   } else {
-    if (pl->r2c) return fail(DFFT_ERR_UNSUPPORTED, "C2R single-GPU path not built yet");
     A.in = {kUserIn, 0};  // columns (l0 = x, l1 = z)
     set_side(A.a.in, nxc, 1, ny * nxc);
-    A.out = {kUserOut, 0};
+    A.out = c2r ? Ref{kWs, 0} : Ref{kUserOut, 0};
     set_side(A.a.out, nxc, 1, ny * nxc);
     A.a.scale = 1.0;
     ST(finish_stage(pl, A, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
     ST(zpass(B));
-    C.in = {kWs, 0};  // lines (l0 = y, l1 = z) of ws [y][z][x]
+    C.in = {kWs, c2r ? W * es : 0};  // lines (l0 = y, l1 = z) of ws [y][z][x]
     set_side(C.a.in, 1, nz * nxc, nxc);
     C.out = {kUserOut, 0};
     set_side(C.a.out, 1, nxl, ny * nxl);
-    C.a.scale = 1.0 / ((double)nx * (double)ny * (double)nz);
-    ST(finish_stage(pl, C, kContig, (int)nxl, ny, nz, nullptr, nullptr));
+    C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
+    ST(finish_stage(pl, C, c2r ? kContigC2R : kContig, (int)nxl, ny, nz, nullptr, nullptr));
   }
   return DFFT_SUCCESS;
 }
@@ -742,8 +776,8 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     }
   C.out = {kUserOut, 0};
   set_side(C.a.out, 1, nxl, Y1n * nxl);
-  C.a.scale = 1.0 / ((double)g.nx * (double)g.ny * (double)g.nz);
-  ST(finish_stage(pl, C, kContig, (int)nxl, Y1n, Zn, &cseg, nullptr));
+  C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)g.nx * (double)g.ny * (double)g.nz);
+  ST(finish_stage(pl, C, pl->r2c ? kContigC2R : kContig, (int)nxl, Y1n, Zn, &cseg, nullptr));
   return DFFT_SUCCESS;
 }
 
@@ -1259,7 +1293,6 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   ST(validate(P, nx, ny, nz, decomp, &p1, &p2, type, direction));
   bool r2c = type == DFFT_R2C_F32 || type == DFFT_R2C_F64;
   bool f64 = type == DFFT_C2C_F64 || type == DFFT_R2C_F64;
-  if (r2c) return fail(DFFT_ERR_UNSUPPORTED, "R2C/C2R not available in this build yet");
   long long nxc = r2c ? nx / 2 + 1 : nx;
   int Kreq = (int)(flags & 0xff);
   bool overlap = !(flags & DFFT_FLAG_NO_OVERLAP);

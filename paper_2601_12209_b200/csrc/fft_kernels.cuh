@@ -265,6 +265,7 @@ template <typename C> __device__ __forceinline__ void st_out(C* p, C v) {
 struct PassArgs {
   SideMap in, out;
   const void* tw;    // per-pass twiddle tables (complex), sched_twoff layout
+  const void* tw2;   // R2C/C2R: w^k = exp(DIR·2πi·k/(2N)), k < N (the split/merge twiddles)
   long long L0, L1;  // line grid: lines (l0, l1), l0 < L0, l1 < L1 (strided: l0 = the column)
   double scale;      // applied to the outputs of the last pass (1 = none)
 };
@@ -378,7 +379,35 @@ template <int N> struct ContigCfg {
   static constexpr int LS = N + (N >> 4);  // padded line stride in smem
 };
 
-template <typename Real, int N, int DIR>
+// R2C / C2R (reading R8; "exploiting Hermitian symmetry"): a real line of nx = 2N samples
+// is FFT'd as N complex points z[m] = x[2m] + i·x[2m+1].
+//   R2C (MODE 1): Z = DFT_N(z) goes to shared memory; then for k = 0..N
+//       E = (Z[k] + conj Z[N-k]) / 2,  O = (Z[k] - conj Z[N-k]) / (2i),  X[k] = E + w^k O,
+//       w = exp(-2πi/nx), Z[N] ≡ Z[0]; the N+1 bins go out through the side map.
+//   C2R (MODE 2): the first pass loads Z[t] = E + i·O with E = (X[t] + conj X[N-t]) / 2,
+//       O = (X[t] - conj X[N-t])·w^{-t} / 2 (Im X[0] and Im X[N] dropped), and the inverse N-point
+//       FFT yields N·(x[2m] + i·x[2m+1]); the host folds 2/(nx·ny·nz) into `scale`.
+template <typename C> struct SmemZ : GIO<C, true> {  // R2C: the last pass stores Z to shared memory
+  C* zb;
+  __device__ __forceinline__ void store(int t, C v) const { zb[t] = v; }
+};
+template <typename C, int N> struct C2RIO : GIO<C, true> {
+  const C* tw2;
+  __device__ __forceinline__ C load(int t) const {
+    C xt = GIO<C, true>::load(t), xn = GIO<C, true>::load(N - t);
+    if (t == 0) {
+      xt.y = 0;
+      xn.y = 0;
+    }
+    const C w = __ldg(tw2 + t);  // exp(+2πi t / 2N)
+    const C e = {(xt.x + xn.x) * 0.5f, (xt.y - xn.y) * 0.5f};
+    const C d = {(xt.x - xn.x) * 0.5f, (xt.y + xn.y) * 0.5f};
+    const C o = cmul(d, w);
+    return {e.x - o.y, e.y + o.x};  // E + i·O
+  }
+};
+
+template <typename Real, int N, int DIR, int MODE>
 __global__ void __launch_bounds__(ContigCfg<N>::THREADS)
 fft_contig_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
@@ -391,10 +420,37 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
   const bool active = line < a.L0 * a.L1;
   const long long l1 = active ? line / a.L0 : 0;
   const long long l0 = active ? line - l1 * a.L0 : 0;
-  GIO<C, true> io;
-  io.init(a.in, a.out, l0, l1, a.scale);
   ContigSM sm{li * Cfg::LS};
-  stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
+  const C* tw = reinterpret_cast<const C*>(a.tw);
+  if constexpr (MODE == 0) {
+    GIO<C, true> io;
+    io.init(a.in, a.out, l0, l1, a.scale);
+    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+  } else if constexpr (MODE == 1) {
+    SmemZ<C> io;
+    io.init(a.in, a.out, l0, l1, a.scale);
+    C* zb = smem + li * Cfg::LS;
+    io.zb = zb;
+    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+    __syncthreads();
+    if (active) {
+      const C* tw2 = reinterpret_cast<const C*>(a.tw2);
+      for (int k = j; k <= N; k += Cfg::S.T) {
+        const C zk = zb[k == N ? 0 : k], zn = zb[k == 0 ? 0 : N - k];
+        const C e = {(zk.x + zn.x) * 0.5f, (zk.y - zn.y) * 0.5f};
+        const C o = {(zk.y + zn.y) * 0.5f, (zn.x - zk.x) * 0.5f};  // (Z[k] - conj Z[N-k]) / 2i
+        C w;
+        if (k == N) w = {-1, 0};
+        else w = __ldg(tw2 + k);
+        io.GIO<C, true>::store(k, cadd(e, cmul(w, o)));
+      }
+    }
+  } else {
+    C2RIO<C, N> io;
+    io.init(a.in, a.out, l0, l1, a.scale);
+    io.tw2 = reinterpret_cast<const C*>(a.tw2);
+    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+  }
 }
 
 // ------------------------------------------------------------------ strided-axis family

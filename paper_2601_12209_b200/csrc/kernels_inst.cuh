@@ -5,14 +5,14 @@
 namespace dfft {
 
 namespace {
-template <typename Real, int N, int DIR>
+template <typename Real, int N, int DIR, int MODE = 0>
 KernelInfo make_contig() {
   using Cfg = ContigCfg<N>;
   KernelInfo k;
-  k.fn = (const void*)&fft_contig_kernel<Real, N, DIR>;
+  k.fn = (const void*)&fft_contig_kernel<Real, N, DIR, MODE>;
   k.threads = Cfg::THREADS;
   k.per_cta = Cfg::LPC;
-  k.smem = Cfg::S.npass > 1 ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
+  k.smem = (Cfg::S.npass > 1 || MODE == 1) ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
   k.twlen = sched_twlen(Cfg::S);
   return k;
 }
@@ -42,6 +42,8 @@ bool DFFT_LOOKUP(int family, int n, int dir, KernelInfo* out) {
 #define DFFT_CASE(N)                                                                             \
   case N:                                                                                        \
     if (family == kContig) *out = dir < 0 ? make_contig<DFFT_REAL, N, -1>() : make_contig<DFFT_REAL, N, 1>(); \
+    else if (family == kContigR2C) *out = make_contig<DFFT_REAL, N, -1, 1>();                  \
+    else if (family == kContigC2R) *out = make_contig<DFFT_REAL, N, 1, 2>();                   \
     else *out = dir < 0 ? make_strided<DFFT_REAL, N, -1>() : make_strided<DFFT_REAL, N, 1>();    \
     return true;
   switch (n) {

@@ -8,7 +8,7 @@
 
 namespace dfft {
 
-enum Family { kContig = 0, kStrided = 1 };
+enum Family { kContig = 0, kStrided = 1, kContigR2C = 2, kContigC2R = 3 };
 
 struct KernelInfo {
   const void* fn = nullptr;

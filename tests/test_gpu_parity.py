@@ -222,3 +222,76 @@ def test_headline_1024cubed_c64_single_gpu(oracle_mod):
     del y
     d = (z - x).abs().double().pow(2).sum().item()
     assert np.sqrt(d / sx) <= GATE["f32"]
+
+
+# ------------------------------------------------------------------------------ R2C / C2R
+def _r2c_case(oracle_mod, shape, decomp, grid, prec, chunks=0, seed=9):
+    """Forward R2C vs oracle rfft3d; C2R of an arbitrary (non-Hermitian) half spectrum vs the
+    oracle's Hermitian-extension C2R (reading R8); C2R(R2C(x)) round trip."""
+    nx, ny, nz = shape
+    P = grid[0] * grid[1]
+    comm = dfft.Comm.simulated(P, 0) if P > 1 else dfft.Comm.create(nranks=1, rank=0, device=0)
+    dt = "r2c_" + prec
+    fwd = dfft.Plan(comm, shape, decomp, grid, dt, dfft.FORWARD, chunks=chunks)
+    inv = dfft.Plan(comm, shape, decomp, grid, dt, dfft.INVERSE, chunks=chunks)
+    f32 = prec == "f32"
+    xs, ys = [], []
+    for r in range(P):
+        lo, n = fwd.box(0, r)
+        x = fwd.alloc_in(r)
+        inputs.fill_box_cuda(x, seed, shape, lo, n, False)
+        xs.append(x)
+        ys.append(fwd.alloc_out(r))
+    # arbitrary complex half spectrum for the C2R check
+    H = inputs.gen_complex_np(seed + 1, (nx // 2 + 1, ny, nz), f32=f32).astype(np.complex128)
+    hs = []
+    for r in range(P):
+        lo, n = inv.box(0, r)
+        hs.append(_t(box_slice(H, lo, n), prec))
+    zs = [inv.alloc_out(r) for r in range(P)]
+    ws = [inv.alloc_out(r) for r in range(P)]
+    if P > 1:
+        fwd.execute_sim(xs, ys)
+        inv.execute_sim(hs, zs)
+        inv.execute_sim(ys, ws)
+    else:
+        fwd.execute(xs[0], ys[0])
+        inv.execute(hs[0], zs[0])
+        inv.execute(ys[0], ws[0])
+    torch.cuda.synchronize()
+    a = oracle_mod.gen_real(seed, shape, f32=f32)
+    A = oracle_mod.rfft3d(a)
+    Y = np.zeros_like(A)
+    Zc = np.zeros((nz, ny, nx))
+    Wr = np.zeros((nz, ny, nx))
+    for r in range(P):
+        lo, n = fwd.box(1, r)
+        box_slice(Y, lo, n)[...] = ys[r].cpu().numpy()
+        lo, n = inv.box(1, r)
+        box_slice(Zc, lo, n)[...] = zs[r].cpu().numpy()
+        box_slice(Wr, lo, n)[...] = ws[r].cpu().numpy()
+    ef = oracle_mod.rel_l2(Y, A)
+    ec = oracle_mod.rel_l2(Zc, oracle_mod.irfft3d(H, nx))
+    er = oracle_mod.rel_l2(Wr, a)
+    return ef, ec, er
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,decomp,grid,chunks", [
+    ((16, 12, 8), "pencil", (1, 1), 0),
+    ((768, 48, 24), "pencil", (1, 1), 0),
+    ((24, 16, 12), "pencil", (2, 4), 0),    # nx/2+1 = 13 bins split 7/6 (uneven, like cfg5's 193/192)
+    ((24, 16, 12), "pencil", (2, 4), 3),
+    ((48, 24, 12), "slab", (4, 1), 2),
+    ((96, 48, 24), "pencil", (2, 2), 2),
+])
+def test_r2c_c2r(oracle_mod, shape, decomp, grid, chunks, prec):
+    ef, ec, er = _r2c_case(oracle_mod, shape, decomp, grid, prec, chunks)
+    assert ef <= GATE[prec] and ec <= GATE[prec] and er <= GATE[prec], (ef, ec, er)
+    assert ef <= QUALITY[prec] and ec <= QUALITY[prec], (ef, ec, er)
+
+
+def test_cfg5_r2c_768x768x384_f64_single_gpu(oracle_mod):
+    # BASELINE configs[4] shape (fp64, mixed radix 3·2^k) on one GPU: forward vs oracle, round trip
+    ef, ec, er = _r2c_case(oracle_mod, (768, 768, 384), "pencil", (1, 1), "f64", seed=260112209 + 5)
+    assert ef <= 1e-12 and ec <= 1e-12 and er <= 1e-12, (ef, ec, er)
