@@ -84,24 +84,24 @@ bool length_ok(long long n) { return dfft::length_supported(n); }
 // w_{Ns R}^{m r} for r in [1,R), m in [0,Ns) at [(r-1)·Ns + m];  w = exp(dir·2πi/(Ns R)).
 // Computed in long double (x87 80-bit), rounded once (never by recurrence).
 struct TwKey {
-  int n, f64, dir, dev;
+  int n, f64, dir, dev, maxr;
   bool operator<(const TwKey& o) const {
-    return std::tie(n, f64, dir, dev) < std::tie(o.n, o.f64, o.dir, o.dev);
+    return std::tie(n, f64, dir, dev, maxr) < std::tie(o.n, o.f64, o.dir, o.dev, o.maxr);
   }
 };
 std::mutex g_tw_mu;
 std::map<TwKey, void*> g_tw;
 
-dfft_status_t get_twiddles(int n, bool f64, int dir, int dev, const void** out) {
+dfft_status_t get_twiddles(int n, bool f64, int dir, int dev, const void** out, int maxr = 16) {
   std::lock_guard<std::mutex> lk(g_tw_mu);
-  TwKey key{n, f64 ? 1 : 0, dir, dev};
+  TwKey key{n, f64 ? 1 : 0, dir, dev, maxr};
   auto it = g_tw.find(key);
   if (it != g_tw.end()) {
     *out = it->second;
     return DFFT_SUCCESS;
   }
   int rad[kMaxPass];
-  int np = length_schedule(n, rad);
+  int np = length_schedule(n, rad, maxr);
   std::vector<long double> re, im;
   int ns = rad[0];
   for (int p = 1; p < np; ++p) {
@@ -149,7 +149,7 @@ bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
 // R2C/C2R split twiddles: w^k = exp(dir·2πi·k/(2N)), k ∈ [0, N), long double once each.
 dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void** out) {
   std::lock_guard<std::mutex> lk(g_tw_mu);
-  TwKey key{-N, f64 ? 1 : 0, dir, dev};  // negative n: the split table of length N
+  TwKey key{-N, f64 ? 1 : 0, dir, dev, 0};  // negative n: the split table of length N
   auto it = g_tw.find(key);
   if (it != g_tw.end()) {
     *out = it->second;
@@ -218,6 +218,7 @@ struct Stage {
   void* out_tab = nullptr;
   long long grid = 0;
   long long tma_grid = 0;  // persistent grid of the TMA variant (0 = not usable)
+  const void* tw_tma = nullptr;  // twiddles of the TMA variant's radix schedule
   bool empty = false;
 };
 
@@ -384,6 +385,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
       CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       long long tiles = ((L0 + s.k.tma_w - 1) / s.k.tma_w) * L1;
       if (occ > 0) s.tma_grid = std::min<long long>(tiles, (long long)sms * occ);
+      ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, s.k.tma_maxr));
     }
   }
   return DFFT_SUCCESS;
@@ -457,10 +459,17 @@ InvLayout inv_layout(const Geo& g, long long i, long long j, int mode) {
 
 int exch_mode(dfft_plan_t pl) { return pl->p2p ? 2 : pl->ce ? 1 : 0; }
 
-void add_flags(dfft_plan_t pl, const Geo& g, RankPlan& rp, long long end_elems) {
+// The flag block sits at the same byte offset in every rank's window (peers write into it at
+// their own idea of the offset): after the largest rank's data region.
+void add_flags(dfft_plan_t pl, const Geo& g, RankPlan& rp, long long end_elems, bool forward) {
   rp.ws_bytes = (size_t)end_elems * pl->es;
   if (pl->p2p || pl->ce) {
-    pl->flag_off = (rp.ws_bytes + 255) / 256 * 256;
+    long long mx = 0;
+    const int mode = exch_mode(pl);
+    for (long long i = 0; i < g.P1; ++i)
+      for (long long j = 0; j < g.P2; ++j)
+        mx = std::max(mx, forward ? fwd_layout(g, i, j, mode).end : inv_layout(g, i, j, mode).end);
+    pl->flag_off = ((size_t)mx * pl->es + 255) / 256 * 256;
     rp.ws_bytes = pl->flag_off + flag_bytes(g);
   }
 }
@@ -472,7 +481,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const int mode = exch_mode(pl);
   const bool nccl = mode == 0, ce = mode == 1, p2p = mode == 2;
   const FwdLayout L = fwd_layout(g, i, j, mode);
-  add_flags(pl, g, rp, L.end);
+  add_flags(pl, g, rp, L.end, true);
   auto s1off = [&](long long k, long long ip) {  // send1 block (k, i'): [zz][y][x_i'] (NCCL: [y][zz][x])
     long long acc = 0;
     for (long long q = 0; q < ip; ++q)
@@ -665,7 +674,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const int mode = exch_mode(pl);
   const bool nccl = mode == 0, ce = mode == 1, p2p = mode == 2;
   const InvLayout L = inv_layout(g, i, j, mode);
-  add_flags(pl, g, rp, L.end);
+  add_flags(pl, g, rp, L.end, false);
   auto s2off = [&](long long k, long long jp) {  // send2' block (k, j'): [y'][z ∈ Z_j'][xc]
     long long acc = 0;
     for (long long q = 0; q < jp; ++q)
@@ -826,6 +835,7 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
                     (a.out.tstride * (long long)ces) % 16 == 0 && (a.L1 == 1 || (a.out.s1 * (long long)ces) % 16 == 0) &&
                     encode(&tout, a.out.base, a.out.tstride, a.out.s1);
       if (!use_st) tout = tin;  // unused by the non-TST variant
+      a.tw = s.tw_tma;
       void* targs[] = {&tin, &tout, &a};
       CU(cudaLaunchKernel(use_st ? s.k.tma_st_fn : s.k.tma_fn, dim3((unsigned)s.tma_grid), dim3(s.k.tma_threads), targs,
                           s.k.tma_smem, st));
@@ -1600,8 +1610,8 @@ bool length_supported(long long n) {
   KernelInfo k;
   return n > 0 && n <= 4096 && lookup_kernel_f32(kContig, (int)n, -1, &k);
 }
-int length_schedule(int n, int rad[kMaxPass]) {
-  Sched s = make_sched(n);
+int length_schedule(int n, int rad[kMaxPass], int maxr) {
+  Sched s = make_sched(n, maxr);
   for (int p = 0; p < kMaxPass; ++p) rad[p] = s.rad[p];
   return s.npass;
 }

@@ -50,14 +50,15 @@ struct Sched {
   int n, npass, T;
   int rad[kMaxPass];
 };
-// radix-16 passes first, then the 2^k remainder, then 3, 5, 7.
-constexpr Sched make_sched(int n) {
+// radix-MAXR (16 or 32) passes first, then the 2^k remainder, then 3, 5, 7.
+constexpr Sched make_sched(int n, int maxr = 16) {
   Sched s{n, 0, 1, {0, 0, 0, 0, 0, 0, 0, 0}};
   int m = n, odd[kMaxPass] = {0, 0, 0, 0, 0, 0, 0, 0}, nodd = 0;
   for (int p = 7; p >= 3; p -= 2)
     while (m % p == 0) { odd[nodd++] = p; m /= p; }
-  while (m % 16 == 0) { s.rad[s.npass++] = 16; m /= 16; }
-  if (m > 1) s.rad[s.npass++] = m;  // 2, 4 or 8
+  while (m % maxr == 0) { s.rad[s.npass++] = maxr; m /= maxr; }
+  if (m >= 32) { s.rad[s.npass++] = 16; m /= 16; }
+  if (m > 1) s.rad[s.npass++] = m;  // 2, 4, 8 or 16
   for (int q = nodd - 1; q >= 0; --q) s.rad[s.npass++] = odd[q];
   int rmax = 1;
   for (int p = 0; p < s.npass; ++p) rmax = s.rad[p] > rmax ? s.rad[p] : rmax;
@@ -82,6 +83,30 @@ constexpr int sched_twlen(const Sched& s) { return sched_twoff(s, s.npass); }
 #define DFFT_C16_1 0.92387953251128675613
 #define DFFT_S16_1 0.38268343236508977173
 #define DFFT_SQH 0.70710678118654752440
+
+// cos(2πq/32), q ∈ [0, 8]
+__host__ __device__ constexpr double cos32(int q) {
+  return q == 0 ? 1.0 : q == 1 ? 0.98078528040323044913 : q == 2 ? 0.92387953251128675613
+       : q == 3 ? 0.83146961230254523708 : q == 4 ? 0.70710678118654752440 : q == 5 ? 0.55557023301960222474
+       : q == 6 ? 0.38268343236508977173 : q == 7 ? 0.19509032201612826785 : 0.0;
+}
+// a · w_32^q, w_32 = exp(DIR·2πi/32), q a compile-time constant after unrolling
+template <int DIR, typename C>
+__device__ __forceinline__ C tw32(C a, int q) {
+  using Real = decltype(a.x);
+  q &= 31;
+  if (q == 0) return a;
+  if (q == 16) return {-a.x, -a.y};
+  if (q == 8) return mul_i<DIR>(a);
+  if (q == 24) return mul_i<-DIR>(a);
+  // cos/sin of 2πq/32 by quadrant
+  const int r = q & 7, quad = q >> 3;
+  const Real cb = (Real)cos32(r), sb = (Real)cos32(8 - r);
+  Real c = quad == 0 ? cb : quad == 1 ? -sb : quad == 2 ? -cb : sb;
+  Real sn = quad == 0 ? sb : quad == 1 ? cb : quad == 2 ? -sb : -cb;
+  const Real ws = DIR < 0 ? -sn : sn;
+  return {a.x * c - a.y * ws, a.x * ws + a.y * c};
+}
 
 // a · w_R^m with w_R = exp(DIR·2πi/R), R ∈ {2,4,8,16}; m is a compile-time constant after
 // unrolling, so every branch folds.
@@ -172,6 +197,33 @@ template <int DIR, int R, typename C> __device__ __forceinline__ void dft_odd(C*
   v[0] = sum;
 }
 
+template <int DIR, int R, typename C> __device__ __forceinline__ void dft(C* v);
+
+// DFT_{A·B} by one Cooley-Tukey step: n = B·n1 + n2, k = k1 + A·k2,
+//   X[k1 + A k2] = Σ_{n2} w_B^{n2 k2} · [w_{AB}^{n2 k1} · Σ_{n1} x[B n1 + n2] w_A^{n1 k1}]
+template <int DIR, int A, int B, typename C> __device__ __forceinline__ void dft_ct(C* v) {
+  constexpr int R = A * B;
+  C t[R];
+#pragma unroll
+  for (int n2 = 0; n2 < B; ++n2) {
+    C u[A];
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) u[n1] = v[B * n1 + n2];
+    dft<DIR, A>(u);
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) t[n2 * A + k1] = tw32<DIR>(u[k1], (n2 * k1 * (32 / R)) & 31);
+  }
+#pragma unroll
+  for (int k1 = 0; k1 < A; ++k1) {
+    C u[B];
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) u[n2] = t[n2 * A + k1];
+    dft<DIR, B>(u);
+#pragma unroll
+    for (int k2 = 0; k2 < B; ++k2) v[k1 + A * k2] = u[k2];
+  }
+}
+
 // DFT_R in registers, in place, natural order in and out.
 template <int DIR, int R, typename C> __device__ __forceinline__ void dft(C* v) {
   if constexpr (R == 1) {
@@ -218,6 +270,8 @@ template <int DIR, int R, typename C> __device__ __forceinline__ void dft(C* v) 
     for (int k1 = 0; k1 < 4; ++k1)
 #pragma unroll
       for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+  } else if constexpr (R == 32) {
+    dft_ct<DIR, 4, 8>(v);
   } else {
     static_assert(R == 3 || R == 5 || R == 7, "unsupported radix");
     dft_odd<DIR, R>(v);
@@ -273,10 +327,10 @@ struct PassArgs {
 // --------------------------------------------------------------------------------- Stockham core
 // One thread's part of the passes of one line.  IO supplies the global side:
 //   C load(int t)  and  void store(int t, C v); SM maps t to a shared-memory slot.
-template <typename C, int N, int DIR, int P, class IO, class SM>
+template <typename C, int N, int DIR, int P, int MAXR = 16, class IO, class SM>
 __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, const C* __restrict__ tw, int j,
                                               bool active) {
-  constexpr Sched S = make_sched(N);
+  constexpr Sched S = make_sched(N, MAXR);
   constexpr int R = S.rad[P];
   constexpr int NR = N / R;
   constexpr int Ns = sched_ns(S, P);
@@ -328,7 +382,7 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
   }
   if constexpr (!LAST) {
     __syncthreads();
-    stockham_pass<C, N, DIR, P + 1>(io, sm, smem, tw, j, active);
+    stockham_pass<C, N, DIR, P + 1, MAXR>(io, sm, smem, tw, j, active);
   }
 }
 
@@ -549,8 +603,14 @@ constexpr int largest_divisor_le(int n, int cap) {
 }
 
 template <typename Real, int N> struct TmaCfg {
-  static constexpr Sched S = make_sched(N);
   static constexpr int ES = (int)sizeof(Real) * 2;
+#ifndef DFFT_TMA_MAXR32
+#define DFFT_TMA_MAXR32 1
+#endif
+  // fp32 lines of >= 512 points use radix-32 passes (1024 = 32·32: two passes, fewer barriers and
+  // less shared-memory traffic per tile); fp64 keeps radix 16 (register budget)
+  static constexpr int MAXR = (DFFT_TMA_MAXR32 && ES == 8 && N >= 512 && N % 32 == 0) ? 32 : 16;
+  static constexpr Sched S = make_sched(N, MAXR);
 #ifndef DFFT_TMA_ROWB
 #define DFFT_TMA_ROWB 64
 #endif
@@ -661,7 +721,7 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     io.bytes = kBytes;
     mbar_wait(&bars[s], parity);
     StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
-    stockham_pass<C, N, DIR, 0>(io, sm, work, reinterpret_cast<const C*>(a.tw), j, active);
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, work, reinterpret_cast<const C*>(a.tw), j, active);
     if constexpr (TST) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
       __syncthreads();

@@ -32,6 +32,7 @@ KernelInfo make_strided() {
     k.tma_threads = TC::THREADS;
     k.tma_w = TC::W;
     k.tma_boxr = TC::BOXR;
+    k.tma_maxr = TC::MAXR;
     k.tma_smem = TC::SMEM;
   }
   return k;

@@ -19,7 +19,7 @@ struct KernelInfo {
   // strided family only: persistent TMA-staged variant (null if not instantiable for n)
   const void* tma_fn = nullptr;
   const void* tma_st_fn = nullptr;  // same, with TMA stores (unsegmented output side)
-  int tma_threads = 0, tma_w = 0, tma_boxr = 0;
+  int tma_threads = 0, tma_w = 0, tma_boxr = 0, tma_maxr = 16;  // tma_maxr: its radix schedule
   size_t tma_smem = 0;
 };
 
@@ -34,6 +34,6 @@ bool lookup_kernel_f32(int family, int n, int dir, KernelInfo* out);
 bool lookup_kernel_f64(int family, int n, int dir, KernelInfo* out);
 bool length_supported(long long n);
 // radix schedule of length n (for twiddle generation): returns npass, fills rad[]
-int length_schedule(int n, int rad[kMaxPass]);
+int length_schedule(int n, int rad[kMaxPass], int maxr = 16);
 
 }  // namespace dfft

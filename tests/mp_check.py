@@ -29,7 +29,15 @@ def gather(t, plan, which):
     return objs
 
 
+def log(*a):
+    if int(os.environ.get("RANK", "0")) == 0 or os.environ.get("MP_VERBOSE"):
+        print(f"[rank {os.environ.get('RANK')}]", *a, flush=True)
+
+
 def main():
+    import faulthandler
+
+    faulthandler.dump_traceback_later(int(os.environ.get("MP_WATCHDOG", "240")), exit=True)
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -45,10 +53,43 @@ def main():
         oracle.build()
     dist.barrier()
     n_ok = 0
+    # R2C / C2R across ranks (uneven nx/2+1 split), every transport
+    for decomp, grid in grids[:2]:
+        shape = (48, 24, 12)
+        results = []
+        for exch in ("ce", "p2p", "nccl"):
+            log("r2c", decomp, grid, exch)
+            fwd = dfft.Plan(comm, shape, decomp, grid, "r2c_f64", dfft.FORWARD, exchange=exch)
+            inv = dfft.Plan(comm, shape, decomp, grid, "r2c_f64", dfft.INVERSE, exchange=exch)
+            lo, n = fwd.box(0)
+            x = fwd.alloc_in()
+            inputs.fill_box_cuda(x, 13, shape, lo, n, False)
+            y, z = fwd.alloc_out(), inv.alloc_out()
+            for _ in range(2):
+                fwd.execute(x, y)
+                inv.execute(y, z)
+            torch.cuda.synchronize()
+            results.append((gather(y, fwd, 1), gather(z, inv, 1)))
+            fwd.destroy()
+            inv.destroy()
+        if rank == 0:
+            a = oracle.gen_real(13, shape)
+            A = oracle.rfft3d(a)
+            for ys, zs in results:
+                Y, Z = np.zeros_like(A), np.zeros_like(a)
+                for lo, n, arr in ys:
+                    box_slice(Y, lo, n)[...] = arr
+                for lo, n, arr in zs:
+                    box_slice(Z, lo, n)[...] = arr
+                ef, er = oracle.rel_l2(Y, A), oracle.rel_l2(Z, a)
+                assert ef <= 1e-12 and er <= 1e-12, ("r2c", decomp, grid, ef, er)
+            n_ok += 1
+        dist.barrier()
     for decomp, grid, shape, prec in cases:
         results = []
         for chunks, overlap, exch in ((0, True, "ce"), (1, True, "ce"), (3, True, "ce"), (0, True, "p2p"),
                                       (3, True, "p2p"), (0, True, "nccl"), (3, True, "nccl"), (2, False, "nccl")):
+            log(decomp, grid, shape, prec, chunks, overlap, exch)
             fwd = dfft.Plan(comm, shape, decomp, grid, "c2c_" + prec, dfft.FORWARD, chunks=chunks, overlap=overlap,
                             exchange=exch)
             inv = dfft.Plan(comm, shape, decomp, grid, "c2c_" + prec, dfft.INVERSE, chunks=chunks, overlap=overlap,
