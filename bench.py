@@ -45,9 +45,10 @@ def parse():
     p.add_argument("--grid-p", default="", help="process grid P1,P2 (default by N)")
     p.add_argument("--chunks", type=int, default=0)
     p.add_argument("--no-overlap", action="store_true")
-    p.add_argument("--exchange", default="ce", choices=["ce", "p2p", "nccl"],
-                   help="ce: copy engines into peers' IPC windows; p2p: FFT epilogues store into the windows; "
-                        "nccl: grouped send/recv")
+    p.add_argument("--exchange", default="auto", choices=["auto", "ce", "p2p", "hybrid", "nccl"],
+                   help="p2p: FFT epilogues store into peers' IPC windows over NVLink; ce: copy engines move "
+                        "packed blocks into the windows; hybrid: p2p for the x-FFT, ce elsewhere; nccl: grouped "
+                        "send/recv; auto: p2p if P1 > 1 else ce")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=260112209 + 4)

@@ -70,14 +70,17 @@ typedef enum { DFFT_FORWARD = -1, DFFT_INVERSE = 1 } dfft_direction_t;
  *   DFFT_FLAG_NO_OVERLAP: one stream, each exchange completes before the next stage starts
  *             (the "SimpleMPIFFT" static-barrier ablation of P:438).  Results are bitwise
  *             identical to the pipelined schedule.
- *   Exchange transport for P > 1 (same kernels and bitwise-identical results in every mode):
- *     default:  the FFT epilogue packs each off-rank block into a local send block and the
- *               copy engine of the comm stream writes it into the receiving peer's workspace
- *               (a CUDA IPC window exchanged at plan creation) over NVLink; flag words in the
- *               windows (system-scope release stores, cuStreamWaitValue32) order producer and
- *               consumer per chunk.  No SM time is spent on transfers.
- *     DFFT_FLAG_FUSED_STORE: the FFT epilogue stores each off-rank element straight into the
- *               peer's window (no send block; the exchange is inside the FFT kernel).
+ *   Exchange transport for P > 1 (same kernels and bitwise-identical results in every mode).
+ *   Every rank's workspace is a CUDA IPC window exchanged at plan creation; flag words in the
+ *   windows (system-scope release stores, cuStreamWaitValue32) order producer and consumer per
+ *   chunk, and consumer -> producer for buffer reuse across executes.
+ *     DFFT_FLAG_FUSED_STORE: each FFT epilogue stores its off-rank elements straight into the
+ *               peers' windows over NVLink (pack + send + unpack fused into the FFT's stores).
+ *     DFFT_FLAG_CE: the FFT epilogue packs each off-rank block into a local send block and the
+ *               comm stream's copy engine moves it into the receiver's window, K chunks
+ *               pipelined against the FFTs (no SM time on transfers).
+ *     DFFT_FLAG_HYBRID: fused stores for the forward x-FFT (long x-runs), CE elsewhere.
+ *     default: fused stores when p1 > 1, CE with 8 chunks for a 1×P2 grid (measured best).
  *     DFFT_FLAG_NCCL: grouped ncclSend/ncclRecv of the send blocks (baseline/ablation).
  *   Env DFFT_EXCHANGE=ce|p2p|nccl overrides.
  */
@@ -85,6 +88,8 @@ typedef enum { DFFT_FORWARD = -1, DFFT_INVERSE = 1 } dfft_direction_t;
 #define DFFT_FLAG_NO_OVERLAP ((uint64_t)1 << 8)
 #define DFFT_FLAG_NCCL ((uint64_t)1 << 9)
 #define DFFT_FLAG_FUSED_STORE ((uint64_t)1 << 10)
+#define DFFT_FLAG_CE ((uint64_t)1 << 11)
+#define DFFT_FLAG_HYBRID ((uint64_t)1 << 12)
 
 int dfft_version(void);
 const char* dfft_status_string(dfft_status_t status);

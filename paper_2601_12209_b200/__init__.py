@@ -25,6 +25,8 @@ TYPES = {"c2c_f32": 1, "c2c_f64": 2, "r2c_f32": 3, "r2c_f64": 4}
 FLAG_NO_OVERLAP = 1 << 8
 FLAG_NCCL = 1 << 9
 FLAG_FUSED_STORE = 1 << 10
+FLAG_CE = 1 << 11
+FLAG_HYBRID = 1 << 12
 
 # symbols include/dfft.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -166,10 +168,10 @@ class Plan:
 
     def __init__(self, comm: Comm, shape: Sequence[int], decomp: str = "pencil", grid: Sequence[int] = (1, 1),
                  dtype: str = "c2c_f32", direction: int = FORWARD, chunks: int = 0, overlap: bool = True,
-                 exchange: str = "ce"):
+                 exchange: str = "auto"):
         self.comm, self.shape, self.dtype, self.direction = comm, tuple(int(s) for s in shape), dtype, direction
         self.decomp = decomp
-        flags = flag_chunks(chunks) | (0 if overlap else FLAG_NO_OVERLAP) | {"nccl": FLAG_NCCL, "p2p": FLAG_FUSED_STORE, "ce": 0}[exchange]
+        flags = flag_chunks(chunks) | (0 if overlap else FLAG_NO_OVERLAP) | {"nccl": FLAG_NCCL, "p2p": FLAG_FUSED_STORE, "ce": FLAG_CE, "hybrid": FLAG_HYBRID, "auto": 0}[exchange]
         h = _vp()
         d = SLAB if decomp == "slab" else PENCIL
         _check(lib().dfft_plan_create(ctypes.byref(h), comm.h, *self.shape, d, int(grid[0]), int(grid[1]),

@@ -145,6 +145,7 @@ CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP
                                      : getenv("DFFT_TMA_PROMO128") ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
+bool g_use_tma2 = getenv("DFFT_TMA2") != nullptr;  // two-group variant: correct, not faster
 
 // R2C/C2R split twiddles: w^k = exp(dir·2πi·k/(2N)), k ∈ [0, N), long double once each.
 dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void** out) {
@@ -184,6 +185,10 @@ dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
     CU(cudaFuncSetAttribute(k->tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     CU(cudaFuncSetAttribute(k->tma_st_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
   }
+  if (k->tma2_fn && k->tma2_smem > 48 * 1024) {
+    CU(cudaFuncSetAttribute(k->tma2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma2_smem));
+    CU(cudaFuncSetAttribute(k->tma2_st_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma2_smem));
+  }
   return DFFT_SUCCESS;
 }
 
@@ -218,6 +223,7 @@ struct Stage {
   void* out_tab = nullptr;
   long long grid = 0;
   long long tma_grid = 0;  // persistent grid of the TMA variant (0 = not usable)
+  int tma_variant = 0;     // 1 = single-group TMA kernel, 2 = two-group in-place kernel
   const void* tw_tma = nullptr;  // twiddles of the TMA variant's radix schedule
   bool empty = false;
 };
@@ -233,7 +239,8 @@ struct Xfer {
 struct Exchange {
   int comm = 0;  // 0 = row (P1 group), 1 = column (P2 group)
   std::vector<Xfer> sends, recvs;     // NCCL mode: the blocks to move
-  std::vector<int> peers;             // P2P mode: global ranks of the other group members
+  std::vector<int> peers;             // P2P / CE modes: global ranks of the other group members
+  bool fused = false;                 // the producing FFT stored straight into the peers' windows
   bool empty() const { return sends.empty() && recvs.empty() && peers.empty(); }
 };
 
@@ -273,6 +280,7 @@ struct dfft_plan_s {
   // store straight into the peers' receive regions over NVLink; flags in the windows order it
   bool p2p = false;
   bool ce = false;                   // copy-engine exchange (cudaMemcpyAsync into the peers' windows)
+  bool hybrid = false;               // CE, except the forward's first exchange: fused x-FFT stores
   std::vector<void*> peer_ws;        // by global rank (own rank = own workspace), null if not a peer
   size_t flag_off = 0;               // byte offset of the flag block in every workspace
   unsigned int epoch = 0;            // executes so far (flag values)
@@ -375,17 +383,27 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   if (is_contig(family)) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
   else s.grid = ((L0 + s.k.per_cta - 1) / s.k.per_cta) * L1;
   if (s.grid >= (1LL << 31)) return fail(DFFT_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", s.grid);
-  if (family == kStrided && s.k.tma_fn && g_use_tma && !in_tab && tensor_map_encoder()) {
+  if (family == kStrided && (s.k.tma_fn || s.k.tma2_fn) && g_use_tma && !in_tab && tensor_map_encoder()) {
     const long long es = (long long)pl->es;
     bool ok = s.a.in.s0 == 1 && (s.a.in.tstride * es) % 16 == 0 && (L1 == 1 || (s.a.in.s1 * es) % 16 == 0) &&
               2 * L0 < (1LL << 32) && L1 < (1LL << 31);
     if (ok) {
+      const bool v2 = g_use_tma2 && s.k.tma2_fn;
+      const void* fn = v2 ? s.k.tma2_fn : s.k.tma_fn;
+      const int thr = v2 ? s.k.tma2_threads : s.k.tma_threads, w = v2 ? s.k.tma2_w : s.k.tma_w;
+      const size_t sm = v2 ? s.k.tma2_smem : s.k.tma_smem;
       int occ = 0, dev = pl->comm->device, sms = 0;
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, s.k.tma_fn, s.k.tma_threads, s.k.tma_smem));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, thr, sm));
       CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      long long tiles = ((L0 + s.k.tma_w - 1) / s.k.tma_w) * L1;
-      if (occ > 0) s.tma_grid = std::min<long long>(tiles, (long long)sms * occ);
-      ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, s.k.tma_maxr));
+      long long tiles = ((L0 + w - 1) / w) * L1;
+      if (occ > 0) {
+        s.tma_variant = v2 ? 2 : 1;
+        s.tma_grid = std::min<long long>(tiles, (long long)sms * occ);
+        ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, v2 ? s.k.tma2_maxr : s.k.tma_maxr));
+      }
+      if (getenv("DFFT_DEBUG"))
+        fprintf(stderr, "dfft: strided n=%d L0=%lld L1=%lld tma variant %d grid %lld (occ %d, tma2_fn %p)\n", n, L0, L1,
+                s.tma_variant, s.tma_grid, occ, s.k.tma2_fn);
     }
   }
   return DFFT_SUCCESS;
@@ -431,10 +449,10 @@ inline size_t flag_bytes(const Geo& g) { return (size_t)4 * 2 * 2 * g.K * g.P1 *
 struct FwdLayout {
   long long S1, R1, S2, R2, end;
 };
-FwdLayout fwd_layout(const Geo& g, long long i, long long j, int mode /*0 nccl 1 ce 2 p2p*/) {
+FwdLayout fwd_layout(const Geo& g, long long i, long long j, int mode /*0 nccl 1 ce 2 p2p 3 hybrid*/) {
   FwdLayout L{};
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
-  const long long S1n = mode == 2 ? 0 : Y1n * Zn * (g.nxc - Xn);
+  const long long S1n = (mode == 2 || mode == 3) ? 0 : Y1n * Zn * (g.nxc - Xn);
   const long long S2n = mode == 2 ? 0 : Zn * Xn * (g.ny - Y3n);
   L.S1 = 0;
   L.R1 = S1n;
@@ -457,7 +475,7 @@ InvLayout inv_layout(const Geo& g, long long i, long long j, int mode) {
   return L;
 }
 
-int exch_mode(dfft_plan_t pl) { return pl->p2p ? 2 : pl->ce ? 1 : 0; }
+int exch_mode(dfft_plan_t pl) { return pl->p2p ? 2 : pl->hybrid ? 3 : pl->ce ? 1 : 0; }
 
 // The flag block sits at the same byte offset in every rank's window (peers write into it at
 // their own idea of the offset): after the largest rank's data region.
@@ -465,7 +483,7 @@ void add_flags(dfft_plan_t pl, const Geo& g, RankPlan& rp, long long end_elems, 
   rp.ws_bytes = (size_t)end_elems * pl->es;
   if (pl->p2p || pl->ce) {
     long long mx = 0;
-    const int mode = exch_mode(pl);
+    const int mode = (!forward && exch_mode(pl) == 3) ? 1 : exch_mode(pl);
     for (long long i = 0; i < g.P1; ++i)
       for (long long j = 0; j < g.P2; ++j)
         mx = std::max(mx, forward ? fwd_layout(g, i, j, mode).end : inv_layout(g, i, j, mode).end);
@@ -479,7 +497,9 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long i = rp.i, j = rp.j, K = g.K, es = (long long)pl->es;
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
   const int mode = exch_mode(pl);
-  const bool nccl = mode == 0, ce = mode == 1, p2p = mode == 2;
+  // per exchange: E1 fused (P2P, hybrid) or packed; E2 fused (P2P) or packed (NCCL, CE, hybrid)
+  const bool nccl = mode == 0, p2p = mode == 2, hyb = mode == 3, ce = mode == 1 || hyb;
+  const bool f1 = p2p || hyb;
   const FwdLayout L = fwd_layout(g, i, j, mode);
   add_flags(pl, g, rp, L.end, true);
   auto s1off = [&](long long k, long long ip) {  // send1 block (k, i'): [zz][y][x_i'] (NCCL: [y][zz][x])
@@ -508,12 +528,12 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     set_side(A.a.in, 1, nxl, Y1n * nxl);
     A.out = {kWs, 0};
     A.out_bases.push_back({kWs, 0});
-    if (p2p)  // selector 1 + i' = rank (i', j)'s window (own window for i' == i)
+    if (f1)  // selector 1 + i' = rank (i', j)'s window (own window for i' == i)
       for (long long ip = 0; ip < g.P1; ++ip) A.out_bases.push_back({kPeer, 0, row_rank(g, ip, j)});
     Segs aseg;
     for (long long ip = 0; ip < g.P1; ++ip) {
       const long long xl = g.Xlo(ip), xn = g.Xn(ip);
-      if (p2p) {
+      if (f1) {
         const FwdLayout Lr = fwd_layout(g, ip, j, mode);
         aseg.push_back({1 + (int)ip, xl, xn, Lr.R1 + g.ny * z0 * xn + g.Y1lo(i) * xn, 1, xn, g.ny * xn});
       } else if (ip == i) {
@@ -529,10 +549,11 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     // ---- exchange 1 (row group)
     Exchange& E1 = rp.E1[k];
     E1.comm = 0;
+    E1.fused = f1;
     for (long long ip = 0; ip < g.P1; ++ip) {
       if (ip == i) continue;
       if (!nccl) E1.peers.push_back(row_rank(g, ip, j));
-      if (p2p) continue;
+      if (f1) continue;
       const long long xn = g.Xn(ip);
       Xfer x{(int)ip, {kWs, s1off(k, ip) * es}, (size_t)(Y1n * zc * xn * es)};
       if (ce) {  // zc rows of Y1n·xn elements into [zz][y][x] of the receiver
@@ -576,6 +597,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     // ---- exchange 2 (column group)
     Exchange& E2 = rp.E2[k];
     E2.comm = 1;
+    E2.fused = p2p;
     for (long long jp = 0; jp < g.P2; ++jp) {
       if (jp == j) continue;
       if (!nccl) E2.peers.push_back(col_rank(g, i, jp));
@@ -671,7 +693,7 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
 dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long i = rp.i, j = rp.j, K = g.K, es = (long long)pl->es;
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
-  const int mode = exch_mode(pl);
+  const int mode = exch_mode(pl) == 3 ? 1 : exch_mode(pl);  // hybrid: the inverse is all CE
   const bool nccl = mode == 0, ce = mode == 1, p2p = mode == 2;
   const InvLayout L = inv_layout(g, i, j, mode);
   add_flags(pl, g, rp, L.end, false);
@@ -723,6 +745,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     // first exchange of the inverse = T2⁻¹ on the column group
     Exchange& E1 = rp.E1[k];
     E1.comm = 1;
+    E1.fused = p2p;
     for (long long jp = 0; jp < g.P2; ++jp) {
       if (jp == j) continue;
       if (!nccl) E1.peers.push_back(col_rank(g, i, jp));
@@ -761,6 +784,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     // second exchange of the inverse = T1⁻¹ on the row group
     Exchange& E2 = rp.E2[k];
     E2.comm = 0;
+    E2.fused = p2p;
     for (long long ip = 0; ip < g.P1; ++ip) {
       if (ip == i) continue;
       if (!nccl) E2.peers.push_back(row_rank(g, ip, j));
@@ -823,7 +847,9 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
       cuuint64_t dims[3] = {(cuuint64_t)(2 * a.L0), (cuuint64_t)s.n, (cuuint64_t)a.L1};
       cuuint64_t strides[2] = {(cuuint64_t)tstride * ces,
                                (cuuint64_t)(a.L1 > 1 ? lstride * ces : 16 * ((tstride * ces * s.n + 15) / 16))};
-      cuuint32_t box[3] = {(cuuint32_t)(2 * s.k.tma_w), (cuuint32_t)s.k.tma_boxr, 1};
+      const bool v2 = s.tma_variant == 2;
+      cuuint32_t box[3] = {(cuuint32_t)(2 * (v2 ? s.k.tma2_w : s.k.tma_w)), (cuuint32_t)(v2 ? s.k.tma2_r0 : s.k.tma_boxr),
+                           1};
       cuuint32_t estr[3] = {1, 1, 1};
       return tensor_map_encoder()(tm, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -837,8 +863,12 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
       if (!use_st) tout = tin;  // unused by the non-TST variant
       a.tw = s.tw_tma;
       void* targs[] = {&tin, &tout, &a};
-      CU(cudaLaunchKernel(use_st ? s.k.tma_st_fn : s.k.tma_fn, dim3((unsigned)s.tma_grid), dim3(s.k.tma_threads), targs,
-                          s.k.tma_smem, st));
+      if (s.tma_variant == 2)
+        CU(cudaLaunchKernel(use_st ? s.k.tma2_st_fn : s.k.tma2_fn, dim3((unsigned)s.tma_grid), dim3(s.k.tma2_threads),
+                            targs, s.k.tma2_smem, st));
+      else
+        CU(cudaLaunchKernel(use_st ? s.k.tma_st_fn : s.k.tma_fn, dim3((unsigned)s.tma_grid), dim3(s.k.tma_threads),
+                            targs, s.k.tma_smem, st));
       return DFFT_SUCCESS;
     }
   }
@@ -1027,27 +1057,38 @@ dfft_status_t execute_ce(dfft_plan_t pl, const Ctx& cx, cudaStream_t user) {
   CU(cudaEventRecord(pl->ev_fork, user));
   CU(cudaStreamWaitEvent(sc, pl->ev_fork, 0));
   CU(cudaStreamWaitEvent(sm, pl->ev_fork, 0));
+  // a fused exchange is produced inside the FFT kernel: WAR wait before it, ready signal after it,
+  // both on the compute stream; a CE exchange is a copy on the comm stream after the kernel
   auto do_A = [&](size_t k) -> dfft_status_t {
+    const Exchange& x = rp.E1[k];
+    if (x.fused && ep > 1) ST(p2p_wait(pl, 1, 0, (int)k, x.peers, ep - 1, sc));
     ST(launch_p(pl, 0, rp.A[k], cx, sc));
+    if (x.fused) return p2p_signal(pl, 0, 0, (int)k, x.peers, ep, sc);
     CU(cudaEventRecord(pl->evA[k], sc));
     CU(cudaStreamWaitEvent(sm, pl->evA[k], 0));
     size_t slot = 0;
     ST(prof_begin(pl, 1, sm, &slot));
-    ST(exchange_ce(pl, 0, (int)k, rp.E1[k], cx, ep, sm));
+    ST(exchange_ce(pl, 0, (int)k, x, cx, ep, sm));
     return prof_end(pl, slot, sm);
   };
   ST(do_A(0));
   for (size_t k = 0; k < K; ++k) {
     if (k + 1 < K) ST(do_A(k + 1));
+    const Exchange& x2 = rp.E2[k];
     ST(p2p_wait(pl, 0, 0, (int)k, rp.E1[k].peers, ep, sc));  // peers' blocks of chunk k have landed
+    if (x2.fused && ep > 1) ST(p2p_wait(pl, 1, 1, (int)k, x2.peers, ep - 1, sc));
     ST(launch_p(pl, 2, rp.B[k], cx, sc));
     ST(p2p_signal(pl, 1, 0, (int)k, rp.E1[k].peers, ep, sc));  // done reading my first receive region
-    CU(cudaEventRecord(pl->evB[k], sc));
-    CU(cudaStreamWaitEvent(sm, pl->evB[k], 0));
-    size_t slot = 0;
-    ST(prof_begin(pl, 3, sm, &slot));
-    ST(exchange_ce(pl, 1, (int)k, rp.E2[k], cx, ep, sm));
-    ST(prof_end(pl, slot, sm));
+    if (x2.fused) {
+      ST(p2p_signal(pl, 0, 1, (int)k, x2.peers, ep, sc));
+    } else {
+      CU(cudaEventRecord(pl->evB[k], sc));
+      CU(cudaStreamWaitEvent(sm, pl->evB[k], 0));
+      size_t slot = 0;
+      ST(prof_begin(pl, 3, sm, &slot));
+      ST(exchange_ce(pl, 1, (int)k, x2, cx, ep, sm));
+      ST(prof_end(pl, slot, sm));
+    }
   }
   for (size_t k = 0; k < K; ++k) ST(p2p_wait(pl, 0, 1, (int)k, rp.E2[k].peers, ep, sc));
   ST(launch_p(pl, 4, rp.C, cx, sc));
@@ -1312,11 +1353,18 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   const char* exch_env = getenv("DFFT_EXCHANGE");
   auto env_is = [&](const char* v) { return exch_env && strcmp(exch_env, v) == 0; };
   const bool nccl_mode = comm->sim || P == 1 || (flags & DFFT_FLAG_NCCL) || env_is("nccl");
-  const bool p2p_mode = !nccl_mode && ((flags & DFFT_FLAG_FUSED_STORE) || env_is("p2p"));
+  const bool want_ce = (flags & DFFT_FLAG_CE) || env_is("ce");
+  const bool want_fused = (flags & DFFT_FLAG_FUSED_STORE) || env_is("p2p");
+  const bool want_hybrid = (flags & DFFT_FLAG_HYBRID) || env_is("hybrid");
+  // automatic choice (measured r01, 1024^3 c64): a 1×P2 grid (only the second exchange) is best
+  // with the copy engine and 8 chunks; grids with P1 > 1 are best with fused epilogue stores
+  const bool auto_fused = !want_ce && !want_fused && !want_hybrid && p1 > 1;
+  const bool p2p_mode = !nccl_mode && (want_fused || auto_fused);
+  const bool ce_only = !nccl_mode && !p2p_mode && !want_hybrid;
   const bool ce_mode = !nccl_mode && !p2p_mode;
   // chunks pipeline the transfers against the FFTs; with fused stores the transfer happens
   // inside the FFT kernels themselves, so one chunk is the default there
-  long long K = Kreq > 0 ? Kreq : (P > 1 && !p2p_mode ? 4 : 1);
+  long long K = Kreq > 0 ? Kreq : (P > 1 && !p2p_mode ? (nccl_mode ? 4 : 8) : 1);
   K = std::max<long long>(1, std::min<long long>(K, kmax));
   if (P == 1) K = 1;  // nothing to overlap
 
@@ -1338,6 +1386,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   // exchange over NVLink peer memory unless asked for NCCL (flag or DFFT_EXCHANGE=nccl)
   pl->p2p = p2p_mode;
   pl->ce = ce_mode;
+  pl->hybrid = ce_mode && !ce_only;
   if ((pl->p2p || pl->ce) && !stream_wait_value32())
     return fail(DFFT_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
   Geo g{nx, ny, nz, nxc, p1, p2, K};

@@ -355,7 +355,7 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
   }
   // every read of this pass is done before anything is overwritten (also makes a single-pass
   // transform safe in place)
-  if constexpr (P > 0 || LAST || IO::kSyncAfterLoad) __syncthreads();
+  if constexpr (P > 0 || LAST || IO::kSyncAfterLoad) io.bar();
   if constexpr (P == 0 && IO::kSyncAfterLoad) io.after_load();  // e.g. refill the drained TMA stage
   // ---- twiddle, butterfly, scatter
 #pragma unroll
@@ -381,7 +381,7 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
     }
   }
   if constexpr (!LAST) {
-    __syncthreads();
+    io.bar();
     stockham_pass<C, N, DIR, P + 1, MAXR>(io, sm, smem, tw, j, active);
   }
 }
@@ -392,6 +392,7 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
 template <typename C, bool UNIT_T = false> struct GIO {
   static constexpr bool kSyncAfterLoad = false;
   __device__ __forceinline__ void after_load() {}
+  __device__ __forceinline__ void bar() const { __syncthreads(); }  // barrier among the threads of a tile
   const C* __restrict__ in;
   C* __restrict__ out;
   const SideMap* mi;
@@ -614,8 +615,11 @@ template <typename Real, int N> struct TmaCfg {
 #ifndef DFFT_TMA_ROWB
 #define DFFT_TMA_ROWB 64
 #endif
+#ifndef DFFT_TMA_MINTHR
+#define DFFT_TMA_MINTHR 256
+#endif
   static constexpr int W0 = DFFT_TMA_ROWB / ES;  // row segment of a tile (bytes / element size)
-  static constexpr int W = S.T * W0 >= 256 ? W0 : 256 / S.T;
+  static constexpr int W = S.T * W0 >= DFFT_TMA_MINTHR ? W0 : DFFT_TMA_MINTHR / S.T;
   static constexpr int THREADS = S.T * W;
   static constexpr int NS = 2;
   static constexpr int BOXR = largest_divisor_le(N, 256);
@@ -635,7 +639,7 @@ template <typename C, int W, bool TST> struct TmaIO : GIO<C> {
   int c;
   // refill: thread 0 issues the TMA for the tile NS steps ahead into the drained stage
   const void* tmap;
-  uint64_t* bar;
+  uint64_t* mbar;
   C* stage_ptr;
   int next_c0, next_l1, nbox, boxr;
   uint32_t bytes;
@@ -652,9 +656,9 @@ template <typename C, int W, bool TST> struct TmaIO : GIO<C> {
   __device__ __forceinline__ void after_load() {
     if (refill && threadIdx.x == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(bar, bytes);
+      mbar_expect_tx(mbar, bytes);
       for (int q = 0; q < nbox; ++q)
-        tma_load_3d(stage_ptr + q * boxr * W, tmap, next_c0, q * boxr, next_l1, bar);
+        tma_load_3d(stage_ptr + q * boxr * W, tmap, next_c0, q * boxr, next_l1, mbar);
     }
   }
 };
@@ -709,7 +713,7 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     const long long next = tile + (long long)Cfg::NS * gridDim.x;
     io.refill = next < total;
     io.tmap = &tmap;
-    io.bar = &bars[s];
+    io.mbar = &bars[s];
     io.stage_ptr = stages + s * Cfg::STAGE_ELEMS;
     {
       const long long nl1 = next / ntile;
@@ -733,6 +737,144 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     }
   }
   if (TST && threadIdx.x == 0) bulk_wait0();
+}
+
+// ------------------------------------------------------------------ strided family, 2 warp groups
+// Two independent warp groups per CTA each run their own tile (named barriers, no CTA-wide sync),
+// so one group's barrier stalls are covered by the other's work (the single-group TMA kernel was
+// barrier-bound at 8-16 warps/SM, ncu r01).  The FFT runs in place in the stage buffer: TMA lands
+// each box of R0 rows at a padded offset, giving the conflict-free layout t·W + c + (t/R0)·PAD
+// directly, so no separate work buffer is needed and three stage buffers fit: two being
+// computed.  Tile it (it-th of this CTA) is processed by group it % 2 in that group's buffer; the
+// group refills its buffer with its next tile as soon as its TMA store has read it, and the other
+// group's compute covers the load latency.
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <typename Real, int N> struct Tma2Cfg {
+  static constexpr int ES = (int)sizeof(Real) * 2;
+  static constexpr int MAXR = (ES == 8 && N >= 512 && N % 32 == 0) ? 32 : 16;
+  static constexpr Sched S = make_sched(N, MAXR);
+  static constexpr int W0 = 64 / ES;
+  // 64 B rows, widened (power of 2) only for short lines so a group has >= 128 threads
+  static constexpr int W = S.T * W0 >= 128 ? W0 : (S.T * 2 * W0 >= 128 ? 2 * W0 : S.T * 4 * W0 >= 128 ? 4 * W0 : 8 * W0);
+  static constexpr int GT = S.T * W;  // threads per group
+#ifndef DFFT_TMA2_GROUPS
+#define DFFT_TMA2_GROUPS 2
+#endif
+  static constexpr int NG = DFFT_TMA2_GROUPS;
+  static constexpr int THREADS = NG * GT;
+  // dense [t][W] stage (TMA destinations must be 128 B aligned, which rules out the 64-B-mod-128
+  // padding; the in-place pass-0 scatter then has 2-way bank conflicts on 64 B rows)
+  static constexpr int R0 = largest_divisor_le(N, 256);  // rows per TMA box
+  static constexpr int PAD = 0;
+  static constexpr int NBOX = N / R0;
+  static constexpr int BOX_ELEMS = R0 * W;
+  static constexpr int STAGE_ELEMS = NBOX * BOX_ELEMS;
+  // one stage buffer per group: each group refills its own buffer, so the mbarrier phases of a
+  // buffer advance in step with its single consumer (buffers shared round-robin between groups
+  // let one group run two phases ahead and pass a parity wait spuriously)
+  static constexpr int NSTAGE = NG;
+  static constexpr size_t SMEM = (size_t)NSTAGE * STAGE_ELEMS * ES + NSTAGE * 8 + 16;
+  static constexpr bool OK = S.npass >= 2 && THREADS <= 1024 && SMEM <= 227 * 1024 && 2 * W <= 256 &&
+                             R0 <= 256 && N % R0 == 0 && THREADS <= 512;
+};
+
+template <typename C, int W, int R0, int PAD, bool TST> struct Tma2IO : GIO<C> {
+  static constexpr bool kSyncAfterLoad = true;  // the gather and the in-place writes of pass 0
+  C* buf;
+  int c, gbar, gthreads;
+  __device__ __forceinline__ int sidx(int t) const { return t * W + c; }
+  __device__ __forceinline__ C load(int t) const { return buf[sidx(t)]; }
+  __device__ __forceinline__ void store(int t, C v) const {
+    if constexpr (TST) {
+      if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
+      buf[sidx(t)] = v;
+    } else {
+      GIO<C>::store(t, v);
+    }
+  }
+  __device__ __forceinline__ void bar() const { named_bar(gbar, gthreads); }
+};
+
+template <typename Real, int N, int DIR, bool TST>
+__global__ void __launch_bounds__(Tma2Cfg<Real, N>::THREADS)
+fft_strided_tma2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
+                        const __grid_constant__ PassArgs a) {
+  using C = typename CT<Real>::type;
+  using Cfg = Tma2Cfg<Real, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* stages = reinterpret_cast<C*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + Cfg::NSTAGE * Cfg::STAGE_ELEMS);
+  const int g = threadIdx.x / Cfg::GT;        // warp group
+  const int lt = threadIdx.x - g * Cfg::GT;   // thread within the group
+  const int c = lt % Cfg::W;
+  const int j = lt / Cfg::W;
+  const bool leader = lt == 0;
+  const long long ntile = (a.L0 + Cfg::W - 1) / Cfg::W;
+  const long long total = ntile * a.L1;
+  constexpr uint32_t kBytes = (uint32_t)(Cfg::NBOX * Cfg::R0 * Cfg::W * Cfg::ES);
+  auto coords = [&](long long tile, int& c0, int& l1) {
+    const long long q = tile / ntile;
+    l1 = (int)q;
+    c0 = (int)((tile - q * ntile) * Cfg::W * 2);  // TMA coordinates are in reals
+  };
+  auto issue = [&](long long tile, int b) {
+    int c0, l1;
+    coords(tile, c0, l1);
+    C* dst = stages + b * Cfg::STAGE_ELEMS;
+    mbar_expect_tx(&full[b], kBytes);
+    for (int q = 0; q < Cfg::NBOX; ++q) tma_load_3d(dst + q * Cfg::BOX_ELEMS, &tmap, c0, q * Cfg::R0, l1, &full[b]);
+  };
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < Cfg::NSTAGE; ++b) mbar_init(&full[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int b = 0; b < Cfg::NSTAGE; ++b) {
+      const long long tile = blockIdx.x + (long long)b * gridDim.x;
+      if (tile < total) issue(tile, b);
+    }
+  }
+  __syncthreads();
+  for (int it = g;; it += Cfg::NG) {
+    const long long tile = blockIdx.x + (long long)it * gridDim.x;
+    if (tile >= total) break;
+    const int b = it % Cfg::NSTAGE;
+    const uint32_t parity = (uint32_t)((it / Cfg::NSTAGE) & 1);
+    int c0, l1i;
+    coords(tile, c0, l1i);
+    const long long l0 = (long long)(c0 / 2) + c;
+    const bool active = l0 < a.L0;
+    Tma2IO<C, Cfg::W, Cfg::R0, Cfg::PAD, TST> io;
+    io.init(a.in, a.out, active ? l0 : 0, l1i, a.scale);
+    io.buf = stages + b * Cfg::STAGE_ELEMS;
+    io.c = c;
+    io.gbar = 1 + g;
+    io.gthreads = Cfg::GT;
+    mbar_wait(&full[b], parity);
+    StridedSM<Cfg::W, 1, 0> sm{c};
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, io.buf, reinterpret_cast<const C*>(a.tw), j, active);
+    if constexpr (TST) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    named_bar(1 + g, Cfg::GT);  // the tile is complete (in the buffer, or stored from registers)
+    if (leader) {
+      if constexpr (TST) {
+        for (int q = 0; q < Cfg::NBOX; ++q)
+          tma_store_3d(&omap, c0, q * Cfg::R0, l1i, io.buf + q * Cfg::BOX_ELEMS);
+        bulk_commit();
+      }
+      const long long next = tile + (long long)Cfg::NSTAGE * gridDim.x;
+      if (next < total) {
+#ifdef DFFT_TMA2_WAIT_FULL
+        if constexpr (TST) bulk_wait0();
+#else
+        if constexpr (TST) bulk_wait_read0();  // the store has read the buffer
+#endif
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(next, b);
+      }
+    }
+  }
+  if (TST && threadIdx.x % Cfg::GT == 0) bulk_wait0();
 }
 
 }  // namespace dfft

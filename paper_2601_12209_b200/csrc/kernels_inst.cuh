@@ -35,6 +35,17 @@ KernelInfo make_strided() {
     k.tma_maxr = TC::MAXR;
     k.tma_smem = TC::SMEM;
   }
+  using T2 = Tma2Cfg<Real, N>;
+  if constexpr (T2::OK) {
+    k.tma2_fn = (const void*)&fft_strided_tma2_kernel<Real, N, DIR, false>;
+    k.tma2_st_fn = (const void*)&fft_strided_tma2_kernel<Real, N, DIR, true>;
+    k.tma2_threads = T2::THREADS;
+    k.tma2_w = T2::W;
+    k.tma2_r0 = T2::R0;
+    k.tma2_box = T2::BOX_ELEMS;
+    k.tma2_maxr = T2::MAXR;
+    k.tma2_smem = T2::SMEM;
+  }
   return k;
 }
 }  // namespace

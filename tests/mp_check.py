@@ -57,7 +57,7 @@ def main():
     for decomp, grid in grids[:2]:
         shape = (48, 24, 12)
         results = []
-        for exch in ("ce", "p2p", "nccl"):
+        for exch in ("auto", "hybrid", "ce", "p2p", "nccl"):
             log("r2c", decomp, grid, exch)
             fwd = dfft.Plan(comm, shape, decomp, grid, "r2c_f64", dfft.FORWARD, exchange=exch)
             inv = dfft.Plan(comm, shape, decomp, grid, "r2c_f64", dfft.INVERSE, exchange=exch)
@@ -87,7 +87,8 @@ def main():
         dist.barrier()
     for decomp, grid, shape, prec in cases:
         results = []
-        for chunks, overlap, exch in ((0, True, "ce"), (1, True, "ce"), (3, True, "ce"), (0, True, "p2p"),
+        for chunks, overlap, exch in ((0, True, "auto"), (3, True, "hybrid"), (0, True, "ce"), (1, True, "ce"),
+                                      (3, True, "ce"), (0, True, "p2p"),
                                       (3, True, "p2p"), (0, True, "nccl"), (3, True, "nccl"), (2, False, "nccl")):
             log(decomp, grid, shape, prec, chunks, overlap, exch)
             fwd = dfft.Plan(comm, shape, decomp, grid, "c2c_" + prec, dfft.FORWARD, chunks=chunks, overlap=overlap,
