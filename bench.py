@@ -278,12 +278,20 @@ def main():
             tr = json.load(f)
         traffic = tr.get(f"{shape[0]}x{shape[1]}x{shape[2]}_{args.precision}_{grid[0]}x{grid[1]}", {}).get(
             f"{tag_k}_{ph_k}")
+        if traffic is not None:
+            traffic = traffic / (cnt_k / args.steps)  # per launch
     except Exception:
         pass
-    stage_names = {"fwd": {"stage_A": "x-FFT (contig, fused T1 pack)", "stage_B": "y-FFT (strided, fused pack)",
-                           "stage_C": "z-FFT (strided, in place)"},
-                   "inv": {"stage_A": "z-IFFT (strided, fused T2 pack)", "stage_B": "y-IFFT (strided, fused pack)",
-                           "stage_C": "x-IFFT (contig, fused unpack, 1/N)"}}
+    if grid[0] * grid[1] == 1:  # single GPU: forward x, z, y; inverse y, z, x
+        stage_names = {"fwd": {"stage_A": "x-FFT (contig)", "stage_B": "z-FFT (strided TMA, writes [y][z][x])",
+                               "stage_C": "y-FFT (strided TMA)"},
+                       "inv": {"stage_A": "y-IFFT (strided TMA)", "stage_B": "z-IFFT (strided TMA)",
+                               "stage_C": "x-IFFT (contig, 1/N)"}}
+    else:
+        stage_names = {"fwd": {"stage_A": "x-FFT (contig, fused T1 pack)", "stage_B": "y-FFT (strided, fused T2 pack)",
+                               "stage_C": "z-FFT (strided)"},
+                       "inv": {"stage_A": "z-IFFT (strided, fused T2 pack)", "stage_B": "y-IFFT (strided, fused pack)",
+                               "stage_C": "x-IFFT (contig, fused unpack, 1/N)"}}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic,
                 "kernel": f"{tag_k} {stage_names[tag_k][ph_k]}", "peak_kind": peak_kind,
