@@ -387,6 +387,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
     const long long es = (long long)pl->es;
     bool ok = s.a.in.s0 == 1 && (s.a.in.tstride * es) % 16 == 0 && (L1 == 1 || (s.a.in.s1 * es) % 16 == 0) &&
               2 * L0 < (1LL << 32) && L1 < (1LL << 31);
+    if (s.a.in.bw > 0) ok = ok && s.k.tma_fn && s.a.in.bw % s.k.tma_w == 0 && (s.a.in.mT * s.a.in.s1 * es) % 16 == 0;
     if (ok) {
       const bool v2 = g_use_tma2 && s.k.tma2_fn;
       const void* fn = v2 ? s.k.tma2_fn : s.k.tma_fn;
@@ -412,6 +413,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
 struct Geo {
   long long nx, ny, nz, nxc;
   long long P1, P2, K;
+  long long wy = 1, wz = 1;  // column-tile widths of the strided kernels for ny / nz (blocked layouts)
   long long Xlo(long long i) const { return blo(nxc, P1, i); }
   long long Xn(long long i) const { return blk(nxc, P1, i); }
   long long Y1lo(long long i) const { return blo(ny, P1, i); }
@@ -449,9 +451,17 @@ inline size_t flag_bytes(const Geo& g) { return (size_t)4 * 2 * 2 * g.K * g.P1 *
 struct FwdLayout {
   long long S1, R1, S2, R2, end;
 };
+inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
 FwdLayout fwd_layout(const Geo& g, long long i, long long j, int mode /*0 nccl 1 ce 2 p2p 3 hybrid*/) {
   FwdLayout L{};
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
+  if (mode == 2) {  // fused: [R1 recv1 [zc][y][x] | R2 column-blocked [xt][z][y'][wy]]
+    L.S1 = L.R1 = 0;
+    L.S2 = L.R2 = g.ny * Zn * Xn;
+    L.end = L.R2 + round_up(Xn, g.wy) * g.nz * Y3n;
+    return L;
+  }
   const long long S1n = (mode == 2 || mode == 3) ? 0 : Y1n * Zn * (g.nxc - Xn);
   const long long S2n = mode == 2 ? 0 : Zn * Xn * (g.ny - Y3n);
   L.S1 = 0;
@@ -467,6 +477,14 @@ struct InvLayout {
 InvLayout inv_layout(const Geo& g, long long i, long long j, int mode) {
   InvLayout L{};
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
+  if (mode == 2) {  // fused: [R2' blocked [xt][y][z][wz] | R1' blocked per source [i][xt][z][y][wy]]
+    L.S2 = L.R2 = 0;
+    L.S1 = L.R1 = round_up(Xn, g.wz) * g.ny * Zn;
+    long long r1 = 0;
+    for (long long q = 0; q < g.P1; ++q) r1 += round_up(g.Xn(q), g.wy) * Zn * Y1n;
+    L.end = L.R1 + r1;
+    return L;
+  }
   L.S2 = 0;
   L.R2 = mode == 2 ? 0 : Y3n * Xn * (g.nz - Zn);
   L.S1 = L.R2 + g.ny * Zn * Xn;
@@ -581,9 +599,9 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Segs bseg;
     for (long long jp = 0; jp < g.P2; ++jp) {
       const long long yl = g.Y3lo(jp), yn = g.Y3n(jp);
-      if (p2p) {
+      if (p2p) {  // receiver's R2 [xt][z][y'][wy]: a warp's rows of one block are contiguous
         const FwdLayout Lr = fwd_layout(g, i, jp, mode);
-        bseg.push_back({2 + (int)jp, yl, yn, Lr.R2 + (g.Zlo(j) + z0) * Xn, g.nz * Xn, 1, Xn});
+        bseg.push_back({2 + (int)jp, yl, yn, Lr.R2 + (g.Zlo(j) + z0) * yn * g.wy, g.wy, 1, yn * g.wy});
       } else if (jp == j) {
         if (nccl) bseg.push_back({1, yl, yn, (g.Zlo(j) + z0) * Y3n * Xn, Xn, 1, Y3n * Xn});
         else bseg.push_back({0, yl, yn, L.R2 + (g.Zlo(j) + z0) * Xn, g.nz * Xn, 1, Xn});
@@ -591,6 +609,10 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
         if (nccl) bseg.push_back({0, yl, yn, s2off(k, jp), Xn, 1, yn * Xn});
         else bseg.push_back({0, yl, yn, s2off(k, jp), zc * Xn, 1, Xn});
       }
+    }
+    if (p2p) {
+      B.a.out.bw = (int)g.wy;
+      B.a.out.mT = g.nz;
     }
     B.a.scale = 1.0;
     ST(finish_stage(pl, B, kStrided, (int)g.ny, Xn, zc, nullptr, &bseg));
@@ -624,6 +646,11 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   if (nccl) {
     C.in = {kUserOut, 0};
     set_side(C.a.in, Y3n * Xn, 1, Xn);
+  } else if (p2p) {  // R2 [xt][z][y'][wy]
+    C.in = {kWs, L.R2 * es};
+    set_side(C.a.in, Y3n * g.wy, 1, g.wy);
+    C.a.in.bw = (int)g.wy;
+    C.a.in.mT = g.nz * Y3n;
   } else {
     C.in = {kWs, L.R2 * es};
     set_side(C.a.in, Xn, 1, g.nz * Xn);
@@ -731,14 +758,18 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Segs aseg;
     for (long long jp = 0; jp < g.P2; ++jp) {
       const long long zl = g.Zlo(jp), zn = g.Zn(jp);
-      if (p2p) {
+      if (p2p) {  // receiver's R2' [xt][y][z][wz]
         const InvLayout Lr = inv_layout(g, i, jp, mode);
-        aseg.push_back({1 + (int)jp, zl, zn, Lr.R2 + g.ny * zn * x0 + g.Y3lo(j) * zn * xc, xc, 1, zn * xc});
+        aseg.push_back({1 + (int)jp, zl, zn, Lr.R2 + g.Y3lo(j) * zn * g.wz, g.wz, 1, zn * g.wz});
       } else if (jp == j) {
         aseg.push_back({0, zl, zn, L.R2 + g.ny * Zn * x0 + g.Y3lo(j) * Zn * xc, xc, 1, Zn * xc});
       } else {
         aseg.push_back({0, zl, zn, s2off(k, jp), xc, 1, zn * xc});
       }
+    }
+    if (p2p) {
+      A.a.out.bw = (int)g.wz;
+      A.a.out.mT = g.ny;
     }
     A.a.scale = 1.0;
     ST(finish_stage(pl, A, kStrided, (int)g.nz, xc, Y3n, nullptr, &aseg));
@@ -763,6 +794,12 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Stage& B = rp.B[k];
     B.in = {kWs, (L.R2 + g.ny * Zn * x0) * es};
     set_side(B.a.in, Zn * xc, 1, xc);
+    if (p2p) {  // R2' [xt][y][z][wz] (p2p runs one chunk: x0 = 0)
+      B.in = {kWs, L.R2 * es};
+      set_side(B.a.in, Zn * g.wz, 1, g.wz);
+      B.a.in.bw = (int)g.wz;
+      B.a.in.mT = g.ny * Zn;
+    }
     B.out = {kWs, 0};
     B.out_bases.push_back({kWs, 0});
     if (p2p)
@@ -770,14 +807,20 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Segs bseg;
     for (long long ip = 0; ip < g.P1; ++ip) {
       const long long yl = g.Y1lo(ip), yn = g.Y1n(ip);
-      if (p2p) {
+      if (p2p) {  // receiver's R1' [source i][xt][z][y][wy]
         const InvLayout Lr = inv_layout(g, ip, j, mode);
-        bseg.push_back({1 + (int)ip, yl, yn, r1off(Lr, ip, i, k), xc, 1, yn * xc});
+        long long src = 0;
+        for (long long q = 0; q < i; ++q) src += round_up(g.Xn(q), g.wy) * Zn * yn;
+        bseg.push_back({1 + (int)ip, yl, yn, Lr.R1 + src, g.wy, 1, yn * g.wy});
       } else if (ip == i) {
         bseg.push_back({0, yl, yn, r1off(L, i, i, k), xc, 1, Y1n * xc});
       } else {
         bseg.push_back({0, yl, yn, s1off(k, ip), xc, 1, yn * xc});
       }
+    }
+    if (p2p) {
+      B.a.out.bw = (int)g.wy;
+      B.a.out.mT = Zn;
     }
     B.a.scale = 1.0;
     ST(finish_stage(pl, B, kStrided, (int)g.ny, xc, Zn, nullptr, &bseg));
@@ -802,11 +845,23 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   Stage& C = rp.C;
   C.in = {kWs, 0};
   Segs cseg;
-  for (long long is = 0; is < g.P1; ++is)
-    for (long long k = 0; k < K; ++k) {
-      const long long xcs = g.xc(is, k);
-      if (xcs > 0) cseg.push_back({0, g.Xlo(is) + g.x0(is, k), xcs, r1off(L, i, is, k), 1, xcs, Y1n * xcs});
+  if (p2p) {  // R1' [source][xt][z][y][wy]: one segment per (source, column block)
+    long long src = L.R1;
+    for (long long is = 0; is < g.P1; ++is) {
+      const long long xn = g.Xn(is), nb = (xn + g.wy - 1) / g.wy;
+      for (long long xb = 0; xb < nb; ++xb) {
+        const long long tn = std::min(g.wy, xn - xb * g.wy);
+        cseg.push_back({0, g.Xlo(is) + xb * g.wy, tn, src + xb * Zn * Y1n * g.wy, 1, g.wy, Y1n * g.wy});
+      }
+      src += nb * g.wy * Zn * Y1n;
     }
+  } else {
+    for (long long is = 0; is < g.P1; ++is)
+      for (long long k = 0; k < K; ++k) {
+        const long long xcs = g.xc(is, k);
+        if (xcs > 0) cseg.push_back({0, g.Xlo(is) + g.x0(is, k), xcs, r1off(L, i, is, k), 1, xcs, Y1n * xcs});
+      }
+  }
   C.out = {kUserOut, 0};
   set_side(C.a.out, 1, nxl, Y1n * nxl);
   C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)g.nx * (double)g.ny * (double)g.nz);
@@ -855,9 +910,22 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                   g_tma_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
+    auto encode4 = [&](CUtensorMap* tm, const SideMap& m) {  // column-blocked: (2·bw reals, n, L1, blocks)
+      const long long nb = (a.L0 + m.bw - 1) / m.bw;
+      cuuint64_t dims[4] = {(cuuint64_t)(2 * m.bw), (cuuint64_t)s.n, (cuuint64_t)a.L1, (cuuint64_t)nb};
+      cuuint64_t strides[3] = {(cuuint64_t)m.tstride * ces, (cuuint64_t)m.s1 * ces, (cuuint64_t)(m.mT * m.s1) * ces};
+      cuuint32_t box[4] = {(cuuint32_t)(2 * s.k.tma_w), (cuuint32_t)s.k.tma_boxr, 1, 1};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      return tensor_map_encoder()(tm, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, m.base,
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  g_tma_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
     CUtensorMap tin, tout;
-    if (encode(&tin, a.in.base, a.in.tstride, a.in.s1)) {
-      bool use_st = g_tma_store && a.out.ttab == nullptr && a.out.s0 == 1 && ((uintptr_t)a.out.base & 15) == 0 &&
+    const bool in_ok = a.in.bw > 0 ? (s.tma_variant == 1 && encode4(&tin, a.in))
+                                   : encode(&tin, a.in.base, a.in.tstride, a.in.s1);
+    if (in_ok) {
+      bool use_st = g_tma_store && a.out.ttab == nullptr && a.out.bw == 0 && a.out.s0 == 1 &&
+                    ((uintptr_t)a.out.base & 15) == 0 &&
                     (a.out.tstride * (long long)ces) % 16 == 0 && (a.L1 == 1 || (a.out.s1 * (long long)ces) % 16 == 0) &&
                     encode(&tout, a.out.base, a.out.tstride, a.out.s1);
       if (!use_st) tout = tin;  // unused by the non-TST variant
@@ -1365,6 +1433,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   // chunks pipeline the transfers against the FFTs; with fused stores the transfer happens
   // inside the FFT kernels themselves, so one chunk is the default there
   long long K = Kreq > 0 ? Kreq : (P > 1 && !p2p_mode ? (nccl_mode ? 4 : 8) : 1);
+  if (p2p_mode) K = 1;  // fused stores into column-blocked windows: one chunk
   K = std::max<long long>(1, std::min<long long>(K, kmax));
   if (P == 1) K = 1;  // nothing to overlap
 
@@ -1390,6 +1459,13 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   if ((pl->p2p || pl->ce) && !stream_wait_value32())
     return fail(DFFT_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
   Geo g{nx, ny, nz, nxc, p1, p2, K};
+  {  // column-tile widths of the strided kernels (the TMA kernel's when it exists)
+    KernelInfo ky, kz;
+    if (f64 ? lookup_kernel_f64(kStrided, (int)ny, direction, &ky) : lookup_kernel_f32(kStrided, (int)ny, direction, &ky))
+      g.wy = ky.tma_fn ? ky.tma_w : ky.per_cta;
+    if (f64 ? lookup_kernel_f64(kStrided, (int)nz, direction, &kz) : lookup_kernel_f32(kStrided, (int)nz, direction, &kz))
+      g.wz = kz.tma_fn ? kz.tma_w : kz.per_cta;
+  }
 
   if (!comm->sim && P > 1) {
     // collective consistency check: every rank must pass identical arguments

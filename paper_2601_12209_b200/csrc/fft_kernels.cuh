@@ -296,7 +296,24 @@ struct SideMap {
   void* bases[kMaxBases];     // segmented: base pointer per selector (local buffers, peers' windows)
   const SegEnt* ttab;         // nullptr => unsegmented
   long long tstride, s0, s1;  // unsegmented strides (elements)
+  // column-blocked layouts (bw > 0): column l0 lives in block l0/bw at position l0%bw, and the
+  // block index strides like mT lines of l1:  off(t) + (l0%bw)·s0 + ((l0/bw)·mT + l1)·s1.
+  // A warp's rows of one block are then contiguous (256 B pieces over NVLink).
+  int bw;
+  long long mT;
 };
+
+// effective (l0, l1) of a side for column l0 / line l1 (blocked layouts fold the block into l1)
+__device__ __forceinline__ void side_lines(const SideMap& m, long long l0, long long l1, long long& e0, long long& e1) {
+  if (m.bw > 0) {
+    const long long xb = l0 / m.bw;
+    e0 = l0 - xb * m.bw;
+    e1 = xb * m.mT + l1;
+  } else {
+    e0 = l0;
+    e1 = l1;
+  }
+}
 
 template <typename C>
 __device__ __forceinline__ C* seg_ptr(const SideMap& m, int t, long long l0, long long l1) {
@@ -397,28 +414,28 @@ template <typename C, bool UNIT_T = false> struct GIO {
   C* __restrict__ out;
   const SideMap* mi;
   const SideMap* mo;
-  long long l0, l1;
-  long long lin, lout;  // unsegmented sides: l0·s0 + l1·s1
+  long long i0, i1, o0, o1;  // effective (l0, l1) per side
+  long long lin, lout;       // unsegmented sides: l0·s0 + l1·s1
   decltype(C{}.x) scale;
   __device__ __forceinline__ void init(const SideMap& i, const SideMap& o, long long l0_, long long l1_, double sc) {
     in = reinterpret_cast<const C*>(i.base);
     out = reinterpret_cast<C*>(o.base);
     mi = &i;
     mo = &o;
-    l0 = l0_;
-    l1 = l1_;
-    lin = l0_ * i.s0 + l1_ * i.s1;
-    lout = l0_ * o.s0 + l1_ * o.s1;
+    side_lines(i, l0_, l1_, i0, i1);
+    side_lines(o, l0_, l1_, o0, o1);
+    lin = i0 * i.s0 + i1 * i.s1;
+    lout = o0 * o.s0 + o1 * o.s1;
     scale = (decltype(C{}.x))sc;
   }
   __device__ __forceinline__ C load(int t) const {
     if (mi->ttab == nullptr) return UNIT_T ? in[lin + t] : in[(long long)t * mi->tstride + lin];
-    return *seg_ptr<const C>(*mi, t, l0, l1);
+    return *seg_ptr<const C>(*mi, t, i0, i1);
   }
   __device__ __forceinline__ void store(int t, C v) const {
     if (scale != 1) { v.x *= scale; v.y *= scale; }
     if (mo->ttab == nullptr) st_out(out + (UNIT_T ? lout + t : (long long)t * mo->tstride + lout), v);
-    else st_out(seg_ptr<C>(*mo, t, l0, l1), v);
+    else st_out(seg_ptr<C>(*mo, t, o0, o1), v);
   }
 };
 
@@ -588,6 +605,21 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0,
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const void* tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+// a tile's box: 3D (reals, row, l1) or, for a column-blocked input, 4D (reals in block, row, l1,
+// block) — the host encodes the matching tensor map
+__device__ __forceinline__ void tma_load_tile(void* dst, const void* tmap, int bw, int c0, int row, int l1,
+                                              uint64_t* bar) {
+  if (bw > 0) tma_load_4d(dst, tmap, c0 % (2 * bw), row, l1, c0 / (2 * bw), bar);
+  else tma_load_3d(dst, tmap, c0, row, l1, bar);
+}
 __device__ __forceinline__ void tma_store_3d(const void* tmap, int c0, int c1, int c2, const void* src) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tmap), "r"(c0),
                "r"(c1), "r"(c2), "r"(smem_u32(src))
@@ -641,7 +673,7 @@ template <typename C, int W, bool TST> struct TmaIO : GIO<C> {
   const void* tmap;
   uint64_t* mbar;
   C* stage_ptr;
-  int next_c0, next_l1, nbox, boxr;
+  int next_c0, next_l1, nbox, boxr, in_bw;
   uint32_t bytes;
   bool refill;
   __device__ __forceinline__ C load(int t) const { return stage[t * W + c]; }
@@ -658,7 +690,7 @@ template <typename C, int W, bool TST> struct TmaIO : GIO<C> {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(mbar, bytes);
       for (int q = 0; q < nbox; ++q)
-        tma_load_3d(stage_ptr + q * boxr * W, tmap, next_c0, q * boxr, next_l1, mbar);
+        tma_load_tile(stage_ptr + q * boxr * W, tmap, in_bw, next_c0, q * boxr, next_l1, mbar);
     }
   }
 };
@@ -686,7 +718,8 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     const int c0 = (int)((tile - l1 * ntile) * Cfg::W * 2);
     mbar_expect_tx(&bars[s], kBytes);
     for (int q = 0; q < Cfg::NBOX; ++q)
-      tma_load_3d(stages + s * Cfg::STAGE_ELEMS + q * Cfg::BOXR * Cfg::W, &tmap, c0, q * Cfg::BOXR, (int)l1, &bars[s]);
+      tma_load_tile(stages + s * Cfg::STAGE_ELEMS + q * Cfg::BOXR * Cfg::W, &tmap, a.in.bw, c0, q * Cfg::BOXR, (int)l1,
+                    &bars[s]);
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::NS; ++s) mbar_init(&bars[s], 1);
@@ -722,6 +755,7 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     }
     io.nbox = Cfg::NBOX;
     io.boxr = Cfg::BOXR;
+    io.in_bw = a.in.bw;
     io.bytes = kBytes;
     mbar_wait(&bars[s], parity);
     StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
@@ -825,7 +859,8 @@ fft_strided_tma2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_c
     coords(tile, c0, l1);
     C* dst = stages + b * Cfg::STAGE_ELEMS;
     mbar_expect_tx(&full[b], kBytes);
-    for (int q = 0; q < Cfg::NBOX; ++q) tma_load_3d(dst + q * Cfg::BOX_ELEMS, &tmap, c0, q * Cfg::R0, l1, &full[b]);
+    for (int q = 0; q < Cfg::NBOX; ++q)
+      tma_load_tile(dst + q * Cfg::BOX_ELEMS, &tmap, a.in.bw, c0, q * Cfg::R0, l1, &full[b]);
   };
   if (threadIdx.x == 0) {
     for (int b = 0; b < Cfg::NSTAGE; ++b) mbar_init(&full[b], 1);
