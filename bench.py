@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--exchange", default="auto", choices=["auto", "ce", "p2p", "hybrid", "nccl"],
                    help="p2p: FFT epilogues store into peers' IPC windows over NVLink; ce: copy engines move "
                         "packed blocks into the windows; hybrid: p2p for the x-FFT, ce elsewhere; nccl: grouped "
-                        "send/recv; auto: p2p if P1 > 1 else ce")
+                        "send/recv; auto: p2p")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=260112209 + 4)

@@ -146,6 +146,7 @@ CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP
                                                                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
 bool g_use_tma2 = getenv("DFFT_TMA2") != nullptr;  // two-group variant: correct, not faster
+bool g_use_bulk = getenv("DFFT_NO_BULK") == nullptr;  // bulk-copy epilogue for blocked segmented outputs
 
 // R2C/C2R split twiddles: w^k = exp(dir·2πi·k/(2N)), k ∈ [0, N), long double once each.
 dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void** out) {
@@ -184,6 +185,7 @@ dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
   if (k->tma_fn && k->tma_smem > 48 * 1024) {
     CU(cudaFuncSetAttribute(k->tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     CU(cudaFuncSetAttribute(k->tma_st_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
+    CU(cudaFuncSetAttribute(k->tma_bk_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
   }
   if (k->tma2_fn && k->tma2_smem > 48 * 1024) {
     CU(cudaFuncSetAttribute(k->tma2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma2_smem));
@@ -223,6 +225,9 @@ struct Stage {
   void* out_tab = nullptr;
   long long grid = 0;
   long long tma_grid = 0;  // persistent grid of the TMA variant (0 = not usable)
+  int tma_occ = 0;         // resident CTAs per SM of the TMA variant
+  int sm_cap = 0;          // > 0: run the persistent variant on at most this many SMs (leaves the
+                           // rest to a concurrently running HBM-bound stage)
   int tma_variant = 0;     // 1 = single-group TMA kernel, 2 = two-group in-place kernel
   const void* tw_tma = nullptr;  // twiddles of the TMA variant's radix schedule
   bool empty = false;
@@ -252,6 +257,7 @@ struct RankPlan {
   std::vector<Stage> A, B;  // per chunk
   std::vector<Exchange> E1, E2;  // first / second exchange (each names its comm group)
   Stage C;
+  std::vector<Stage> Cc;  // B→C pipelined plans (dfft_plan_s::bc): stage C per chunk, C unused
 };
 
 }  // namespace
@@ -281,6 +287,10 @@ struct dfft_plan_s {
   bool p2p = false;
   bool ce = false;                   // copy-engine exchange (cudaMemcpyAsync into the peers' windows)
   bool hybrid = false;               // CE, except the forward's first exchange: fused x-FFT stores
+  // fused stores with both exchanges remote (P1 > 1 and P2 > 1): stage A runs whole and stages B
+  // and C run in K chunks along the axis both leave local (x forward, z inverse), so the HBM-bound
+  // C(k) overlaps the NVLink-bound B(k+1)
+  bool bc = false;
   std::vector<void*> peer_ws;        // by global rank (own rank = own workspace), null if not a peer
   size_t flag_off = 0;               // byte offset of the flag block in every workspace
   unsigned int epoch = 0;            // executes so far (flag values)
@@ -342,6 +352,36 @@ bool linearize(const Segs& segs, long long n, Ref& base, const std::vector<Ref>&
   return true;
 }
 
+// tile-group width of a persistent strided stage (PassArgs::g0), overridable for A/B runs
+int tile_g0(int dflt, const char* env) {
+  const char* v = getenv(env);
+  return v ? atoi(v) : dflt;
+}
+
+// Segments of equal width B (unit t-stride, one base, same line strides) laid end to end at a
+// constant block stride: an unsegmented t-blocked side (SideMap::tb), no per-t table.
+bool linearize_tblocked(const Segs& segs, Ref& base, const std::vector<Ref>& bases, SideMap& m, long long es) {
+  if (segs.size() < 2) return false;
+  const Seg& f = segs[0];
+  const long long B = f.tn, BS = segs[1].off0 - f.off0;
+  if (f.tlo != 0 || B <= 0 || B > (1 << 30)) return false;
+  for (size_t q = 0; q < segs.size(); ++q) {
+    const Seg& g = segs[q];
+    if (g.sel != f.sel || g.s0 != f.s0 || g.s1 != f.s1 || g.ts != 1 || g.tn != B || g.tlo != (long long)q * B ||
+        g.off0 != f.off0 + (long long)q * BS)
+      return false;
+  }
+  Ref b = bases[f.sel];
+  b.off += f.off0 * es;
+  base = b;
+  m.tstride = 1;
+  m.s0 = f.s0;
+  m.s1 = f.s1;
+  m.tb = (int)B;
+  m.tbs = BS;
+  return true;
+}
+
 inline void set_side(SideMap& m, long long ts, long long s0, long long s1) {
   m.tstride = ts;
   m.s0 = s0;
@@ -355,6 +395,9 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   if (s.in_bases.size() > (size_t)kMaxBases || s.out_bases.size() > (size_t)kMaxBases)
     return fail(DFFT_ERR_UNSUPPORTED, "more than %d segment bases", kMaxBases);
   if (in_segs && linearize(*in_segs, n, s.in, s.in_bases, s.a.in, (long long)pl->es)) in_segs = nullptr;
+  if (in_segs && is_contig(family) && family != kContigC2R && !getenv("DFFT_NO_TBLOCK") &&
+      linearize_tblocked(*in_segs, s.in, s.in_bases, s.a.in, (long long)pl->es))
+    in_segs = nullptr;
   if (out_segs && linearize(*out_segs, n, s.out, s.out_bases, s.a.out, (long long)pl->es)) out_segs = nullptr;
   if (is_contig(family) && ((!in_segs && s.a.in.tstride != 1) || (!out_segs && s.a.out.tstride != 1)))
     return fail(DFFT_ERR_INTERNAL, "contig stage with a non-unit t-stride side");
@@ -380,6 +423,23 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   if (out_tab) ST(upload_table(*out_tab, &s.out_tab));
   s.a.in.ttab = (const SegEnt*)s.in_tab;
   s.a.out.ttab = (const SegEnt*)s.out_tab;
+  // bulk epilogue: a column-blocked segmented output whose block is the TMA tile (each segment
+  // of a tile is then one contiguous run of tn·W elements)
+  if (family == kStrided && out_segs && s.k.tma_bk_fn && g_use_bulk && s.a.out.bw == s.k.tma_w &&
+      out_segs->size() <= (size_t)kMaxBulk) {
+    const long long es = (long long)pl->es;
+    bool ok = (s.a.out.mT * 1) > 0;
+    for (const Seg& q : *out_segs)
+      ok = ok && q.ts == s.a.out.bw && q.s0 == 1 && (q.off0 * es) % 16 == 0 && (q.s1 * es) % 16 == 0 &&
+           q.tn < (1LL << 30);
+    if (ok) {
+      s.a.out.nbulk = (int)out_segs->size();
+      for (size_t q = 0; q < out_segs->size(); ++q) {
+        const Seg& g = (*out_segs)[q];
+        s.a.out.bulk[q] = BulkSeg{g.off0, g.s1, (int)g.tlo, (int)g.tn, g.sel};
+      }
+    }
+  }
   if (is_contig(family)) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
   else s.grid = ((L0 + s.k.per_cta - 1) / s.k.per_cta) * L1;
   if (s.grid >= (1LL << 31)) return fail(DFFT_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", s.grid);
@@ -400,6 +460,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
       if (occ > 0) {
         s.tma_variant = v2 ? 2 : 1;
         s.tma_grid = std::min<long long>(tiles, (long long)sms * occ);
+        s.tma_occ = occ;
         ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, v2 ? s.k.tma2_maxr : s.k.tma_maxr));
       }
       if (getenv("DFFT_DEBUG"))
@@ -425,8 +486,14 @@ struct Geo {
   // forward chunks along local z of rank column j; inverse chunks along local x of row i
   long long zc(long long j, long long k) const { return blk(Zn(j), K, k); }
   long long z0(long long j, long long k) const { return blo(Zn(j), K, k); }
-  long long xc(long long i, long long k) const { return blk(Xn(i), K, k); }
-  long long x0(long long i, long long k) const { return blo(Xn(i), K, k); }
+  // (xq > 1: inverse chunk bounds at multiples of xq, the column-block width of the fused-store
+  // windows, so a chunk is a whole number of blocks)
+  long long xq = 1;
+  long long x0(long long i, long long k) const {
+    const long long nb = (Xn(i) + xq - 1) / xq;
+    return std::min(Xn(i), blo(nb, K, k) * xq);
+  }
+  long long xc(long long i, long long k) const { return (k + 1 < K ? x0(i, k + 1) : Xn(i)) - x0(i, k); }
 };
 
 // Group members as global ranks: row group = same j (index i'), column group = same i (index j').
@@ -651,12 +718,177 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     set_side(C.a.in, Y3n * g.wy, 1, g.wy);
     C.a.in.bw = (int)g.wy;
     C.a.in.mT = g.nz * Y3n;
+    // blocked input (adjacent y' adjacent) vs natural output (adjacent x adjacent): groups of 4
+    // column tiles give 256 B output pieces and ~(#CTAs/4)·64 B input runs
+    C.a.g0 = tile_g0(4, "DFFT_G0_FWD_C");
   } else {
     C.in = {kWs, L.R2 * es};
     set_side(C.a.in, Xn, 1, g.nz * Xn);
   }
   C.a.scale = 1.0;
   ST(finish_stage(pl, C, kStrided, (int)g.nz, Xn, Y3n, nullptr, nullptr));
+  return DFFT_SUCCESS;
+}
+
+// Fused-store plan with the B→C pipeline, forward (both exchanges remote).  Stage A (x-FFT) runs
+// whole and stores into the row peers' R1 [z][y][x]; stage B (y-FFT) and C (z-FFT) run in K
+// chunks of whole column blocks along x: B(k) stores its columns into the column peers' R2
+// [xt][z][y'][wy] and C(k) transforms them once every column peer has signalled chunk k.
+dfft_status_t build_forward_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
+  const long long i = rp.i, j = rp.j, K = g.K, es = (long long)pl->es;
+  const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
+  const FwdLayout L = fwd_layout(g, i, j, 2);
+  add_flags(pl, g, rp, L.end, true);
+  const long long nxl = pl->r2c ? g.nx / 2 : g.nx;
+  rp.A.resize(K);
+  rp.B.resize(K);
+  rp.E1.resize(K);
+  rp.E2.resize(K);
+  rp.Cc.resize(K);
+  // ---- stage A (whole): x-FFT of lines (l0 = y, l1 = z); out segmented by x-owner i'
+  Stage& A = rp.A[0];
+  A.in = {kUserIn, 0};
+  set_side(A.a.in, 1, nxl, Y1n * nxl);
+  A.out = {kWs, 0};
+  A.out_bases.push_back({kWs, 0});
+  for (long long ip = 0; ip < g.P1; ++ip) A.out_bases.push_back({kPeer, 0, row_rank(g, ip, j)});
+  Segs aseg;
+  for (long long ip = 0; ip < g.P1; ++ip) {
+    const long long xn = g.Xn(ip);
+    const FwdLayout Lr = fwd_layout(g, ip, j, 2);
+    aseg.push_back({1 + (int)ip, g.Xlo(ip), xn, Lr.R1 + g.Y1lo(i) * xn, 1, xn, g.ny * xn});
+  }
+  A.a.scale = 1.0;
+  ST(finish_stage(pl, A, pl->r2c ? kContigR2C : kContig, (int)nxl, Y1n, Zn, nullptr, &aseg));
+  for (long long k = 1; k < K; ++k) rp.A[k].empty = true;
+  rp.E1[0].comm = 0;
+  rp.E1[0].fused = true;
+  for (long long ip = 0; ip < g.P1; ++ip)
+    if (ip != i) rp.E1[0].peers.push_back(row_rank(g, ip, j));
+  for (long long k = 0; k < K; ++k) {
+    const long long x0 = g.x0(i, k), xc = g.xc(i, k);
+    // ---- stage B(k): y-FFT of columns (l0 = x - x0, l1 = z) of R1; out to the column peers' R2
+    Stage& B = rp.B[k];
+    B.in = {kWs, (L.R1 + x0) * es};
+    set_side(B.a.in, Xn, 1, g.ny * Xn);
+    B.out = {kWs, 0};
+    B.out_bases.push_back({kWs, 0});
+    B.out_bases.push_back({kUserOut, 0});
+    for (long long jp = 0; jp < g.P2; ++jp) B.out_bases.push_back({kPeer, 0, col_rank(g, i, jp)});
+    Segs bseg;
+    for (long long jp = 0; jp < g.P2; ++jp) {
+      const long long yn = g.Y3n(jp);
+      const FwdLayout Lr = fwd_layout(g, i, jp, 2);
+      bseg.push_back({2 + (int)jp, g.Y3lo(jp), yn, Lr.R2 + x0 * g.nz * yn + g.Zlo(j) * yn * g.wy, g.wy, 1, yn * g.wy});
+    }
+    B.a.out.bw = (int)g.wy;
+    B.a.out.mT = g.nz;
+    B.a.scale = 1.0;
+    ST(finish_stage(pl, B, kStrided, (int)g.ny, xc, Zn, nullptr, &bseg));
+    Exchange& E2 = rp.E2[k];
+    E2.comm = 1;
+    E2.fused = true;
+    for (long long jp = 0; jp < g.P2; ++jp)
+      if (jp != j) E2.peers.push_back(col_rank(g, i, jp));
+    // ---- stage C(k): z-FFT of columns (l0 = x - x0, l1 = y') of R2 chunk k -> `out`
+    Stage& C = rp.Cc[k];
+    C.in = {kWs, (L.R2 + x0 * g.nz * Y3n) * es};
+    set_side(C.a.in, Y3n * g.wy, 1, g.wy);
+    C.a.in.bw = (int)g.wy;
+    C.a.in.mT = g.nz * Y3n;
+    C.a.g0 = tile_g0(4, "DFFT_G0_FWD_C");
+    C.out = {kUserOut, x0 * es};
+    set_side(C.a.out, Y3n * Xn, 1, Xn);
+    C.a.scale = 1.0;
+    ST(finish_stage(pl, C, kStrided, (int)g.nz, xc, Y3n, nullptr, nullptr));
+  }
+  return DFFT_SUCCESS;
+}
+
+// Inverse counterpart (both exchanges remote): stage A (z-IFFT) whole into the column peers' R2'
+// [xt][y][z][wz]; stage B (y-IFFT) and C (x-IFFT, ×1/N) in K chunks along local z: B(k) stores
+// into the row peers' R1' [source i][xt][z][y][wy], C(k) reads the chunk from every source.
+dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
+  const long long i = rp.i, j = rp.j, K = g.K, es = (long long)pl->es;
+  const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
+  const InvLayout L = inv_layout(g, i, j, 2);
+  add_flags(pl, g, rp, L.end, false);
+  const long long nxl = pl->r2c ? g.nx / 2 : g.nx;
+  rp.A.resize(K);
+  rp.B.resize(K);
+  rp.E1.resize(K);
+  rp.E2.resize(K);
+  rp.Cc.resize(K);
+  // ---- stage A (whole): z-IFFT of columns (l0 = x, l1 = y') of `in`; out to the column peers' R2'
+  Stage& A = rp.A[0];
+  A.in = {kUserIn, 0};
+  set_side(A.a.in, Y3n * Xn, 1, Xn);
+  A.out = {kWs, 0};
+  A.out_bases.push_back({kWs, 0});
+  for (long long jp = 0; jp < g.P2; ++jp) A.out_bases.push_back({kPeer, 0, col_rank(g, i, jp)});
+  Segs aseg;
+  for (long long jp = 0; jp < g.P2; ++jp) {
+    const long long zn = g.Zn(jp);
+    const InvLayout Lr = inv_layout(g, i, jp, 2);
+    aseg.push_back({1 + (int)jp, g.Zlo(jp), zn, Lr.R2 + g.Y3lo(j) * zn * g.wz, g.wz, 1, zn * g.wz});
+  }
+  A.a.out.bw = (int)g.wz;
+  A.a.out.mT = g.ny;
+  A.a.scale = 1.0;
+  ST(finish_stage(pl, A, kStrided, (int)g.nz, Xn, Y3n, nullptr, &aseg));
+  for (long long k = 1; k < K; ++k) rp.A[k].empty = true;
+  rp.E1[0].comm = 1;
+  rp.E1[0].fused = true;
+  for (long long jp = 0; jp < g.P2; ++jp)
+    if (jp != j) rp.E1[0].peers.push_back(col_rank(g, i, jp));
+  for (long long k = 0; k < K; ++k) {
+    const long long z0 = blo(Zn, K, k), zc = blk(Zn, K, k);
+    // ---- stage B(k): y-IFFT of columns (l0 = x, l1 = z - z0) of R2'; out to the row peers' R1'
+    Stage& B = rp.B[k];
+    B.in = {kWs, (L.R2 + z0 * g.wz) * es};
+    set_side(B.a.in, Zn * g.wz, 1, g.wz);
+    B.a.in.bw = (int)g.wz;
+    B.a.in.mT = g.ny * Zn;
+    B.a.g0 = tile_g0(1, "DFFT_G0_INV_B");
+    B.out = {kWs, 0};
+    B.out_bases.push_back({kWs, 0});
+    for (long long ip = 0; ip < g.P1; ++ip) B.out_bases.push_back({kPeer, 0, row_rank(g, ip, j)});
+    Segs bseg;
+    for (long long ip = 0; ip < g.P1; ++ip) {
+      const long long yn = g.Y1n(ip);
+      const InvLayout Lr = inv_layout(g, ip, j, 2);
+      long long src = 0;
+      for (long long q = 0; q < i; ++q) src += round_up(g.Xn(q), g.wy) * Zn * yn;
+      bseg.push_back({1 + (int)ip, g.Y1lo(ip), yn, Lr.R1 + src + z0 * yn * g.wy, g.wy, 1, yn * g.wy});
+    }
+    B.a.out.bw = (int)g.wy;
+    B.a.out.mT = Zn;
+    B.a.scale = 1.0;
+    ST(finish_stage(pl, B, kStrided, (int)g.ny, Xn, zc, nullptr, &bseg));
+    Exchange& E2 = rp.E2[k];
+    E2.comm = 0;
+    E2.fused = true;
+    for (long long ip = 0; ip < g.P1; ++ip)
+      if (ip != i) E2.peers.push_back(row_rank(g, ip, j));
+    // ---- stage C(k): x-IFFT of lines (l0 = y, l1 = z - z0) of R1' chunk k, ×1/N -> `out`
+    Stage& C = rp.Cc[k];
+    C.in = {kWs, 0};
+    Segs cseg;
+    long long src = L.R1;
+    for (long long is = 0; is < g.P1; ++is) {
+      const long long xn = g.Xn(is), nb = (xn + g.wy - 1) / g.wy;
+      for (long long xb = 0; xb < nb; ++xb) {
+        const long long tn = std::min(g.wy, xn - xb * g.wy);
+        cseg.push_back({0, g.Xlo(is) + xb * g.wy, tn, src + xb * Zn * Y1n * g.wy + z0 * Y1n * g.wy, 1, g.wy,
+                        Y1n * g.wy});
+      }
+      src += nb * g.wy * Zn * Y1n;
+    }
+    C.out = {kUserOut, z0 * Y1n * nxl * es};  // C2R: nxl = nx/2 complex = nx reals per line
+    set_side(C.a.out, 1, nxl, Y1n * nxl);
+    C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)g.nx * (double)g.ny * (double)g.nz);
+    ST(finish_stage(pl, C, pl->r2c ? kContigC2R : kContig, (int)nxl, Y1n, zc, &cseg, nullptr));
+  }
   return DFFT_SUCCESS;
 }
 
@@ -760,7 +992,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       const long long zl = g.Zlo(jp), zn = g.Zn(jp);
       if (p2p) {  // receiver's R2' [xt][y][z][wz]
         const InvLayout Lr = inv_layout(g, i, jp, mode);
-        aseg.push_back({1 + (int)jp, zl, zn, Lr.R2 + g.Y3lo(j) * zn * g.wz, g.wz, 1, zn * g.wz});
+        aseg.push_back({1 + (int)jp, zl, zn, Lr.R2 + x0 * g.ny * zn + g.Y3lo(j) * zn * g.wz, g.wz, 1, zn * g.wz});
       } else if (jp == j) {
         aseg.push_back({0, zl, zn, L.R2 + g.ny * Zn * x0 + g.Y3lo(j) * Zn * xc, xc, 1, Zn * xc});
       } else {
@@ -794,11 +1026,13 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Stage& B = rp.B[k];
     B.in = {kWs, (L.R2 + g.ny * Zn * x0) * es};
     set_side(B.a.in, Zn * xc, 1, xc);
-    if (p2p) {  // R2' [xt][y][z][wz] (p2p runs one chunk: x0 = 0)
-      B.in = {kWs, L.R2 * es};
+    if (p2p) {  // R2' [xt][y][z][wz]; chunk k starts at block x0 / wz
+      B.in = {kWs, (L.R2 + x0 * g.ny * Zn) * es};
       set_side(B.a.in, Zn * g.wz, 1, g.wz);
       B.a.in.bw = (int)g.wz;
       B.a.in.mT = g.ny * Zn;
+      // blocked input (adjacent z adjacent) and per-tile contiguous blocked output: z fastest
+      B.a.g0 = tile_g0(1, "DFFT_G0_INV_B");
     }
     B.out = {kWs, 0};
     B.out_bases.push_back({kWs, 0});
@@ -811,7 +1045,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
         const InvLayout Lr = inv_layout(g, ip, j, mode);
         long long src = 0;
         for (long long q = 0; q < i; ++q) src += round_up(g.Xn(q), g.wy) * Zn * yn;
-        bseg.push_back({1 + (int)ip, yl, yn, Lr.R1 + src, g.wy, 1, yn * g.wy});
+        bseg.push_back({1 + (int)ip, yl, yn, Lr.R1 + src + x0 * Zn * yn, g.wy, 1, yn * g.wy});
       } else if (ip == i) {
         bseg.push_back({0, yl, yn, r1off(L, i, i, k), xc, 1, Y1n * xc});
       } else {
@@ -931,12 +1165,13 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
       if (!use_st) tout = tin;  // unused by the non-TST variant
       a.tw = s.tw_tma;
       void* targs[] = {&tin, &tout, &a};
+      const long long grid = s.sm_cap > 0 ? std::min<long long>(s.tma_grid, (long long)s.sm_cap * s.tma_occ) : s.tma_grid;
       if (s.tma_variant == 2)
-        CU(cudaLaunchKernel(use_st ? s.k.tma2_st_fn : s.k.tma2_fn, dim3((unsigned)s.tma_grid), dim3(s.k.tma2_threads),
+        CU(cudaLaunchKernel(use_st ? s.k.tma2_st_fn : s.k.tma2_fn, dim3((unsigned)grid), dim3(s.k.tma2_threads),
                             targs, s.k.tma2_smem, st));
       else
-        CU(cudaLaunchKernel(use_st ? s.k.tma_st_fn : s.k.tma_fn, dim3((unsigned)s.tma_grid), dim3(s.k.tma_threads),
-                            targs, s.k.tma_smem, st));
+        CU(cudaLaunchKernel(a.out.nbulk > 0 ? s.k.tma_bk_fn : use_st ? s.k.tma_st_fn : s.k.tma_fn, dim3((unsigned)grid),
+                            dim3(s.k.tma_threads), targs, s.k.tma_smem, st));
       return DFFT_SUCCESS;
     }
   }
@@ -1078,26 +1313,64 @@ dfft_status_t p2p_wait(dfft_plan_t pl, int arr, int e, int k, const std::vector<
   return DFFT_SUCCESS;
 }
 
-dfft_status_t execute_p2p(dfft_plan_t pl, const Ctx& cx, cudaStream_t st) {
+// Two compute streams: X runs stage A chunk by chunk, Y runs stage B of each chunk as soon as
+// its first exchange has landed, then stage C.  So A(k+1) overlaps B(k) (Fig. 1, the
+// progressive per-chunk pipelining); when one of the two is NVLink-bound (fused remote stores)
+// it runs on at most sm_cap SMs so the HBM-bound one can co-reside (Stage::sm_cap).
+dfft_status_t execute_p2p(dfft_plan_t pl, const Ctx& cx, cudaStream_t user) {
   RankPlan& rp = pl->ranks[0];
   const int K = (int)rp.A.size();
   const unsigned ep = ++pl->epoch;
+  cudaStream_t X = pl->s_comp, Y = pl->s_comm;
+  CU(cudaEventRecord(pl->ev_fork, user));
+  CU(cudaStreamWaitEvent(X, pl->ev_fork, 0));
+  CU(cudaStreamWaitEvent(Y, pl->ev_fork, 0));
+  if (pl->bc) {
+    // X: A (whole), then C(k) as chunk k of the second exchange completes; Y: B(k), k = 0..K-1
+    const std::vector<int>& p1 = rp.E1[0].peers;
+    if (ep > 1) ST(p2p_wait(pl, 1, 0, 0, p1, ep - 1, X));
+    ST(launch_p(pl, 0, rp.A[0], cx, X));
+    ST(p2p_signal(pl, 0, 0, 0, p1, ep, X));
+    CU(cudaEventRecord(pl->evA[0], X));
+    CU(cudaStreamWaitEvent(Y, pl->evA[0], 0));
+    ST(p2p_wait(pl, 0, 0, 0, p1, ep, Y));
+    for (int k = 0; k < K; ++k) {
+      if (ep > 1) ST(p2p_wait(pl, 1, 1, k, rp.E2[k].peers, ep - 1, Y));
+      ST(launch_p(pl, 2, rp.B[k], cx, Y));
+      ST(p2p_signal(pl, 0, 1, k, rp.E2[k].peers, ep, Y));
+      CU(cudaEventRecord(pl->evB[k], Y));
+    }
+    ST(p2p_signal(pl, 1, 0, 0, p1, ep, Y));  // done reading my first-exchange window
+    for (int k = 0; k < K; ++k) {
+      CU(cudaStreamWaitEvent(X, pl->evB[k], 0));
+      ST(p2p_wait(pl, 0, 1, k, rp.E2[k].peers, ep, X));
+      ST(launch_p(pl, 4, rp.Cc[k], cx, X));
+      ST(p2p_signal(pl, 1, 1, k, rp.E2[k].peers, ep, X));
+    }
+  } else {
   for (int k = 0; k < K; ++k) {
     // my epoch-1 stores into the first-exchange peers were consumed
-    if (ep > 1) ST(p2p_wait(pl, 1, 0, k, rp.E1[k].peers, ep - 1, st));
-    ST(launch_p(pl, 0, rp.A[k], cx, st));
-    ST(p2p_signal(pl, 0, 0, k, rp.E1[k].peers, ep, st));
+    if (ep > 1) ST(p2p_wait(pl, 1, 0, k, rp.E1[k].peers, ep - 1, X));
+    ST(launch_p(pl, 0, rp.A[k], cx, X));
+    ST(p2p_signal(pl, 0, 0, k, rp.E1[k].peers, ep, X));
+    CU(cudaEventRecord(pl->evA[k], X));
   }
   for (int k = 0; k < K; ++k) {
-    ST(p2p_wait(pl, 0, 0, k, rp.E1[k].peers, ep, st));
-    if (ep > 1) ST(p2p_wait(pl, 1, 1, k, rp.E2[k].peers, ep - 1, st));
-    ST(launch_p(pl, 2, rp.B[k], cx, st));
-    ST(p2p_signal(pl, 1, 0, k, rp.E1[k].peers, ep, st));  // done reading my first-exchange window
-    ST(p2p_signal(pl, 0, 1, k, rp.E2[k].peers, ep, st));  // ready: stored into the peers' second windows
+    CU(cudaStreamWaitEvent(Y, pl->evA[k], 0));  // my own block of chunk k
+    ST(p2p_wait(pl, 0, 0, k, rp.E1[k].peers, ep, Y));
+    if (ep > 1) ST(p2p_wait(pl, 1, 1, k, rp.E2[k].peers, ep - 1, Y));
+    ST(launch_p(pl, 2, rp.B[k], cx, Y));
+    ST(p2p_signal(pl, 1, 0, k, rp.E1[k].peers, ep, Y));  // done reading my first-exchange window
+    ST(p2p_signal(pl, 0, 1, k, rp.E2[k].peers, ep, Y));  // ready: stored into the peers' second windows
   }
-  for (int k = 0; k < K; ++k) ST(p2p_wait(pl, 0, 1, k, rp.E2[k].peers, ep, st));
-  ST(launch_p(pl, 4, rp.C, cx, st));
-  for (int k = 0; k < K; ++k) ST(p2p_signal(pl, 1, 1, k, rp.E2[k].peers, ep, st));
+  for (int k = 0; k < K; ++k) ST(p2p_wait(pl, 0, 1, k, rp.E2[k].peers, ep, Y));
+  ST(launch_p(pl, 4, rp.C, cx, Y));
+  for (int k = 0; k < K; ++k) ST(p2p_signal(pl, 1, 1, k, rp.E2[k].peers, ep, Y));
+  }
+  CU(cudaEventRecord(pl->ev_join_comp, X));
+  CU(cudaEventRecord(pl->ev_join_comm, Y));
+  CU(cudaStreamWaitEvent(user, pl->ev_join_comp, 0));
+  CU(cudaStreamWaitEvent(user, pl->ev_join_comm, 0));
   return DFFT_SUCCESS;
 }
 
@@ -1222,6 +1495,23 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
 
 dfft_status_t execute_sim(dfft_plan_t pl, const void* const* ins, void* const* outs, cudaStream_t st) {
   const size_t P = pl->ranks.size(), K = pl->ranks[0].A.size();
+  if (pl->p2p) {
+    // fused-store layouts: every stage of every rank stores straight into the other ranks'
+    // workspaces; stream order replaces the ready/done flags
+    void* const* peers = pl->peer_ws.data();
+    auto cx = [&](size_t r) { return Ctx{ins[r], outs[r], pl->ranks[r].ws, peers}; };
+    for (size_t k = 0; k < K; ++k)
+      for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].A[k], cx(r), st));
+    for (size_t k = 0; k < K; ++k)
+      for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].B[k], cx(r), st));
+    for (size_t r = 0; r < P; ++r) {
+      if (pl->bc)
+        for (size_t k = 0; k < K; ++k) ST(launch(pl->ranks[r].Cc[k], cx(r), st));
+      else
+        ST(launch(pl->ranks[r].C, cx(r), st));
+    }
+    return DFFT_SUCCESS;
+  }
   for (size_t k = 0; k < K; ++k)
     for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].A[k], Ctx{ins[r], outs[r], pl->ranks[r].ws, nullptr}, st));
   for (size_t k = 0; k < K; ++k) ST(exchange_sim(pl, false, k, ins, outs, st));
@@ -1251,13 +1541,15 @@ void free_plan(dfft_plan_t pl) {
   }
   if (pl->s_comp) cudaStreamSynchronize(pl->s_comp);
   if (pl->s_comm) cudaStreamSynchronize(pl->s_comm);
-  for (size_t r = 0; r < pl->peer_ws.size(); ++r)
-    if (pl->peer_ws[r] && (int)r != pl->comm->rank) cudaIpcCloseMemHandle(pl->peer_ws[r]);
+  if (!pl->comm->sim)
+    for (size_t r = 0; r < pl->peer_ws.size(); ++r)
+      if (pl->peer_ws[r] && (int)r != pl->comm->rank) cudaIpcCloseMemHandle(pl->peer_ws[r]);
   pl->peer_ws.clear();
   for (RankPlan& rp : pl->ranks) {
     for (Stage& s : rp.A) free_stage(s);
     for (Stage& s : rp.B) free_stage(s);
     free_stage(rp.C);
+    for (Stage& c : rp.Cc) free_stage(c);
     if (rp.ws) cudaFree(rp.ws);
   }
   for (auto* v : {&pl->evA, &pl->evE1, &pl->evB, &pl->evE2})
@@ -1278,6 +1570,36 @@ struct PlanGuard {
     if (p) free_plan(p);
   }
 };
+
+// Fused-store plans with K > 1 run stage A(k+1) and B(k) concurrently on two streams.  The one
+// of the pair that stores to peers (NVLink-bound) gets at most DFFT_NVL_SMS SMs (default 64) and
+// the HBM-bound one the rest, except in the last chunk, which runs alone.
+dfft_status_t apply_sm_caps(dfft_plan_t pl, RankPlan& rp) {
+  const size_t K = rp.A.size();
+  if (!pl->p2p || K < 2) return DFFT_SUCCESS;
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->comm->device));
+  const char* v = getenv("DFFT_NVL_SMS");
+  const int nvl = std::max(1, std::min(sms - 1, v ? atoi(v) : 64));
+  if (pl->bc) {  // B(k) stores to peers, C(k) runs beside B(k+1)
+    for (size_t k = 0; k < K; ++k) {
+      rp.B[k].sm_cap = nvl;
+      if (k + 1 < K) rp.Cc[k].sm_cap = sms - nvl;
+    }
+    return DFFT_SUCCESS;
+  }
+  for (size_t k = 0; k < K; ++k) {
+    const bool a_remote = !rp.E1[k].peers.empty(), b_remote = !rp.E2[k].peers.empty();
+    if (a_remote == b_remote) continue;  // both or neither NVLink-bound: nothing to balance
+    Stage& nv = a_remote ? rp.A[k] : rp.B[k];
+    nv.sm_cap = nvl;
+    // the local stage of the pair: B(k) runs beside A(k+1) (none after the last chunk); A(k+1)
+    // runs beside B(k)
+    if (a_remote && k + 1 < K) rp.B[k].sm_cap = sms - nvl;
+    if (b_remote && k >= 1) rp.A[k].sm_cap = sms - nvl;
+  }
+  return DFFT_SUCCESS;
+}
 
 }  // namespace
 
@@ -1403,6 +1725,7 @@ dfft_status_t dfft_decomp_box(int64_t nx, int64_t ny, int64_t nz, dfft_decomp_t 
   return DFFT_SUCCESS;
 }
 
+
 dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, int64_t ny, int64_t nz,
                                dfft_decomp_t decomp, int p1, int p2, dfft_type_t type, dfft_direction_t direction,
                                uint64_t flags) {
@@ -1415,25 +1738,31 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   long long nxc = r2c ? nx / 2 + 1 : nx;
   int Kreq = (int)(flags & 0xff);
   bool overlap = !(flags & DFFT_FLAG_NO_OVERLAP);
-  long long kmax = direction == DFFT_FORWARD ? nz / p2 : nxc / p1;
+  long long kmax = direction == DFFT_FORWARD ? nz / p2 : nxc / p1;  // chunk axis extent
   // exchange transport for P > 1: copy engines into IPC windows (default),
   // fused epilogue stores into the windows (DFFT_FLAG_FUSED_STORE), or NCCL (DFFT_FLAG_NCCL)
   const char* exch_env = getenv("DFFT_EXCHANGE");
   auto env_is = [&](const char* v) { return exch_env && strcmp(exch_env, v) == 0; };
-  const bool nccl_mode = comm->sim || P == 1 || (flags & DFFT_FLAG_NCCL) || env_is("nccl");
-  const bool want_ce = (flags & DFFT_FLAG_CE) || env_is("ce");
-  const bool want_fused = (flags & DFFT_FLAG_FUSED_STORE) || env_is("p2p");
-  const bool want_hybrid = (flags & DFFT_FLAG_HYBRID) || env_is("hybrid");
-  // automatic choice (measured r01, 1024^3 c64): a 1×P2 grid (only the second exchange) is best
-  // with the copy engine and 8 chunks; grids with P1 > 1 are best with fused epilogue stores
-  const bool auto_fused = !want_ce && !want_fused && !want_hybrid && p1 > 1;
+  const bool want_fused = (flags & DFFT_FLAG_FUSED_STORE) || (!comm->sim && env_is("p2p"));
+  // simulated ranks run the NCCL layouts, or (DFFT_FLAG_FUSED_STORE) the fused-store layouts with
+  // every rank's workspace standing in for its IPC window (same kernels, same addresses)
+  const bool nccl_mode = (comm->sim && !want_fused) || P == 1 || (flags & DFFT_FLAG_NCCL) || env_is("nccl");
+  const bool want_ce = !comm->sim && ((flags & DFFT_FLAG_CE) || env_is("ce"));
+  const bool want_hybrid = !comm->sim && ((flags & DFFT_FLAG_HYBRID) || env_is("hybrid"));
+  // automatic choice (measured r01, 1024^3 c64): fused epilogue stores into column-blocked
+  // windows beat the copy engine on every grid (1x2: 16.1 vs 18.0 ms, 2x2: 9.4 vs 16.9 ms)
+  const bool auto_fused = !comm->sim && !want_ce && !want_fused && !want_hybrid;
   const bool p2p_mode = !nccl_mode && (want_fused || auto_fused);
   const bool ce_only = !nccl_mode && !p2p_mode && !want_hybrid;
   const bool ce_mode = !nccl_mode && !p2p_mode;
   // chunks pipeline the transfers against the FFTs; with fused stores the transfer happens
   // inside the FFT kernels themselves, so one chunk is the default there
   long long K = Kreq > 0 ? Kreq : (P > 1 && !p2p_mode ? (nccl_mode ? 4 : 8) : 1);
-  if (p2p_mode) K = 1;  // fused stores into column-blocked windows: one chunk
+  // fused stores: with a 1×P2 grid the x-FFT is local and overlaps the NVLink-bound y-FFT of the
+  // previous chunk (two streams); with P1 > 1 both are NVLink-bound, so one chunk
+  const bool bc_mode = p2p_mode && p1 > 1 && p2 > 1;
+  if (p2p_mode && Kreq == 0) K = 1;  // r01 sweep: fused stores need every SM
+  if (bc_mode) kmax = direction == DFFT_FORWARD ? nxc / p1 : nz / p2;
   K = std::max<long long>(1, std::min<long long>(K, kmax));
   if (P == 1) K = 1;  // nothing to overlap
 
@@ -1456,6 +1785,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   pl->p2p = p2p_mode;
   pl->ce = ce_mode;
   pl->hybrid = ce_mode && !ce_only;
+  pl->bc = bc_mode;
   if ((pl->p2p || pl->ce) && !stream_wait_value32())
     return fail(DFFT_ERR_UNSUPPORTED, "cuStreamWaitValue32 unavailable");
   Geo g{nx, ny, nz, nxc, p1, p2, K};
@@ -1466,6 +1796,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
     if (f64 ? lookup_kernel_f64(kStrided, (int)nz, direction, &kz) : lookup_kernel_f32(kStrided, (int)nz, direction, &kz))
       g.wz = kz.tma_fn ? kz.tma_w : kz.per_cta;
   }
+  if (p2p_mode) g.xq = std::max(g.wy, g.wz);
 
   if (!comm->sim && P > 1) {
     // collective consistency check: every rank must pass identical arguments
@@ -1517,7 +1848,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       memcpy(rp.out_n, d3n, sizeof d3n);
       rp.in_bytes = d1b;
       rp.out_bytes = d3b;
-      ST(P == 1 ? build_single(pl, g, rp) : build_forward(pl, g, rp));
+      ST(P == 1 ? build_single(pl, g, rp) : pl->bc ? build_forward_bc(pl, g, rp) : build_forward(pl, g, rp));
     } else {
       memcpy(rp.in_lo, d3lo, sizeof d3lo);
       memcpy(rp.in_n, d3n, sizeof d3n);
@@ -1525,14 +1856,19 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       memcpy(rp.out_n, d1n, sizeof d1n);
       rp.in_bytes = d3b;
       rp.out_bytes = d1b;
-      ST(P == 1 ? build_single(pl, g, rp) : build_inverse(pl, g, rp));
+      ST(P == 1 ? build_single(pl, g, rp) : pl->bc ? build_inverse_bc(pl, g, rp) : build_inverse(pl, g, rp));
     }
+    ST(apply_sm_caps(pl, rp));
     if (rp.ws_bytes) {
       cudaError_t e = cudaMalloc(&rp.ws, rp.ws_bytes);
       if (e != cudaSuccess) return fail(DFFT_ERR_ALLOC, "workspace of %zu bytes: %s", rp.ws_bytes, cudaGetErrorString(e));
     }
   }
-  if (pl->p2p || pl->ce) {
+  if (comm->sim && pl->p2p) {
+    // simulated fused stores: rank q's "window" is its workspace on this device
+    pl->peer_ws.resize(P);
+    for (int q = 0; q < P; ++q) pl->peer_ws[q] = pl->ranks[q].ws;
+  } else if (pl->p2p || pl->ce) {
     // every workspace becomes an IPC window; open the windows of the row and column peers
     RankPlan& rp = pl->ranks[0];
     CU(cudaMemset((char*)rp.ws + pl->flag_off, 0, flag_bytes(g)));
@@ -1697,6 +2033,7 @@ dfft_status_t dfft_plan_stage_bytes(dfft_plan_t pl, double bytes[5]) {
     bytes[3] += xch_b(rp.E2[k]);
   }
   bytes[4] = stage_b(rp.C);
+  for (const Stage& c : rp.Cc) bytes[4] += stage_b(c);
   return DFFT_SUCCESS;
 }
 

@@ -291,6 +291,14 @@ struct SegEnt {
   long long off;  // sel << 56 | element offset of (t, 0, 0) relative to bases[sel]
   int s0, s1;     // line strides of this segment
 };
+// One segment of a column-blocked segmented output side, as the persistent strided kernel's bulk
+// epilogue sees it: rows t ∈ [tlo, tlo+tn) of a tile land contiguously at bases[sel] +
+// off0 + (block·mT + l1)·s1 (requires t-stride == bw == tile width, column stride 1).
+constexpr int kMaxBulk = 16;
+struct BulkSeg {
+  long long off0, s1;
+  int tlo, tn, sel;
+};
 struct SideMap {
   void* base;                 // unsegmented: the side's pointer
   void* bases[kMaxBases];     // segmented: base pointer per selector (local buffers, peers' windows)
@@ -301,6 +309,14 @@ struct SideMap {
   // A warp's rows of one block are then contiguous (256 B pieces over NVLink).
   int bw;
   long long mT;
+  // t-blocked unsegmented side (tb > 0, contig family): t lives at (t/tb)·tbs + t%tb — the
+  // column-blocked receive windows seen along the FFT axis, without a per-t table
+  int tb;
+  long long tbs;
+  // bulk epilogue (output side of the persistent strided kernel, OM = 2): one
+  // cp.async.bulk shared→global copy per segment per tile instead of per-element stores
+  int nbulk;
+  BulkSeg bulk[kMaxBulk];
 };
 
 // effective (l0, l1) of a side for column l0 / line l1 (blocked layouts fold the block into l1)
@@ -339,7 +355,29 @@ struct PassArgs {
   const void* tw2;   // R2C/C2R: w^k = exp(DIR·2πi·k/(2N)), k < N (the split/merge twiddles)
   long long L0, L1;  // line grid: lines (l0, l1), l0 < L0, l1 < L1 (strided: l0 = the column)
   double scale;      // applied to the outputs of the last pass (1 = none)
+  // persistent strided kernels: tile order.  Tiles run in groups of g0 column tiles × all L1
+  // (column tile fastest inside a group); g0 = 0 means one group (column tile fastest overall).
+  // Concurrently resident CTAs then touch g0 adjacent column tiles × (#CTAs / g0) adjacent
+  // lines: g0 = 1 suits a side where adjacent l1 are adjacent in memory (column-blocked
+  // windows), a small g0 balances a blocked side against a natural one.
+  int g0;
 };
+
+// tile -> (column tile tx, line l1) under the grouped order above
+__device__ __forceinline__ void tile_coords(long long tile, long long ntile, long long L1, int g0, long long& tx,
+                                            long long& l1) {
+  if (g0 <= 0 || g0 >= ntile) {
+    l1 = tile / ntile;
+    tx = tile - l1 * ntile;
+    return;
+  }
+  const long long grp = tile / ((long long)g0 * L1);
+  const long long base = grp * g0;
+  const long long gw = ntile - base < g0 ? ntile - base : g0;
+  const long long r = tile - grp * g0 * L1;
+  l1 = r / gw;
+  tx = base + (r - l1 * gw);
+}
 
 // --------------------------------------------------------------------------------- Stockham core
 // One thread's part of the passes of one line.  IO supplies the global side:
@@ -429,7 +467,10 @@ template <typename C, bool UNIT_T = false> struct GIO {
     scale = (decltype(C{}.x))sc;
   }
   __device__ __forceinline__ C load(int t) const {
-    if (mi->ttab == nullptr) return UNIT_T ? in[lin + t] : in[(long long)t * mi->tstride + lin];
+    if (mi->ttab == nullptr) {
+      if (mi->tb > 0) return in[lin + (long long)(t / mi->tb) * mi->tbs + t % mi->tb];
+      return UNIT_T ? in[lin + t] : in[(long long)t * mi->tstride + lin];
+    }
     return *seg_ptr<const C>(*mi, t, i0, i1);
   }
   __device__ __forceinline__ void store(int t, C v) const {
@@ -664,10 +705,10 @@ template <typename Real, int N> struct TmaCfg {
   static constexpr bool OK = S.npass >= 2 && THREADS <= 1024 && SMEM <= 227 * 1024 && 2 * W <= 256;
 };
 
-template <typename C, int W, bool TST> struct TmaIO : GIO<C> {
+template <typename C, int W, int OM> struct TmaIO : GIO<C> {
   static constexpr bool kSyncAfterLoad = true;
   const C* stage;  // this tile's stage buffer, dense [t][W]
-  C* obuf;         // TST: dense [t][W] output tile, written to HBM by a TMA store
+  C* obuf;         // OM > 0: dense [t][W] output tile, written by a TMA tensor store (1) or bulk copies (2)
   int c;
   // refill: thread 0 issues the TMA for the tile NS steps ahead into the drained stage
   const void* tmap;
@@ -678,7 +719,7 @@ template <typename C, int W, bool TST> struct TmaIO : GIO<C> {
   bool refill;
   __device__ __forceinline__ C load(int t) const { return stage[t * W + c]; }
   __device__ __forceinline__ void store(int t, C v) const {
-    if constexpr (TST) {
+    if constexpr (OM != 0) {
       if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
       obuf[t * W + c] = v;
     } else {
@@ -695,12 +736,22 @@ template <typename C, int W, bool TST> struct TmaIO : GIO<C> {
   }
 };
 
-// TST: the output side is unsegmented and written by TMA stores (omap) from the work buffer —
-// issuing 64 B row stores at a large stride from the SMs throttles the LSU (r01 ncu: lg_throttle).
-template <typename Real, int N, int DIR, bool TST>
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+               "r"(bytes)
+               : "memory");
+}
+
+// OM (output mode): 0 = per-element stores through the SideMap; 1 = the output side is
+// unsegmented and written by TMA tensor stores (omap) from the work buffer — issuing 64 B row
+// stores at a large stride from the SMs throttles the LSU (r01 ncu: lg_throttle); 2 = the
+// output is segmented into column-blocked windows (possibly peers' over NVLink) and each
+// segment of a tile leaves as one contiguous cp.async.bulk copy.
+template <typename Real, int N, int DIR, int OM>
 __global__ void __launch_bounds__(TmaCfg<Real, N>::THREADS)
 fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
                        const __grid_constant__ PassArgs a) {
+  constexpr bool TST = OM != 0;
   using C = typename CT<Real>::type;
   using Cfg = TmaCfg<Real, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -714,8 +765,9 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
   constexpr uint32_t kBytes = (uint32_t)(Cfg::STAGE_ELEMS * Cfg::ES);
   // TMA coordinates are in reals: column c -> 2c
   auto issue = [&](long long tile, int s) {
-    const long long l1 = tile / ntile;
-    const int c0 = (int)((tile - l1 * ntile) * Cfg::W * 2);
+    long long tx, l1;
+    tile_coords(tile, ntile, a.L1, a.g0, tx, l1);
+    const int c0 = (int)(tx * Cfg::W * 2);
     mbar_expect_tx(&bars[s], kBytes);
     for (int q = 0; q < Cfg::NBOX; ++q)
       tma_load_tile(stages + s * Cfg::STAGE_ELEMS + q * Cfg::BOXR * Cfg::W, &tmap, a.in.bw, c0, q * Cfg::BOXR, (int)l1,
@@ -734,11 +786,12 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
   for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
     const int s = it % Cfg::NS;
     const uint32_t parity = (uint32_t)((it / Cfg::NS) & 1);
-    const long long l1 = tile / ntile;
-    const long long l0 = (tile - l1 * ntile) * Cfg::W + c;
+    long long tx, l1;
+    tile_coords(tile, ntile, a.L1, a.g0, tx, l1);
+    const long long l0 = tx * Cfg::W + c;
     const bool active = l0 < a.L0;
     if (TST && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
-    TmaIO<C, Cfg::W, TST> io;
+    TmaIO<C, Cfg::W, OM> io;
     io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
     io.obuf = work;
     io.stage = stages + s * Cfg::STAGE_ELEMS;
@@ -749,9 +802,10 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     io.mbar = &bars[s];
     io.stage_ptr = stages + s * Cfg::STAGE_ELEMS;
     {
-      const long long nl1 = next / ntile;
+      long long ntx, nl1;
+      tile_coords(next, ntile, a.L1, a.g0, ntx, nl1);
       io.next_l1 = (int)nl1;
-      io.next_c0 = (int)((next - nl1 * ntile) * Cfg::W * 2);
+      io.next_c0 = (int)(ntx * Cfg::W * 2);
     }
     io.nbox = Cfg::NBOX;
     io.boxr = Cfg::BOXR;
@@ -764,8 +818,18 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
       __syncthreads();
       if (threadIdx.x == 0) {
-        const int c0 = (int)((tile - l1 * ntile) * Cfg::W * 2);
-        for (int q = 0; q < Cfg::NBOX; ++q) tma_store_3d(&omap, c0, q * Cfg::BOXR, (int)l1, work + q * Cfg::BOXR * Cfg::W);
+        if constexpr (OM == 1) {
+          const int c0 = (int)(tx * Cfg::W * 2);
+          for (int q = 0; q < Cfg::NBOX; ++q)
+            tma_store_3d(&omap, c0, q * Cfg::BOXR, (int)l1, work + q * Cfg::BOXR * Cfg::W);
+        } else {
+          const long long e1 = tx * a.out.mT + l1;  // block tx (bw == W), line l1
+          for (int q = 0; q < a.out.nbulk; ++q) {
+            const BulkSeg& g = a.out.bulk[q];
+            C* dst = reinterpret_cast<C*>(a.out.bases[g.sel]) + (g.off0 + e1 * g.s1);
+            bulk_store(dst, work + g.tlo * Cfg::W, (uint32_t)(g.tn * Cfg::W * Cfg::ES));
+          }
+        }
         bulk_commit();
       }
     }
@@ -850,9 +914,10 @@ fft_strided_tma2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_c
   const long long total = ntile * a.L1;
   constexpr uint32_t kBytes = (uint32_t)(Cfg::NBOX * Cfg::R0 * Cfg::W * Cfg::ES);
   auto coords = [&](long long tile, int& c0, int& l1) {
-    const long long q = tile / ntile;
+    long long tx, q;
+    tile_coords(tile, ntile, a.L1, a.g0, tx, q);
     l1 = (int)q;
-    c0 = (int)((tile - q * ntile) * Cfg::W * 2);  // TMA coordinates are in reals
+    c0 = (int)(tx * Cfg::W * 2);  // TMA coordinates are in reals
   };
   auto issue = [&](long long tile, int b) {
     int c0, l1;

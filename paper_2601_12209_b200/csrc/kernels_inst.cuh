@@ -27,8 +27,9 @@ KernelInfo make_strided() {
   k.twlen = sched_twlen(Cfg::S);
   using TC = TmaCfg<Real, N>;
   if constexpr (TC::OK) {
-    k.tma_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, false>;
-    k.tma_st_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, true>;
+    k.tma_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 0>;
+    k.tma_st_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1>;
+    k.tma_bk_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 2>;
     k.tma_threads = TC::THREADS;
     k.tma_w = TC::W;
     k.tma_boxr = TC::BOXR;

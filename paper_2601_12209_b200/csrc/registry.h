@@ -19,6 +19,7 @@ struct KernelInfo {
   // strided family only: persistent TMA-staged variant (null if not instantiable for n)
   const void* tma_fn = nullptr;
   const void* tma_st_fn = nullptr;  // same, with TMA stores (unsegmented output side)
+  const void* tma_bk_fn = nullptr;  // same, with bulk-copy stores (column-blocked segmented output)
   // two-warp-group variant (preferred when it fits): in-place padded stage buffers
   const void* tma2_fn = nullptr;
   const void* tma2_st_fn = nullptr;

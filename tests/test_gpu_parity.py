@@ -132,12 +132,12 @@ def test_closed_forms_3d_gpu():
 
 
 # ------------------------------------------------------------------------------ simulated ranks
-def _run_sim(oracle_mod, shape, decomp, grid, prec, chunks, seed=5):
+def _run_sim(oracle_mod, shape, decomp, grid, prec, chunks, seed=5, exchange="auto"):
     P = grid[0] * grid[1]
     comm = dfft.Comm.simulated(P, 0)
     dt = "c2c_" + prec
-    fwd = dfft.Plan(comm, shape, decomp, grid, dt, dfft.FORWARD, chunks=chunks)
-    inv = dfft.Plan(comm, shape, decomp, grid, dt, dfft.INVERSE, chunks=chunks)
+    fwd = dfft.Plan(comm, shape, decomp, grid, dt, dfft.FORWARD, chunks=chunks, exchange=exchange)
+    inv = dfft.Plan(comm, shape, decomp, grid, dt, dfft.INVERSE, chunks=chunks, exchange=exchange)
     xs, ys, zs = [], [], []
     for r in range(P):
         lo, n = fwd.box(0, r)
@@ -176,6 +176,47 @@ def test_simulated_ranks(oracle_mod, shape, decomp, grid, chunks, prec):
     ef, er, _ = _run_sim(oracle_mod, shape, decomp, grid, prec, chunks)
     assert ef <= GATE[prec] and er <= GATE[prec], (ef, er)
     assert ef <= QUALITY[prec], ef
+
+
+# fused-store ("p2p") layouts on simulated ranks: the column-blocked receive windows and the
+# peer-window side maps the multi-GPU default uses, at grids gpurun cannot run (2x4, 4x2, 5x2)
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,decomp,grid", [
+    ((32, 24, 16), "pencil", (2, 4)),
+    ((64, 64, 64), "pencil", (4, 2)),
+    ((48, 12, 6), "pencil", (5, 2)),       # uneven splits on every axis
+    ((96, 48, 24), "pencil", (2, 4)),      # blocks not multiples of the 64 B column tile
+    ((64, 64, 64), "slab", (8, 1)),
+    ((256, 128, 64), "pencil", (2, 2)),
+])
+def test_simulated_ranks_fused_store(oracle_mod, shape, decomp, grid, prec):
+    ef, er, _ = _run_sim(oracle_mod, shape, decomp, grid, prec, 0, exchange="p2p")
+    assert ef <= GATE[prec] and er <= GATE[prec], (ef, er)
+    assert ef <= QUALITY[prec], ef
+
+
+# chunked fused-store plans (two-stream pipeline on real ranks): z-chunks forward, x-chunks on
+# column-block bounds inverse, incl. chunks that come out empty
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,decomp,grid,chunks", [
+    ((64, 64, 64), "pencil", (1, 4), 4),
+    ((64, 64, 64), "pencil", (2, 4), 3),
+    ((96, 48, 24), "pencil", (2, 2), 2),
+    ((48, 12, 6), "pencil", (5, 2), 3),
+    ((128, 64, 32), "slab", (2, 1), 8),
+])
+def test_simulated_ranks_fused_store_chunked(oracle_mod, shape, decomp, grid, chunks, prec):
+    ef, er, _ = _run_sim(oracle_mod, shape, decomp, grid, prec, chunks, exchange="p2p")
+    assert ef <= GATE[prec] and er <= GATE[prec], (ef, er)
+    assert ef <= QUALITY[prec], ef
+
+
+def test_fused_store_bitwise_equals_nccl_layouts(oracle_mod):
+    # same kernels and radix schedules, different exchange layouts => identical bits
+    shape = (32, 24, 16)
+    _, _, Y1 = _run_sim(oracle_mod, shape, "pencil", (2, 4), "f64", 1)
+    _, _, Y2 = _run_sim(oracle_mod, shape, "pencil", (2, 4), "f64", 0, exchange="p2p")
+    assert np.array_equal(Y1, Y2)
 
 
 def test_simulated_rank_invariance(oracle_mod):
@@ -224,16 +265,58 @@ def test_headline_1024cubed_c64_single_gpu(oracle_mod):
     assert np.sqrt(d / sx) <= GATE["f32"]
 
 
+def test_headline_1024cubed_c64_2x4_fused_store_simulated(oracle_mod):
+    """BASELINE configs[3] in the 8-GPU headline's decomposition (pencil 2x4, fused-store layouts,
+    the multi-GPU default) on one GPU with simulated ranks: sampled bins vs the oracle's direct
+    sums and the round trip.  Same kernels and addresses as 8 processes, stream order for flags."""
+    shape = (1024, 1024, 1024)
+    seed = 260112209 + 4
+    grid = (2, 4)
+    P = 8
+    comm = dfft.Comm.simulated(P, 0)
+    fwd = dfft.Plan(comm, shape, "pencil", grid, "c2c_f32", dfft.FORWARD, exchange="p2p")
+    inv = dfft.Plan(comm, shape, "pencil", grid, "c2c_f32", dfft.INVERSE, exchange="p2p")
+    xs, ys, zs = [], [], []
+    for r in range(P):
+        lo, n = fwd.box(0, r)
+        x = fwd.alloc_in(r)
+        inputs.fill_box_cuda(x, seed, shape, lo, n, True)
+        xs.append(x)
+        ys.append(fwd.alloc_out(r))
+    fwd.execute_sim(xs, ys)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    ks = [(0, 0, 0), (511, 255, 1023), (512, 256, 0), (1023, 1023, 1023)]
+    ks += [tuple(int(v) for v in rng.integers(0, 1024, 3)) for _ in range(8)]
+    N = float(np.prod(shape))
+    err2 = 0.0
+    for kx, ky, kz in ks:
+        for r in range(P):
+            lo, n = fwd.box(1, r)
+            if all(lo[d] <= k < lo[d] + n[d] for d, k in enumerate((kx, ky, kz))):
+                g = complex(ys[r][kz - lo[2], ky - lo[1], kx - lo[0]].item())
+        ref = oracle_mod.dft3d_bin_seeded(seed, shape, (kx, ky, kz), f32=True)
+        err2 += abs(g - ref) ** 2
+    rms_rel = np.sqrt(err2 / len(ks)) / np.sqrt(2 * N / 3)
+    assert rms_rel <= GATE["f32"], rms_rel
+    zs = [inv.alloc_out(r) for r in range(P)]
+    inv.execute_sim(ys, zs)
+    torch.cuda.synchronize()
+    d = sum((z - x).abs().double().pow(2).sum().item() for z, x in zip(zs, xs))
+    sx = sum(x.abs().double().pow(2).sum().item() for x in xs)
+    assert np.sqrt(d / sx) <= GATE["f32"]
+
+
 # ------------------------------------------------------------------------------ R2C / C2R
-def _r2c_case(oracle_mod, shape, decomp, grid, prec, chunks=0, seed=9):
+def _r2c_case(oracle_mod, shape, decomp, grid, prec, chunks=0, seed=9, exchange="auto"):
     """Forward R2C vs oracle rfft3d; C2R of an arbitrary (non-Hermitian) half spectrum vs the
     oracle's Hermitian-extension C2R (reading R8); C2R(R2C(x)) round trip."""
     nx, ny, nz = shape
     P = grid[0] * grid[1]
     comm = dfft.Comm.simulated(P, 0) if P > 1 else dfft.Comm.create(nranks=1, rank=0, device=0)
     dt = "r2c_" + prec
-    fwd = dfft.Plan(comm, shape, decomp, grid, dt, dfft.FORWARD, chunks=chunks)
-    inv = dfft.Plan(comm, shape, decomp, grid, dt, dfft.INVERSE, chunks=chunks)
+    fwd = dfft.Plan(comm, shape, decomp, grid, dt, dfft.FORWARD, chunks=chunks, exchange=exchange)
+    inv = dfft.Plan(comm, shape, decomp, grid, dt, dfft.INVERSE, chunks=chunks, exchange=exchange)
     f32 = prec == "f32"
     xs, ys = [], []
     for r in range(P):
@@ -289,6 +372,21 @@ def test_r2c_c2r(oracle_mod, shape, decomp, grid, chunks, prec):
     ef, ec, er = _r2c_case(oracle_mod, shape, decomp, grid, prec, chunks)
     assert ef <= GATE[prec] and ec <= GATE[prec] and er <= GATE[prec], (ef, ec, er)
     assert ef <= QUALITY[prec] and ec <= QUALITY[prec], (ef, ec, er)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,grid", [((24, 16, 12), (2, 4)), ((96, 48, 24), (2, 2)), ((48, 24, 12), (4, 1))])
+def test_r2c_c2r_fused_store_simulated(oracle_mod, shape, grid, prec):
+    ef, ec, er = _r2c_case(oracle_mod, shape, "pencil", grid, prec, exchange="p2p")
+    assert ef <= GATE[prec] and ec <= GATE[prec] and er <= GATE[prec], (ef, ec, er)
+    assert ef <= QUALITY[prec] and ec <= QUALITY[prec], (ef, ec, er)
+
+
+def test_cfg5_r2c_2x4_fused_store_simulated(oracle_mod):
+    # BASELINE configs[4] (768x768x384 r2c f64, pencil 2x4, uneven 193/192 bins) in the 8-GPU
+    # default layouts, simulated on one GPU
+    ef, ec, er = _r2c_case(oracle_mod, (768, 768, 384), "pencil", (2, 4), "f64", seed=260112209 + 5, exchange="p2p")
+    assert ef <= 1e-12 and ec <= 1e-12 and er <= 1e-12, (ef, ec, er)
 
 
 def test_cfg5_r2c_768x768x384_f64_single_gpu(oracle_mod):
