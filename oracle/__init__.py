@@ -50,6 +50,10 @@ def _load():
         lib.or_dft3d_naive.argtypes = [_dp, _i64, _i64, _i64, _int, _dp]
         lib.or_rfft3d.argtypes = [_dp, _i64, _i64, _i64, _dp]
         lib.or_irfft3d.argtypes = [_dp, _i64, _i64, _i64, _dp]
+        _d = ctypes.c_double
+        lib.or_poisson_eigen.argtypes = [_i64, _d, _dp]
+        lib.or_poisson3d.argtypes = [_dp, _i64, _i64, _i64, _d, _d, _d, _dp]
+        lib.or_laplacian7.argtypes = [_dp, _i64, _i64, _i64, _d, _d, _d, _dp]
         lib.or_dft3d_bin_seeded.argtypes = [_u64, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64, _dp]
         lib.or_err_sums.argtypes = [_dp, _dp, _i64, _dp]
         lib.or_num_threads.restype = _int
@@ -143,6 +147,31 @@ def irfft3d(half: np.ndarray, nx: int) -> np.ndarray:
     assert nxc == nx // 2 + 1 and nx % 2 == 0
     out = np.empty((nz, ny, nx), dtype=np.float64)
     _load().or_irfft3d(_p(half.view(np.float64)), nx, ny, nz, _p(out))
+    return out
+
+
+def poisson_eigen(n: int, h: float = 1.0) -> np.ndarray:
+    """λ_k = -(2 sin(πk/n)/h)², k < n: eigenvalues of the 3-point second difference (reading R20)."""
+    out = np.empty(n)
+    _load().or_poisson_eigen(n, float(h), _p(out))
+    return out
+
+
+def poisson3d(f: np.ndarray, spacing=(1.0, 1.0, 1.0)) -> np.ndarray:
+    """Zero-mean periodic solution of the 7-point discrete Poisson equation (R20)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    nz, ny, nx = f.shape
+    out = np.empty_like(f)
+    _load().or_poisson3d(_p(f), nx, ny, nz, *[float(h) for h in spacing], _p(out))
+    return out
+
+
+def laplacian7(phi: np.ndarray, spacing=(1.0, 1.0, 1.0)) -> np.ndarray:
+    """7-point periodic discrete Laplacian (pins the Poisson solve)."""
+    phi = np.ascontiguousarray(phi, dtype=np.float64)
+    nz, ny, nx = phi.shape
+    out = np.empty_like(phi)
+    _load().or_laplacian7(_p(phi), nx, ny, nz, *[float(h) for h in spacing], _p(out))
     return out
 
 

@@ -375,6 +375,73 @@ void or_irfft3d(const double* half, int64_t nx, int64_t ny, int64_t nz, double* 
     free(a);
 }
 
+/* ------------------------------------------------------------------ periodic Poisson solve */
+
+/*
+ * Periodic Poisson solve ∇²φ = f on an nx×ny×nz grid with spacings (dx, dy, dz): the paper's
+ * application (§VI-B: the Oceananigans pressure solver on a (Periodic, Periodic,
+ * Periodic) box) with the operator the paper leaves unstated taken as the second-order
+ * 7-point discrete Laplacian (reading R20).  Its eigenvalue on the Fourier mode k is
+ *   λ(k) = -Σ_d (2 sin(π k_d / n_d) / Δ_d)²,
+ * so, step by step: F = R2C(f); Φ(k) = F(k) / λ(k) for k ≠ 0, Φ(0) = 0 (zero-mean solution);
+ * φ = C2R(Φ).  λ is evaluated in long double (sinl), rounded once.
+ */
+void or_poisson_eigen(int64_t n, double h, double* lam) {
+    for (int64_t k = 0; k < n; ++k) {
+        long double s = 2.0L * sinl(3.14159265358979323846264338327950288L * (long double)k / (long double)n) /
+                        (long double)h;
+        lam[k] = (double)(-(s * s));
+    }
+}
+
+void or_poisson3d(const double* f, int64_t nx, int64_t ny, int64_t nz, double dx, double dy, double dz,
+                  double* phi) {
+    int64_t nxc = nx / 2 + 1;
+    double* F = (double*)malloc(sizeof(double) * 2 * (size_t)(nxc * ny * nz));
+    double* lx = (double*)malloc(sizeof(double) * (size_t)nx);
+    double* ly = (double*)malloc(sizeof(double) * (size_t)ny);
+    double* lz = (double*)malloc(sizeof(double) * (size_t)nz);
+    or_poisson_eigen(nx, dx, lx);
+    or_poisson_eigen(ny, dy, ly);
+    or_poisson_eigen(nz, dz, lz);
+    or_rfft3d(f, nx, ny, nz, F);
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t z = 0; z < nz; ++z)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t x = 0; x < nxc; ++x) {
+                double lam = lx[x] + ly[y] + lz[z];
+                double* v = F + 2 * (x + nxc * (y + ny * z));
+                if (x == 0 && y == 0 && z == 0) {
+                    v[0] = 0.0;
+                    v[1] = 0.0;
+                } else {
+                    v[0] /= lam;
+                    v[1] /= lam;
+                }
+            }
+    or_irfft3d(F, nx, ny, nz, phi);
+    free(F);
+    free(lx);
+    free(ly);
+    free(lz);
+}
+
+/* 7-point periodic discrete Laplacian (the operator R20 inverts), used only by the pins. */
+void or_laplacian7(const double* phi, int64_t nx, int64_t ny, int64_t nz, double dx, double dy, double dz,
+                   double* out) {
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t z = 0; z < nz; ++z)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t x = 0; x < nx; ++x) {
+#define PHI(a, b, c) phi[(((a) + nx) % nx) + nx * ((((b) + ny) % ny) + ny * (((c) + nz) % nz))]
+                double c0 = PHI(x, y, z);
+                out[x + nx * (y + ny * z)] = (PHI(x + 1, y, z) - 2 * c0 + PHI(x - 1, y, z)) / (dx * dx) +
+                                             (PHI(x, y + 1, z) - 2 * c0 + PHI(x, y - 1, z)) / (dy * dy) +
+                                             (PHI(x, y, z + 1) - 2 * c0 + PHI(x, y, z - 1)) / (dz * dz);
+#undef PHI
+            }
+}
+
 /* ------------------------------------------------------------------ sampled bins */
 
 /*

@@ -221,3 +221,41 @@ def test_err_sums(oracle_mod):
     ref = np.array([1, 2 + 1j, 3j])
     e, r = oracle_mod.err_sums(y, ref)
     assert e == pytest.approx(2.0) and r == pytest.approx(1 + 5 + 9)
+
+
+# ------------------------------------------------------------------ periodic Poisson solve (f3)
+def _lap_np(phi, h):
+    """The 7-point periodic Laplacian written with numpy rolls (independent of the oracle's C)."""
+    hx, hy, hz = h
+    out = (np.roll(phi, 1, 2) - 2 * phi + np.roll(phi, -1, 2)) / hx**2
+    out += (np.roll(phi, 1, 1) - 2 * phi + np.roll(phi, -1, 1)) / hy**2
+    out += (np.roll(phi, 1, 0) - 2 * phi + np.roll(phi, -1, 0)) / hz**2
+    return out
+
+
+@pytest.mark.parametrize("shape,h", [((8, 6, 4), (1.0, 1.0, 1.0)), ((16, 12, 10), (0.5, 2.0, 1.5)),
+                                     ((48, 24, 12), (1.0, 0.25, 3.0))])
+def test_poisson_inverts_the_discrete_laplacian(oracle_mod, shape, h):
+    # P:606-620 (§VI-B) solves the pressure Poisson equation; reading R20: 7-point Laplacian,
+    # zero-mean solution.  Pin: applying the operator (numpy, not the oracle) gives back f - mean(f).
+    nx, ny, nz = shape
+    f = oracle_mod.gen_real(31, shape)
+    phi = oracle_mod.poisson3d(f, h)
+    assert abs(phi.mean()) < 1e-12
+    r = _lap_np(phi, h) - (f - f.mean())
+    assert np.abs(r).max() <= 1e-11 * np.abs(f).max() * max(1.0, max(1 / v**2 for v in h))
+    assert np.allclose(oracle_mod.laplacian7(phi, h), _lap_np(phi, h), rtol=0, atol=1e-12)
+
+
+def test_poisson_single_mode_closed_form(oracle_mod):
+    # f = cos(2π(mx x/nx + my y/ny + mz z/nz)) is an eigenfunction of the 7-point Laplacian with
+    # eigenvalue -Σ (2 sin(π m_d/n_d)/h_d)² (textbook), so φ = f / λ exactly.
+    nx, ny, nz, h = 24, 16, 12, (1.0, 0.5, 2.0)
+    m = (5, 3, 7)
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    f = np.cos(2 * np.pi * (m[0] * x / nx + m[1] * y / ny + m[2] * z / nz))
+    lam = -sum((2 * np.sin(np.pi * md / nd) / hd) ** 2 for md, nd, hd in zip(m, (nx, ny, nz), h))
+    phi = oracle_mod.poisson3d(f, h)
+    assert np.abs(phi - f / lam).max() < 1e-13
+    lx = oracle_mod.poisson_eigen(nx, 0.5)
+    assert lx[0] == 0.0 and abs(lx[nx // 2] + 16.0) < 1e-13  # -(2/h)^2 at the Nyquist mode

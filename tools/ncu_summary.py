@@ -24,4 +24,5 @@ if __name__ == "__main__":
         t = m.get("gpu__time_duration.sum", 0) / 1e6
         rd = m.get("dram__bytes_read.sum", 0) / 1e9
         wr = m.get("dram__bytes_write.sum", 0) / 1e9
-        print(f"{i:3d} {m['name'][:70]:70s} {t:8.3f} ms  R {rd:6.2f} W {wr:6.2f} GB  {(rd + wr) / t if t else 0:7.0f} GB/s")
+        tx = m.get("lts__t_sectors_srcunit_tex_op_read.sum", 0) * 32 / 1e9
+        print(f"{i:3d} {m['name'][:60]:60s} {t:8.3f} ms  R {rd:6.2f} W {wr:6.2f} GB  L2req R {tx:6.2f} GB  {(rd + wr) / t if t else 0:6.2f} TB/s")
