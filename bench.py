@@ -43,6 +43,10 @@ def parse():
     p.add_argument("--precision", default="f32", choices=["f32", "f64"])
     p.add_argument("--strategy", default="pencil", choices=["pencil", "slab"])
     p.add_argument("--grid-p", default="", help="process grid P1,P2 (default by N)")
+    p.add_argument("--kind", default="c2c", choices=["c2c", "r2c"], help="r2c: real input, R2C forward + C2R inverse")
+    p.add_argument("--poisson", action="store_true",
+                   help="periodic Poisson solve: R2C/C2C forward with the fused 1/λ(k) multiplier, then the inverse "
+                        "(SURVEY §8(f) f3, P:606-620)")
     p.add_argument("--chunks", type=int, default=0)
     p.add_argument("--no-overlap", action="store_true")
     p.add_argument("--exchange", default="auto", choices=["auto", "ce", "p2p", "hybrid", "nccl"],
@@ -55,9 +59,10 @@ def parse():
     return p.parse_args()
 
 
-def flops_fwd_inv(shape):
+def flops_fwd_inv(shape, kind="c2c"):
+    """5·N·log2N per c2c transform; R2C/C2R with the real-data convention 2.5·N·log2N (reading Z9)."""
     N = shape[0] * shape[1] * shape[2]
-    return 2 * 5.0 * N * math.log2(N)
+    return 2 * (2.5 if kind == "r2c" else 5.0) * N * math.log2(N)
 
 
 def load_peaks():
@@ -205,16 +210,18 @@ def main():
         grid = tuple(int(v) for v in args.grid_p.split(","))
     else:
         grid = (N, 1) if args.strategy == "slab" else GRIDS.get(N, (1, N))
-    dt = "c2c_" + args.precision
+    dt = args.kind + "_" + args.precision
     es = 8 if args.precision == "f32" else 16
     comm = dfft.Comm.create(nranks=world, rank=rank, device=local)
     fwd = dfft.Plan(comm, shape, args.strategy, grid, dt, dfft.FORWARD, chunks=args.chunks,
                     overlap=not args.no_overlap, exchange=args.exchange)
     inv = dfft.Plan(comm, shape, args.strategy, grid, dt, dfft.INVERSE, chunks=args.chunks,
                     overlap=not args.no_overlap, exchange=args.exchange)
+    if args.poisson:
+        fwd.set_poisson((1.0, 1.0, 1.0))
     lo, n = fwd.box(0)
     x = fwd.alloc_in()
-    inputs.fill_box_cuda(x, args.seed, shape, lo, n, True)
+    inputs.fill_box_cuda(x, args.seed, shape, lo, n, args.kind == "c2c")
     y = fwd.alloc_out()
     z = inv.alloc_out()
     stream = torch.cuda.current_stream()
@@ -256,7 +263,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = t.item()
     ms_step = ms_total / max(args.steps, 1)
-    gflops = flops_fwd_inv(shape) / (ms_step * 1e-3) / 1e9
+    gflops = flops_fwd_inv(shape, args.kind) / (ms_step * 1e-3) / 1e9
 
     # --- roofline of the dominant kernel (largest total time among the FFT stages)
     hbm_peak, peak_kind = load_peaks()
@@ -300,9 +307,12 @@ def main():
     # --- north-star roofline: T_roof = max(T_HBM, T_NVL) per GPU for fwd+inv
     P = grid[0] * grid[1]
     Nloc = shape[0] * shape[1] * shape[2] / P
-    t_hbm = 2 * 6 * Nloc * es / (hbm_peak * 1e9)
+    # complex elements per rank after stage 1 (R2C: nx/2+1 bins along x) and stage-1 bytes
+    Ncl = Nloc * ((shape[0] // 2 + 1) / shape[0] if args.kind == "r2c" else 1.0)
+    a_bytes = (Nloc * es / 2 if args.kind == "r2c" else Nloc * es) + Ncl * es
+    t_hbm = 2 * (a_bytes + 4 * Ncl * es) / (hbm_peak * 1e9)
     p1, p2 = (1, P) if args.strategy == "slab" else grid
-    nvl_bytes = Nloc * es * ((p1 - 1) / p1 + (p2 - 1) / p2)
+    nvl_bytes = Ncl * es * ((p1 - 1) / p1 + (p2 - 1) / p2)
     t_nvl = 2 * nvl_bytes / (NVLINK_GBS * 1e9)
     t_roof = max(t_hbm, t_nvl)
     breakdown = {f"fwd_{k}": v[0] / args.steps for k, v in pf.items() if v[1]}
@@ -336,7 +346,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         el = te.item()
-        e2e = {"value": flops_fwd_inv(shape) / (el * 1e-3) / 1e9, "unit": "GFLOP/s",
+        e2e = {"value": flops_fwd_inv(shape, args.kind) / (el * 1e-3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(x.numel() * x.element_size()),
                "d2h_bytes_per_step": int(z.numel() * z.element_size()), "ms_per_step": el,
                "path": "pinned host -> Plan.execute(fwd) -> Plan.execute(inv) -> pinned host"}
@@ -350,8 +360,12 @@ def main():
             "metric": METRIC, "value": gflops * 1.0, "unit": "GFLOP/s", "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-            "config": {"workload": f"{shape[0]}x{shape[1]}x{shape[2]} complex{'64' if es == 8 else '128'} c2c "
-                                   f"{args.strategy} {grid[0]}x{grid[1]} fwd+inv",
+            "config": {"workload": f"{shape[0]}x{shape[1]}x{shape[2]} "
+                                   + (f"complex{'64' if es == 8 else '128'} c2c" if args.kind == "c2c" else
+                                      f"{'f32' if es == 8 else 'f64'} r2c")
+                                   + f" {args.strategy} {grid[0]}x{grid[1]} "
+                                   + ("Poisson solve (fwd + 1/λ fused + inv)" if args.poisson else "fwd+inv"),
+                       "flop_convention": "2.5·N·log2N per R2C/C2R" if args.kind == "r2c" else "5·N·log2N per c2c",
                        "grid": list(shape), "proc_grid": list(grid), "chunks": fwd.chunks(),
                        "exchange": args.exchange if world > 1 else "none",
                        "overlap": not args.no_overlap,

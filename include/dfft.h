@@ -164,6 +164,19 @@ dfft_status_t dfft_execute_host(dfft_plan_t plan, const void* in_host, void* out
 /* Simulated comm only: ins[r] / outs[r] are rank r's device boxes, r < nranks. */
 dfft_status_t dfft_execute_sim(dfft_plan_t plan, const void* const* ins, void* const* outs, void* stream);
 
+/*
+ * Periodic Poisson solve, fused (the paper's application, §VI-B:
+ * the Oceananigans pressure Poisson solver on a (Periodic, Periodic, Periodic) box).
+ * Turns a FORWARD plan into  F(k) -> F(k) / λ(k),  λ(k) = -Σ_d (2 sin(π k_d / n_d) / h_d)²
+ * (the eigenvalues of the 7-point discrete Laplacian with spacings h = (dx, dy, dz); DESIGN.md
+ * reading R20), with F(0) -> 0 (the zero-mean solution).  The multiply is fused into the
+ * epilogue of the plan's last stage (no extra pass over HBM).  Executing the forward plan and
+ * then the matching INVERSE plan (C2R for R2C plans) solves ∇²φ = f for zero-mean φ.
+ * dx = dy = dz = 0 switches the multiplier off again.  Synchronises the device (plan setup,
+ * not for the hot path).  Errors: INVALID_VALUE for an inverse plan or non-positive spacings.
+ */
+dfft_status_t dfft_plan_set_poisson(dfft_plan_t plan, double dx, double dy, double dz);
+
 /* ------------------------------------------------------------------ per-phase profiling
  * Phases (Fig. 9 breakdown analog): 0 stage-A FFT, 1 first exchange, 2 stage-B FFT,
  * 3 second exchange, 4 stage-C FFT.  When enabled, every stage launch and exchange of

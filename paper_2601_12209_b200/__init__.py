@@ -34,6 +34,7 @@ EXPORTS = [
     "dfft_comm_init_sim", "dfft_comm_destroy", "dfft_plan_create", "dfft_plan_box", "dfft_plan_box_rank",
     "dfft_plan_bytes", "dfft_decomp_box", "dfft_plan_chunks", "dfft_execute", "dfft_execute_host", "dfft_execute_sim",
     "dfft_destroy", "dfft_fft1d", "dfft_plan_set_profiling", "dfft_plan_phase_times", "dfft_plan_stage_bytes",
+    "dfft_plan_set_poisson",
 ]
 PHASES = ["stage_A", "exchange_1", "stage_B", "exchange_2", "stage_C"]
 
@@ -81,6 +82,7 @@ def lib():
         L.dfft_destroy.argtypes = [_vp]
         L.dfft_fft1d.argtypes = [_vp, _vp, _i64, _i64, _int, _int, _vp]
         L.dfft_plan_set_profiling.argtypes = [_vp, _int]
+        L.dfft_plan_set_poisson.argtypes = [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double]
         L.dfft_plan_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), _int]
         L.dfft_plan_stage_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
         for name in EXPORTS:
@@ -256,6 +258,14 @@ class Plan:
         outs = (_vp * P)(*[y.data_ptr() for y in ys])
         _check(lib().dfft_execute_sim(self.h, ins, outs, _stream_ptr(stream, xs[0].device)), "dfft_execute_sim")
         return ys
+
+    # periodic Poisson solve (fused spectral divide; forward plans) ------------------
+    def set_poisson(self, spacing=(1.0, 1.0, 1.0)):
+        """Forward plan: multiply the spectrum by 1/λ(k) of the 7-point Laplacian (0 at k = 0) in
+        the last stage's epilogue; spacing None switches it off (dfft_plan_set_poisson)."""
+        dx, dy, dz = (0.0, 0.0, 0.0) if spacing is None else (float(v) for v in spacing)
+        _check(lib().dfft_plan_set_poisson(self.h, dx, dy, dz), "dfft_plan_set_poisson")
+        return self
 
     # profiling ----------------------------------------------------------------------
     def set_profiling(self, on: bool = True):

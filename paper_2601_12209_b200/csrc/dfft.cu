@@ -231,6 +231,11 @@ struct Stage {
   int tma_variant = 0;     // 1 = single-group TMA kernel, 2 = two-group in-place kernel
   const void* tw_tma = nullptr;  // twiddles of the TMA variant's radix schedule
   bool empty = false;
+  // last forward stage: which global axis (0 x, 1 y, 2 z) its t / l0 / l1 run along and the
+  // rank's global offset of each (dfft_plan_set_poisson addresses the λ tables with them)
+  bool last_fwd = false;
+  int gax[3] = {0, 0, 0};
+  long long glo[3] = {0, 0, 0};
 };
 
 struct Xfer {
@@ -292,6 +297,7 @@ struct dfft_plan_s {
   // C(k) overlaps the NVLink-bound B(k+1)
   bool bc = false;
   std::vector<void*> peer_ws;        // by global rank (own rank = own workspace), null if not a peer
+  void* spec_tab = nullptr;          // dfft_plan_set_poisson: λ tables [nx | ny | nz] (Real)
   size_t flag_off = 0;               // byte offset of the flag block in every workspace
   unsigned int epoch = 0;            // executes so far (flag values)
   // per-phase profiling (dfft_plan_set_profiling): timing events around every stage launch
@@ -726,6 +732,9 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     set_side(C.a.in, Xn, 1, g.nz * Xn);
   }
   C.a.scale = 1.0;
+  C.last_fwd = true;  // t = z, l0 = x, l1 = y
+  C.gax[0] = 2, C.gax[1] = 0, C.gax[2] = 1;
+  C.glo[1] = g.Xlo(i), C.glo[2] = g.Y3lo(j);
   ST(finish_stage(pl, C, kStrided, (int)g.nz, Xn, Y3n, nullptr, nullptr));
   return DFFT_SUCCESS;
 }
@@ -800,6 +809,9 @@ dfft_status_t build_forward_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.out = {kUserOut, x0 * es};
     set_side(C.a.out, Y3n * Xn, 1, Xn);
     C.a.scale = 1.0;
+    C.last_fwd = true;  // t = z, l0 = x - x0, l1 = y
+    C.gax[0] = 2, C.gax[1] = 0, C.gax[2] = 1;
+    C.glo[1] = g.Xlo(i) + x0, C.glo[2] = g.Y3lo(j);
     ST(finish_stage(pl, C, kStrided, (int)g.nz, xc, Y3n, nullptr, nullptr));
   }
   return DFFT_SUCCESS;
@@ -929,6 +941,8 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.out = {kUserOut, 0};
     set_side(C.a.out, nxc, 1, ny * nxc);
     C.a.scale = 1.0;
+    C.last_fwd = true;  // t = y, l0 = x, l1 = z
+    C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
     ST(finish_stage(pl, C, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
   } else {
     A.in = {kUserIn, 0};  // columns (l0 = x, l1 = z)
@@ -1559,6 +1573,7 @@ void free_plan(dfft_plan_t pl) {
     if (e) cudaEventDestroy(e);
   if (pl->s_comp) cudaStreamDestroy(pl->s_comp);
   if (pl->s_comm) cudaStreamDestroy(pl->s_comm);
+  if (pl->spec_tab) cudaFree(pl->spec_tab);
   if (pl->stage_in) cudaFree(pl->stage_in);
   if (pl->stage_out) cudaFree(pl->stage_out);
   delete pl;
@@ -1572,7 +1587,7 @@ struct PlanGuard {
 };
 
 // Fused-store plans with K > 1 run stage A(k+1) and B(k) concurrently on two streams.  The one
-// of the pair that stores to peers (NVLink-bound) gets at most DFFT_NVL_SMS SMs (default 64) and
+// of the pair that stores to peers (NVLink-bound) gets at most DFFT_NVL_SMS SMs (default 80) and
 // the HBM-bound one the rest, except in the last chunk, which runs alone.
 dfft_status_t apply_sm_caps(dfft_plan_t pl, RankPlan& rp) {
   const size_t K = rp.A.size();
@@ -1580,7 +1595,7 @@ dfft_status_t apply_sm_caps(dfft_plan_t pl, RankPlan& rp) {
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->comm->device));
   const char* v = getenv("DFFT_NVL_SMS");
-  const int nvl = std::max(1, std::min(sms - 1, v ? atoi(v) : 64));
+  const int nvl = std::max(1, std::min(sms - 1, v ? atoi(v) : 80));
   if (pl->bc) {  // B(k) stores to peers, C(k) runs beside B(k+1)
     for (size_t k = 0; k < K; ++k) {
       rp.B[k].sm_cap = nvl;
@@ -1761,7 +1776,9 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   // fused stores: with a 1×P2 grid the x-FFT is local and overlaps the NVLink-bound y-FFT of the
   // previous chunk (two streams); with P1 > 1 both are NVLink-bound, so one chunk
   const bool bc_mode = p2p_mode && p1 > 1 && p2 > 1;
-  if (p2p_mode && Kreq == 0) K = 1;  // r01 sweep: fused stores need every SM
+  // r01 sweeps: fused stores need most SMs, so A(k+1)‖B(k) overlap does not pay
+  // (one chunk); with both exchanges remote, B(k)‖C(k-1) with B on 100 SMs does (2x2: 9.0 -> 8.6 ms)
+  if (p2p_mode && Kreq == 0) K = bc_mode ? 4 : 1;
   if (bc_mode) kmax = direction == DFFT_FORWARD ? nxc / p1 : nz / p2;
   K = std::max<long long>(1, std::min<long long>(K, kmax));
   if (P == 1) K = 1;  // nothing to overlap
@@ -1980,6 +1997,52 @@ dfft_status_t dfft_execute_sim(dfft_plan_t pl, const void* const* ins, void* con
   ST(execute_sim(pl, ins, outs, (cudaStream_t)stream));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(DFFT_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double dz) {
+  if (!pl) return fail(DFFT_ERR_INVALID_VALUE, "null plan");
+  if (pl->dir != DFFT_FORWARD) return fail(DFFT_ERR_INVALID_VALUE, "the Poisson multiplier belongs to a forward plan");
+  const bool on = dx > 0 && dy > 0 && dz > 0;
+  if (!on && (dx != 0 || dy != 0 || dz != 0))
+    return fail(DFFT_ERR_INVALID_VALUE, "grid spacings must all be > 0 (or all 0 to switch the multiplier off)");
+  CU(cudaSetDevice(pl->comm->device));
+  CU(cudaDeviceSynchronize());  // no execute of this plan may be reading the old tables
+  if (pl->spec_tab) cudaFree(pl->spec_tab);
+  pl->spec_tab = nullptr;
+  const long long n[3] = {pl->nx, pl->ny, pl->nz};
+  const double h[3] = {dx, dy, dz};
+  const size_t rs = pl->es / 2;
+  if (on) {
+    // λ_d(k) = -(2 sin(πk/n_d)/h_d)², long double, rounded once to the plan's precision (reading R20)
+    std::vector<unsigned char> host((size_t)(n[0] + n[1] + n[2]) * rs);
+    long long o = 0;
+    for (int d = 0; d < 3; ++d)
+      for (long long k = 0; k < n[d]; ++k, ++o) {
+        const long double sv = 2.0L * sinl(3.14159265358979323846264338327950288L * (long double)k / (long double)n[d]) /
+                               (long double)h[d];
+        const long double lam = -(sv * sv);
+        if (pl->f64) reinterpret_cast<double*>(host.data())[o] = (double)lam;
+        else reinterpret_cast<float*>(host.data())[o] = (float)lam;
+      }
+    CU(cudaMalloc(&pl->spec_tab, host.size()));
+    CU(cudaMemcpy(pl->spec_tab, host.data(), host.size(), cudaMemcpyHostToDevice));
+  }
+  const long long base[3] = {0, n[0], n[0] + n[1]};
+  int nlast = 0;
+  for (RankPlan& rp : pl->ranks) {
+    std::vector<Stage*> st{&rp.C};
+    for (Stage& c : rp.Cc) st.push_back(&c);
+    for (Stage* s : st) {
+      if (!s->last_fwd) continue;
+      ++nlast;
+      for (int q = 0; q < 3; ++q)
+        s->a.spec[q] = on ? (const void*)((const char*)pl->spec_tab + (size_t)(base[s->gax[q]] + s->glo[q]) * rs)
+                          : nullptr;
+      if (on && s->tma_variant == 2) s->tma_grid = 0;  // the two-group kernel has no multiplier
+    }
+  }
+  if (nlast == 0) return fail(DFFT_ERR_INTERNAL, "plan has no last forward stage");
   return DFFT_SUCCESS;
 }
 

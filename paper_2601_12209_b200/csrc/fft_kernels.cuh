@@ -361,6 +361,11 @@ struct PassArgs {
   // lines: g0 = 1 suits a side where adjacent l1 are adjacent in memory (column-blocked
   // windows), a small g0 balances a blocked side against a natural one.
   int g0;
+  // spectral multiplier of the last forward stage (dfft_plan_set_poisson): per-axis tables of
+  // the discrete Laplacian's eigenvalues λ_d (Real, indexed by the local t / l0 / l1 of this stage,
+  // already offset to the rank's global bins); each output is multiplied by 1/(λt+λ0+λ1), 0 at
+  // k = 0.  spec[0] == nullptr: off.
+  const void* spec[3];
 };
 
 // tile -> (column tile tx, line l1) under the grouped order above
@@ -455,6 +460,23 @@ template <typename C, bool UNIT_T = false> struct GIO {
   long long i0, i1, o0, o1;  // effective (l0, l1) per side
   long long lin, lout;       // unsegmented sides: l0·s0 + l1·s1
   decltype(C{}.x) scale;
+  using R = decltype(C{}.x);
+  const R* spt = nullptr;  // spectral multiplier (PassArgs::spec): λ table along t, and λ0[l0] + λ1[l1]
+  R lam01 = 0;
+  __device__ __forceinline__ void spectral(const PassArgs& a, long long l0_, long long l1_) {
+    if (a.spec[0] == nullptr) return;
+    spt = reinterpret_cast<const R*>(a.spec[0]);
+    lam01 = __ldg(reinterpret_cast<const R*>(a.spec[1]) + l0_) + __ldg(reinterpret_cast<const R*>(a.spec[2]) + l1_);
+  }
+  __device__ __forceinline__ C apply_spec(int t, C v) const {
+    if (spt != nullptr) {
+      const R lam = __ldg(spt + t) + lam01;
+      const R g = lam != R(0) ? R(1) / lam : R(0);
+      v.x *= g;
+      v.y *= g;
+    }
+    return v;
+  }
   __device__ __forceinline__ void init(const SideMap& i, const SideMap& o, long long l0_, long long l1_, double sc) {
     in = reinterpret_cast<const C*>(i.base);
     out = reinterpret_cast<C*>(o.base);
@@ -475,6 +497,7 @@ template <typename C, bool UNIT_T = false> struct GIO {
   }
   __device__ __forceinline__ void store(int t, C v) const {
     if (scale != 1) { v.x *= scale; v.y *= scale; }
+    v = apply_spec(t, v);
     if (mo->ttab == nullptr) st_out(out + (UNIT_T ? lout + t : (long long)t * mo->tstride + lout), v);
     else st_out(seg_ptr<C>(*mo, t, o0, o1), v);
   }
@@ -607,6 +630,7 @@ fft_strided_kernel(const __grid_constant__ PassArgs a) {
   const bool active = l0 < a.L0;
   GIO<C> io;
   io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
+  io.spectral(a, active ? l0 : 0, l1);
   StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
   stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
 }
@@ -721,7 +745,7 @@ template <typename C, int W, int OM> struct TmaIO : GIO<C> {
   __device__ __forceinline__ void store(int t, C v) const {
     if constexpr (OM != 0) {
       if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
-      obuf[t * W + c] = v;
+      obuf[t * W + c] = this->apply_spec(t, v);
     } else {
       GIO<C>::store(t, v);
     }
@@ -793,6 +817,7 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     if (TST && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
     TmaIO<C, Cfg::W, OM> io;
     io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
+    io.spectral(a, active ? l0 : 0, l1);
     io.obuf = work;
     io.stage = stages + s * Cfg::STAGE_ELEMS;
     io.c = c;

@@ -393,3 +393,68 @@ def test_cfg5_r2c_768x768x384_f64_single_gpu(oracle_mod):
     # BASELINE configs[4] shape (fp64, mixed radix 3·2^k) on one GPU: forward vs oracle, round trip
     ef, ec, er = _r2c_case(oracle_mod, (768, 768, 384), "pencil", (1, 1), "f64", seed=260112209 + 5)
     assert ef <= 1e-12 and ec <= 1e-12 and er <= 1e-12, (ef, ec, er)
+
+
+# ------------------------------------------------------------------------------ Poisson (f3)
+def _poisson_case(oracle_mod, shape, decomp, grid, prec, spacing, kind="r2c", exchange="auto", seed=21):
+    """Forward plan with the fused 1/λ(k) multiplier, then the inverse plan: φ vs the oracle's
+    poisson3d (reading R20) on the same seeded f."""
+    nx, ny, nz = shape
+    P = grid[0] * grid[1]
+    comm = dfft.Comm.simulated(P, 0) if P > 1 else dfft.Comm.create(nranks=1, rank=0, device=0)
+    dt = kind + "_" + prec
+    fwd = dfft.Plan(comm, shape, decomp, grid, dt, dfft.FORWARD, exchange=exchange).set_poisson(spacing)
+    inv = dfft.Plan(comm, shape, decomp, grid, dt, dfft.INVERSE, exchange=exchange)
+    f32 = prec == "f32"
+    xs, ys, zs = [], [], []
+    for r in range(P):
+        lo, n = fwd.box(0, r)
+        x = fwd.alloc_in(r)
+        inputs.fill_box_cuda(x, seed, shape, lo, n, kind == "c2c")
+        xs.append(x)
+        ys.append(fwd.alloc_out(r))
+        zs.append(inv.alloc_out(r))
+    if P > 1:
+        fwd.execute_sim(xs, ys)
+        inv.execute_sim(ys, zs)
+    else:
+        fwd.execute(xs[0], ys[0])
+        inv.execute(ys[0], zs[0])
+    torch.cuda.synchronize()
+    if kind == "r2c":
+        f = oracle_mod.gen_real(seed, shape, f32=f32)
+        ref = oracle_mod.poisson3d(f, spacing)
+        Z = np.zeros((nz, ny, nx))
+    else:  # complex f: the solve is linear, so re and im parts separately
+        a = oracle_mod.gen_complex(seed, shape, f32=f32)
+        ref = oracle_mod.poisson3d(a.real.copy(), spacing) + 1j * oracle_mod.poisson3d(a.imag.copy(), spacing)
+        Z = np.zeros((nz, ny, nx), dtype=complex)
+    for r in range(P):
+        lo, n = inv.box(1, r)
+        box_slice(Z, lo, n)[...] = zs[r].cpu().numpy()
+    return oracle_mod.rel_l2(Z, ref)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,decomp,grid,spacing,kind", [
+    ((16, 12, 8), "pencil", (1, 1), (1.0, 1.0, 1.0), "r2c"),
+    ((64, 48, 24), "pencil", (1, 1), (0.5, 2.0, 1.5), "r2c"),
+    ((32, 24, 16), "pencil", (1, 1), (1.0, 0.25, 3.0), "c2c"),
+    ((48, 24, 12), "pencil", (2, 4), (1.0, 2.0, 0.5), "r2c"),   # fused-store layouts, B->C chunks
+    ((96, 48, 24), "pencil", (2, 2), (1.0, 1.0, 1.0), "c2c"),
+    ((64, 32, 16), "slab", (4, 1), (2.0, 1.0, 1.0), "r2c"),
+])
+def test_poisson_fused(oracle_mod, shape, decomp, grid, spacing, kind, prec):
+    e = _poisson_case(oracle_mod, shape, decomp, grid, prec, spacing, kind, exchange="p2p" if grid != (1, 1) else "auto")
+    assert e <= GATE[prec], e
+
+
+def test_poisson_nccl_layouts_simulated(oracle_mod):
+    e = _poisson_case(oracle_mod, (48, 24, 12), "pencil", (2, 4), "f64", (1.0, 1.0, 1.0), "r2c", exchange="nccl")
+    assert e <= GATE["f64"], e
+
+
+def test_poisson_cfg5_box_f64(oracle_mod):
+    # the paper's application shape class (Oceananigans periodic box, BASELINE configs[4])
+    e = _poisson_case(oracle_mod, (768, 768, 384), "pencil", (1, 1), "f64", (1.0, 1.0, 1.0), "r2c", seed=260112209 + 5)
+    assert e <= 1e-12, e
