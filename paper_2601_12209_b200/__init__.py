@@ -82,12 +82,13 @@ def lib():
         L.dfft_destroy.argtypes = [_vp]
         L.dfft_fft1d.argtypes = [_vp, _vp, _i64, _i64, _int, _int, _vp]
         L.dfft_plan_set_profiling.argtypes = [_vp, _int]
-        L.dfft_plan_set_poisson.argtypes = [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double]
+        if hasattr(L, "dfft_plan_set_poisson"):  # (absent from older dev A/B builds)
+            L.dfft_plan_set_poisson.argtypes = [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double]
         L.dfft_plan_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), _int]
         L.dfft_plan_stage_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
         for name in EXPORTS:
-            if name not in ("dfft_version", "dfft_status_string", "dfft_last_error"):
-                getattr(L, name).restype = _int
+            if name not in ("dfft_version", "dfft_status_string", "dfft_last_error") and hasattr(L, name):
+                getattr(L, name).restype = _int  # (every symbol exists in the in-tree build: test_abi)
         _lib = L
     return _lib
 

@@ -908,6 +908,105 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
 // separable).  Order the stages so no stage both reads and writes at a large stride:
 //   forward: x (in -> out, natural), z (out -> ws as [y][z][x]), y (ws -> out, natural)
 //   inverse: y (in -> out, natural), z (out -> ws as [y][z][x]), x (ws -> out, natural, ×1/N)
+// Single GPU, blocked middle layout (r01 session 2): every pass keeps both sides at a small
+// pitch, so a 1024-row column spans a few 2 MB pages instead of one page per row.
+//   forward: x (in -> L1 = [y][z][x] in `out`), z (L1 -> L2 = [xb][z][y][w] in ws),
+//            y (L2 -> `out`, natural)
+//   inverse: y (in -> L2), z (L2 -> L1), x (L1 -> `out`, natural, ×1/N)
+// L2 is column-blocked with the strided TMA tile width w (a y-pass tile = one contiguous
+// 64 KB block; the z-pass writes it with 4D TMA stores).  Needs the TMA kernel for ny and nz
+// with equal tile widths; otherwise build_single (the natural-layout order) is used.
+bool single_blocked_ok(dfft_plan_t pl, const Geo& g) {
+  // opt-in (measured slower): the z-pass's 4D TMA stores at a 64 KB pitch ran at
+  // 3.3 TB/s and the blocked y-pass reads did not beat the 8 MB-pitch ones (1024^3 c64:
+  // fwd+inv 25.1 vs 22.8 ms on the same B200)
+  if (!getenv("DFFT_SINGLE_BLOCKED") || !g_use_tma || !g_tma_store) return false;
+  KernelInfo ky, kz;
+  const int dir = pl->dir;
+  const bool oky = pl->f64 ? lookup_kernel_f64(kStrided, (int)g.ny, dir, &ky) : lookup_kernel_f32(kStrided, (int)g.ny, dir, &ky);
+  const bool okz = pl->f64 ? lookup_kernel_f64(kStrided, (int)g.nz, dir, &kz) : lookup_kernel_f32(kStrided, (int)g.nz, dir, &kz);
+  if (!oky || !okz || !ky.tma_fn || !kz.tma_fn || ky.tma_w != kz.tma_w) return false;
+  const long long w = ky.tma_w;
+  // the inverse c2c uses `out` as the L2 scratch: no padding room there
+  if (pl->dir == DFFT_INVERSE && !pl->r2c && g.nxc % w != 0) return false;
+  return g.ny * (long long)pl->es % 16 == 0 && g.nxc * (long long)pl->es % 16 == 0;
+}
+
+dfft_status_t build_single_blocked(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
+  const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
+  const long long nxl = pl->r2c ? nx / 2 : nx;
+  KernelInfo ky;
+  if (!(pl->f64 ? lookup_kernel_f64(kStrided, (int)ny, pl->dir, &ky) : lookup_kernel_f32(kStrided, (int)ny, pl->dir, &ky)))
+    return fail(DFFT_ERR_INTERNAL, "no strided kernel for ny");
+  const long long w = ky.tma_w;
+  const long long W = nxc * ny * nz, Wb = round_up(nxc, w) * ny * nz;
+  const bool c2r = pl->r2c && pl->dir == DFFT_INVERSE;
+  rp.A.resize(1);
+  rp.B.resize(1);
+  rp.E1.resize(1);
+  rp.E2.resize(1);
+  Stage &A = rp.A[0], &B = rp.B[0], &C = rp.C;
+  // L1 [y][z][x]: (x, y, z) at x + nxc·(z + nz·y);  L2 [xb][z][y][w]: blocked, block stride ny·nz·w
+  auto set_l1_lines = [&](SideMap& m) { set_side(m, 1, nz * nxc, nxc); };  // contig: l0 = y, l1 = z
+  auto set_l2_zpass = [&](SideMap& m) {  // t = z, l0 = x, l1 = y
+    set_side(m, ny * w, 1, w);
+    m.bw = (int)w;
+    m.mT = nz * ny;
+  };
+  auto set_l2_ypass = [&](SideMap& m) {  // t = y, l0 = x, l1 = z
+    set_side(m, w, 1, ny * w);
+    m.bw = (int)w;
+    m.mT = nz;
+  };
+  if (pl->dir == DFFT_FORWARD) {
+    rp.ws_bytes = (size_t)(Wb * es);
+    A.in = {kUserIn, 0};  // x-pass: lines (l0 = y, l1 = z), natural in
+    set_side(A.a.in, 1, nxl, ny * nxl);
+    A.out = {kUserOut, 0};
+    set_l1_lines(A.a.out);
+    A.a.scale = 1.0;
+    ST(finish_stage(pl, A, pl->r2c ? kContigR2C : kContig, (int)nxl, ny, nz, nullptr, nullptr));
+    B.in = {kUserOut, 0};  // z-pass: columns (l0 = x, l1 = y) of L1 -> L2
+    set_side(B.a.in, nxc, 1, nz * nxc);
+    B.out = {kWs, 0};
+    set_l2_zpass(B.a.out);
+    B.a.scale = 1.0;
+    ST(finish_stage(pl, B, kStrided, (int)nz, nxc, ny, nullptr, nullptr));
+    C.in = {kWs, 0};  // y-pass: columns (l0 = x, l1 = z) of L2 -> natural `out`
+    set_l2_ypass(C.a.in);
+    C.out = {kUserOut, 0};
+    set_side(C.a.out, nxc, 1, ny * nxc);
+    C.a.scale = 1.0;
+    C.last_fwd = true;  // t = y, l0 = x, l1 = z
+    C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
+    ST(finish_stage(pl, C, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
+  } else {
+    // scratch: c2c: L2 in `out` (nxc % w == 0 checked), L1 in ws;  c2r: both in ws
+    rp.ws_bytes = (size_t)((c2r ? Wb + W : W) * es);
+    const Ref l2 = c2r ? Ref{kWs, 0} : Ref{kUserOut, 0};
+    const Ref l1 = c2r ? Ref{kWs, Wb * es} : Ref{kWs, 0};
+    A.in = {kUserIn, 0};  // y-pass: columns (l0 = x, l1 = z), natural in -> L2
+    set_side(A.a.in, nxc, 1, ny * nxc);
+    A.out = l2;
+    set_l2_ypass(A.a.out);
+    A.a.scale = 1.0;
+    ST(finish_stage(pl, A, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
+    B.in = l2;  // z-pass: columns (l0 = x, l1 = y) of L2 -> L1
+    set_l2_zpass(B.a.in);
+    B.out = l1;
+    set_side(B.a.out, nxc, 1, nz * nxc);
+    B.a.scale = 1.0;
+    ST(finish_stage(pl, B, kStrided, (int)nz, nxc, ny, nullptr, nullptr));
+    C.in = l1;  // x-pass: lines (l0 = y, l1 = z) of L1 -> natural `out`, ×1/N
+    set_l1_lines(C.a.in);
+    C.out = {kUserOut, 0};
+    set_side(C.a.out, 1, nxl, ny * nxl);
+    C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
+    ST(finish_stage(pl, C, c2r ? kContigC2R : kContig, (int)nxl, ny, nz, nullptr, nullptr));
+  }
+  return DFFT_SUCCESS;
+}
+
 dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
   const long long nxl = pl->r2c ? nx / 2 : nx;
@@ -1172,10 +1271,14 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
     const bool in_ok = a.in.bw > 0 ? (s.tma_variant == 1 && encode4(&tin, a.in))
                                    : encode(&tin, a.in.base, a.in.tstride, a.in.s1);
     if (in_ok) {
-      bool use_st = g_tma_store && a.out.ttab == nullptr && a.out.bw == 0 && a.out.s0 == 1 &&
+      // TMA stores: unsegmented output, 3D, or 4D into a column-blocked output whose block is
+      // the tile (single-group kernel)
+      const bool out_blk_ok = a.out.bw == 0 || (s.tma_variant == 1 && a.out.bw == s.k.tma_w &&
+                                                (a.out.mT * a.out.s1 * (long long)ces) % 16 == 0);
+      bool use_st = g_tma_store && a.out.ttab == nullptr && out_blk_ok && a.out.s0 == 1 &&
                     ((uintptr_t)a.out.base & 15) == 0 &&
                     (a.out.tstride * (long long)ces) % 16 == 0 && (a.L1 == 1 || (a.out.s1 * (long long)ces) % 16 == 0) &&
-                    encode(&tout, a.out.base, a.out.tstride, a.out.s1);
+                    (a.out.bw > 0 ? encode4(&tout, a.out) : encode(&tout, a.out.base, a.out.tstride, a.out.s1));
       if (!use_st) tout = tin;  // unused by the non-TST variant
       a.tw = s.tw_tma;
       void* targs[] = {&tin, &tout, &a};
@@ -1865,7 +1968,8 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       memcpy(rp.out_n, d3n, sizeof d3n);
       rp.in_bytes = d1b;
       rp.out_bytes = d3b;
-      ST(P == 1 ? build_single(pl, g, rp) : pl->bc ? build_forward_bc(pl, g, rp) : build_forward(pl, g, rp));
+      ST(P == 1 ? (single_blocked_ok(pl, g) ? build_single_blocked(pl, g, rp) : build_single(pl, g, rp))
+                : pl->bc ? build_forward_bc(pl, g, rp) : build_forward(pl, g, rp));
     } else {
       memcpy(rp.in_lo, d3lo, sizeof d3lo);
       memcpy(rp.in_n, d3n, sizeof d3n);
@@ -1873,7 +1977,8 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       memcpy(rp.out_n, d1n, sizeof d1n);
       rp.in_bytes = d3b;
       rp.out_bytes = d1b;
-      ST(P == 1 ? build_single(pl, g, rp) : pl->bc ? build_inverse_bc(pl, g, rp) : build_inverse(pl, g, rp));
+      ST(P == 1 ? (single_blocked_ok(pl, g) ? build_single_blocked(pl, g, rp) : build_single(pl, g, rp))
+                : pl->bc ? build_inverse_bc(pl, g, rp) : build_inverse(pl, g, rp));
     }
     ST(apply_sm_caps(pl, rp));
     if (rp.ws_bytes) {

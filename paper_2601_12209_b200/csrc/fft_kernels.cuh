@@ -690,6 +690,16 @@ __device__ __forceinline__ void tma_store_3d(const void* tmap, int c0, int c1, i
                "r"(c1), "r"(c2), "r"(smem_u32(src))
                : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const void* tmap, int c0, int c1, int c2, int c3, const void* src) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tmap),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+               : "memory");
+}
+// a tile's box on the store side: 3D, or 4D into a column-blocked output (as tma_load_tile)
+__device__ __forceinline__ void tma_store_tile(const void* tmap, int bw, int c0, int row, int l1, const void* src) {
+  if (bw > 0) tma_store_4d(tmap, c0 % (2 * bw), row, l1, c0 / (2 * bw), src);
+  else tma_store_3d(tmap, c0, row, l1, src);
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -846,7 +856,7 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
         if constexpr (OM == 1) {
           const int c0 = (int)(tx * Cfg::W * 2);
           for (int q = 0; q < Cfg::NBOX; ++q)
-            tma_store_3d(&omap, c0, q * Cfg::BOXR, (int)l1, work + q * Cfg::BOXR * Cfg::W);
+            tma_store_tile(&omap, a.out.bw, c0, q * Cfg::BOXR, (int)l1, work + q * Cfg::BOXR * Cfg::W);
         } else {
           const long long e1 = tx * a.out.mT + l1;  // block tx (bw == W), line l1
           for (int q = 0; q < a.out.nbulk; ++q) {
