@@ -147,6 +147,7 @@ CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP
 bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
 bool g_use_tma2 = getenv("DFFT_TMA2") != nullptr;  // two-group variant: correct, not faster
 bool g_use_bulk = getenv("DFFT_NO_BULK") == nullptr;  // bulk-copy epilogue for blocked segmented outputs
+bool g_tst_work = getenv("DFFT_TST_WORK") != nullptr;  // TMA-store kernels: r01 work-buffer flow (A/B)
 
 // R2C/C2R split twiddles: w^k = exp(dir·2πi·k/(2N)), k ∈ [0, N), long double once each.
 dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void** out) {
@@ -181,11 +182,18 @@ inline bool is_contig(int family) { return family != kStrided; }
 dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
   bool ok = f64 ? lookup_kernel_f64(family, n, dir, k) : lookup_kernel_f32(family, n, dir, k);
   if (!ok) return fail(DFFT_ERR_UNSUPPORTED, "axis length %d not instantiated", n);
-  if (k->smem > 48 * 1024) CU(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->smem));
+  if (k->smem > 48 * 1024) {
+    CU(cudaFuncSetAttribute(k->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->smem));
+    if (k->fn_tb) CU(cudaFuncSetAttribute(k->fn_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->smem));
+    if (k->spec_fn) CU(cudaFuncSetAttribute(k->spec_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->smem));
+  }
   if (k->tma_fn && k->tma_smem > 48 * 1024) {
     CU(cudaFuncSetAttribute(k->tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     CU(cudaFuncSetAttribute(k->tma_st_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     CU(cudaFuncSetAttribute(k->tma_bk_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
+    CU(cudaFuncSetAttribute(k->tma_st1_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
+    if (k->tma_st_spec_fn)
+      CU(cudaFuncSetAttribute(k->tma_st_spec_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
   }
   if (k->tma2_fn && k->tma2_smem > 48 * 1024) {
     CU(cudaFuncSetAttribute(k->tma2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma2_smem));
@@ -1280,20 +1288,30 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
                     (a.out.tstride * (long long)ces) % 16 == 0 && (a.L1 == 1 || (a.out.s1 * (long long)ces) % 16 == 0) &&
                     (a.out.bw > 0 ? encode4(&tout, a.out) : encode(&tout, a.out.base, a.out.tstride, a.out.s1));
       if (!use_st) tout = tin;  // unused by the non-TST variant
+      const bool spec = a.spec[0] != nullptr;
       a.tw = s.tw_tma;
       void* targs[] = {&tin, &tout, &a};
       const long long grid = s.sm_cap > 0 ? std::min<long long>(s.tma_grid, (long long)s.sm_cap * s.tma_occ) : s.tma_grid;
-      if (s.tma_variant == 2)
+      if (spec && !(use_st && s.tma_variant == 1 && s.k.tma_st_spec_fn)) goto plain;  // multiplier: TST or plain
+      if (spec)
+        CU(cudaLaunchKernel(s.k.tma_st_spec_fn, dim3((unsigned)grid), dim3(s.k.tma_threads), targs, s.k.tma_smem, st));
+      else if (s.tma_variant == 2)
         CU(cudaLaunchKernel(use_st ? s.k.tma2_st_fn : s.k.tma2_fn, dim3((unsigned)grid), dim3(s.k.tma2_threads),
                             targs, s.k.tma2_smem, st));
       else
-        CU(cudaLaunchKernel(a.out.nbulk > 0 ? s.k.tma_bk_fn : use_st ? s.k.tma_st_fn : s.k.tma_fn, dim3((unsigned)grid),
+        CU(cudaLaunchKernel(a.out.nbulk > 0 ? s.k.tma_bk_fn
+                            : use_st        ? (g_tst_work ? s.k.tma_st1_fn : s.k.tma_st_fn)
+                                            : s.k.tma_fn,
+                            dim3((unsigned)grid),
                             dim3(s.k.tma_threads), targs, s.k.tma_smem, st));
       return DFFT_SUCCESS;
     }
   }
+plain:
   void* args[] = {&a};
-  CU(cudaLaunchKernel(s.k.fn, dim3((unsigned)s.grid), dim3(s.k.threads), args, s.k.smem, st));
+  const void* fn = a.in.tb > 0 ? s.k.fn_tb : a.spec[0] != nullptr ? s.k.spec_fn : s.k.fn;
+  if (!fn) return fail(DFFT_ERR_INTERNAL, "kernel variant not instantiated (n=%d)", s.n);
+  CU(cudaLaunchKernel(fn, dim3((unsigned)s.grid), dim3(s.k.threads), args, s.k.smem, st));
   return DFFT_SUCCESS;
 }
 

@@ -415,8 +415,9 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
   }
   // every read of this pass is done before anything is overwritten (also makes a single-pass
   // transform safe in place)
-  if constexpr (P > 0 || LAST || IO::kSyncAfterLoad) io.bar();
-  if constexpr (P == 0 && IO::kSyncAfterLoad) io.after_load();  // e.g. refill the drained TMA stage
+  // (IO::kLastBar = false: the last pass's outputs go to a buffer no thread is reading)
+  if constexpr ((P > 0 && (!LAST || IO::kLastBar)) || (P == 0 && LAST) || IO::kSyncAfterLoad) io.bar();
+  if constexpr (P == 0 && (IO::kSyncAfterLoad || IO::kRefillNoSync)) io.after_load();  // e.g. refill a TMA stage
   // ---- twiddle, butterfly, scatter
 #pragma unroll
   for (int u = 0; u < NB; ++u) {
@@ -449,8 +450,12 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
 // ------------------------------------------------------------------ contiguous-axis family
 // Global side of a pass for one line (l0, l1): loads of the first pass, stores of the last.
 // UNIT_T: unsegmented sides have t-stride 1 (the contig family; the host guarantees it).
-template <typename C, bool UNIT_T = false> struct GIO {
+// SPEC / TB are compile-time features (runtime branches on them cost 8-30 % in the r01
+// same-box A/B: the stores / loads of every other plan paid for them)
+template <typename C, bool UNIT_T = false, bool SPEC = false, bool TB = false> struct GIO {
   static constexpr bool kSyncAfterLoad = false;
+  static constexpr bool kRefillNoSync = false;
+  static constexpr bool kLastBar = true;
   __device__ __forceinline__ void after_load() {}
   __device__ __forceinline__ void bar() const { __syncthreads(); }  // barrier among the threads of a tile
   const C* __restrict__ in;
@@ -464,12 +469,12 @@ template <typename C, bool UNIT_T = false> struct GIO {
   const R* spt = nullptr;  // spectral multiplier (PassArgs::spec): λ table along t, and λ0[l0] + λ1[l1]
   R lam01 = 0;
   __device__ __forceinline__ void spectral(const PassArgs& a, long long l0_, long long l1_) {
-    if (a.spec[0] == nullptr) return;
+    if (!SPEC || a.spec[0] == nullptr) return;
     spt = reinterpret_cast<const R*>(a.spec[0]);
     lam01 = __ldg(reinterpret_cast<const R*>(a.spec[1]) + l0_) + __ldg(reinterpret_cast<const R*>(a.spec[2]) + l1_);
   }
   __device__ __forceinline__ C apply_spec(int t, C v) const {
-    if (spt != nullptr) {
+    if constexpr (SPEC) {
       const R lam = __ldg(spt + t) + lam01;
       const R g = lam != R(0) ? R(1) / lam : R(0);
       v.x *= g;
@@ -490,7 +495,7 @@ template <typename C, bool UNIT_T = false> struct GIO {
   }
   __device__ __forceinline__ C load(int t) const {
     if (mi->ttab == nullptr) {
-      if (mi->tb > 0) return in[lin + (long long)(t / mi->tb) * mi->tbs + t % mi->tb];
+      if constexpr (TB) return in[lin + (long long)(t / mi->tb) * mi->tbs + t % mi->tb];
       return UNIT_T ? in[lin + t] : in[(long long)t * mi->tstride + lin];
     }
     return *seg_ptr<const C>(*mi, t, i0, i1);
@@ -543,7 +548,7 @@ template <typename C, int N> struct C2RIO : GIO<C, true> {
   }
 };
 
-template <typename Real, int N, int DIR, int MODE>
+template <typename Real, int N, int DIR, int MODE, bool TB = false>
 __global__ void __launch_bounds__(ContigCfg<N>::THREADS)
 fft_contig_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
@@ -559,7 +564,7 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
   ContigSM sm{li * Cfg::LS};
   const C* tw = reinterpret_cast<const C*>(a.tw);
   if constexpr (MODE == 0) {
-    GIO<C, true> io;
+    GIO<C, true, false, TB> io;
     io.init(a.in, a.out, l0, l1, a.scale);
     stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
   } else if constexpr (MODE == 1) {
@@ -615,7 +620,7 @@ template <int W, int R0, int PAD> struct StridedSM {
   __device__ __forceinline__ int operator()(int t) const { return t * W + c + (t / R0) * PAD; }
 };
 
-template <typename Real, int N, int DIR>
+template <typename Real, int N, int DIR, bool SPEC = false>
 __global__ void __launch_bounds__(StridedCfg<Real, N>::THREADS)
 fft_strided_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
@@ -628,7 +633,7 @@ fft_strided_kernel(const __grid_constant__ PassArgs a) {
   const long long l1 = blockIdx.x / ntile;
   const long long l0 = (blockIdx.x - l1 * ntile) * Cfg::W + c;
   const bool active = l0 < a.L0;
-  GIO<C> io;
+  GIO<C, false, SPEC> io;
   io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
   io.spectral(a, active ? l0 : 0, l1);
   StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
@@ -739,8 +744,14 @@ template <typename Real, int N> struct TmaCfg {
   static constexpr bool OK = S.npass >= 2 && THREADS <= 1024 && SMEM <= 227 * 1024 && 2 * W <= 256;
 };
 
-template <typename C, int W, int OM> struct TmaIO : GIO<C> {
-  static constexpr bool kSyncAfterLoad = true;
+// OM 3 (TMA stores, stage as output): the last pass writes the tile back into its own stage
+// buffer (drained by pass 0), the TMA store reads it from there, and thread 0 refills the
+// previous tile's stage right after its own pass-0 loads — two CTA barriers per tile instead
+// of four (ncu r01: barrier stalls were the top stall reason at 8 warps/SM).
+template <typename C, int W, int OM, bool SPEC = false> struct TmaIO : GIO<C, false, SPEC> {
+  static constexpr bool kSyncAfterLoad = OM != 3;
+  static constexpr bool kRefillNoSync = OM == 3;
+  static constexpr bool kLastBar = OM != 3;
   const C* stage;  // this tile's stage buffer, dense [t][W]
   C* obuf;         // OM > 0: dense [t][W] output tile, written by a TMA tensor store (1) or bulk copies (2)
   int c;
@@ -757,11 +768,12 @@ template <typename C, int W, int OM> struct TmaIO : GIO<C> {
       if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
       obuf[t * W + c] = this->apply_spec(t, v);
     } else {
-      GIO<C>::store(t, v);
+      GIO<C, false, SPEC>::store(t, v);
     }
   }
   __device__ __forceinline__ void after_load() {
     if (refill && threadIdx.x == 0) {
+      if constexpr (OM == 3) bulk_wait_read0();  // the previous tile's store has read that stage
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(mbar, bytes);
       for (int q = 0; q < nbox; ++q)
@@ -781,11 +793,12 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
 // stores at a large stride from the SMs throttles the LSU (r01 ncu: lg_throttle); 2 = the
 // output is segmented into column-blocked windows (possibly peers' over NVLink) and each
 // segment of a tile leaves as one contiguous cp.async.bulk copy.
-template <typename Real, int N, int DIR, int OM>
+template <typename Real, int N, int DIR, int OM, bool SPEC = false>
 __global__ void __launch_bounds__(TmaCfg<Real, N>::THREADS)
 fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
                        const __grid_constant__ PassArgs a) {
   constexpr bool TST = OM != 0;
+  constexpr bool SOUT = OM == 3;  // stage-as-output flow
   using C = typename CT<Real>::type;
   using Cfg = TmaCfg<Real, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -824,18 +837,21 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     tile_coords(tile, ntile, a.L1, a.g0, tx, l1);
     const long long l0 = tx * Cfg::W + c;
     const bool active = l0 < a.L0;
-    if (TST && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
-    TmaIO<C, Cfg::W, OM> io;
+    if (TST && !SOUT && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
+    TmaIO<C, Cfg::W, OM, SPEC> io;
     io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
     io.spectral(a, active ? l0 : 0, l1);
-    io.obuf = work;
     io.stage = stages + s * Cfg::STAGE_ELEMS;
+    io.obuf = SOUT ? stages + s * Cfg::STAGE_ELEMS : work;
     io.c = c;
-    const long long next = tile + (long long)Cfg::NS * gridDim.x;
-    io.refill = next < total;
+    // refill: the drained stage gets the tile NS steps ahead (SOUT: the previous tile's stage,
+    // free once its store has read it, gets the next tile)
+    const int rs = SOUT ? (it + Cfg::NS - 1) % Cfg::NS : s;
+    const long long next = SOUT ? tile + gridDim.x : tile + (long long)Cfg::NS * gridDim.x;
+    io.refill = next < total && (!SOUT || it >= Cfg::NS - 1);
     io.tmap = &tmap;
-    io.mbar = &bars[s];
-    io.stage_ptr = stages + s * Cfg::STAGE_ELEMS;
+    io.mbar = &bars[rs];
+    io.stage_ptr = stages + rs * Cfg::STAGE_ELEMS;
     {
       long long ntx, nl1;
       tile_coords(next, ntile, a.L1, a.g0, ntx, nl1);
@@ -853,10 +869,11 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
       __syncthreads();
       if (threadIdx.x == 0) {
-        if constexpr (OM == 1) {
+        if constexpr (OM == 1 || OM == 3) {
           const int c0 = (int)(tx * Cfg::W * 2);
+          const C* src = SOUT ? stages + s * Cfg::STAGE_ELEMS : work;
           for (int q = 0; q < Cfg::NBOX; ++q)
-            tma_store_tile(&omap, a.out.bw, c0, q * Cfg::BOXR, (int)l1, work + q * Cfg::BOXR * Cfg::W);
+            tma_store_tile(&omap, a.out.bw, c0, q * Cfg::BOXR, (int)l1, src + q * Cfg::BOXR * Cfg::W);
         } else {
           const long long e1 = tx * a.out.mT + l1;  // block tx (bw == W), line l1
           for (int q = 0; q < a.out.nbulk; ++q) {

@@ -10,6 +10,7 @@ KernelInfo make_contig() {
   using Cfg = ContigCfg<N>;
   KernelInfo k;
   k.fn = (const void*)&fft_contig_kernel<Real, N, DIR, MODE>;
+  if constexpr (MODE == 0) k.fn_tb = (const void*)&fft_contig_kernel<Real, N, DIR, 0, true>;
   k.threads = Cfg::THREADS;
   k.per_cta = Cfg::LPC;
   k.smem = (Cfg::S.npass > 1 || MODE == 1) ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
@@ -21,6 +22,7 @@ KernelInfo make_strided() {
   using Cfg = StridedCfg<Real, N>;
   KernelInfo k;
   k.fn = (const void*)&fft_strided_kernel<Real, N, DIR>;
+  if constexpr (DIR < 0) k.spec_fn = (const void*)&fft_strided_kernel<Real, N, DIR, true>;
   k.threads = Cfg::THREADS;
   k.per_cta = Cfg::W;
   k.smem = Cfg::S.npass > 1 ? (size_t)Cfg::SMEM_ELEMS * sizeof(Real) * 2 : 0;
@@ -28,8 +30,10 @@ KernelInfo make_strided() {
   using TC = TmaCfg<Real, N>;
   if constexpr (TC::OK) {
     k.tma_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 0>;
-    k.tma_st_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1>;
+    k.tma_st_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 3>;   // stage-as-output flow
+    k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1>;  // work-buffer flow (A/B)
     k.tma_bk_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 2>;
+    if constexpr (DIR < 0) k.tma_st_spec_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 3, true>;
     k.tma_threads = TC::THREADS;
     k.tma_w = TC::W;
     k.tma_boxr = TC::BOXR;

@@ -12,6 +12,8 @@ enum Family { kContig = 0, kStrided = 1, kContigR2C = 2, kContigC2R = 3 };
 
 struct KernelInfo {
   const void* fn = nullptr;
+  const void* fn_tb = nullptr;    // contig c2c: t-blocked input side (SideMap::tb)
+  const void* spec_fn = nullptr;  // strided forward: with the Poisson multiplier (PassArgs::spec)
   int threads = 0;       // CTA size
   int per_cta = 0;       // contig: lines per CTA; strided: columns per CTA (W)
   size_t smem = 0;       // dynamic shared memory bytes
@@ -19,7 +21,9 @@ struct KernelInfo {
   // strided family only: persistent TMA-staged variant (null if not instantiable for n)
   const void* tma_fn = nullptr;
   const void* tma_st_fn = nullptr;  // same, with TMA stores (unsegmented output side)
+  const void* tma_st1_fn = nullptr;  // same, the r01 work-buffer flow (DFFT_TST_WORK=1)
   const void* tma_bk_fn = nullptr;  // same, with bulk-copy stores (column-blocked segmented output)
+  const void* tma_st_spec_fn = nullptr;  // TMA stores + Poisson multiplier (forward only)
   // two-warp-group variant (preferred when it fits): in-place padded stage buffers
   const void* tma2_fn = nullptr;
   const void* tma2_st_fn = nullptr;
