@@ -54,6 +54,7 @@ def _load():
         lib.or_poisson_eigen.argtypes = [_i64, _d, _dp]
         lib.or_poisson3d.argtypes = [_dp, _i64, _i64, _i64, _d, _d, _d, _dp]
         lib.or_laplacian7.argtypes = [_dp, _i64, _i64, _i64, _d, _d, _d, _dp]
+        lib.or_dct3d.argtypes = [_dp, _i64, _i64, _i64, _int]
         lib.or_dft3d_bin_seeded.argtypes = [_u64, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64, _dp]
         lib.or_err_sums.argtypes = [_dp, _dp, _i64, _dp]
         lib.or_num_threads.restype = _int
@@ -147,6 +148,14 @@ def irfft3d(half: np.ndarray, nx: int) -> np.ndarray:
     assert nxc == nx // 2 + 1 and nx % 2 == 0
     out = np.empty((nz, ny, nx), dtype=np.float64)
     _load().or_irfft3d(_p(half.view(np.float64)), nx, ny, nz, _p(out))
+    return out
+
+
+def dct3d(a: np.ndarray, inverse: bool = False) -> np.ndarray:
+    """R2R (reading R21): DCT-II along every axis (FFTW REDFT10), or DCT-III / (2N) per axis."""
+    out = np.array(a, dtype=np.float64, order="C", copy=True)
+    nz, ny, nx = out.shape
+    _load().or_dct3d(_p(out), nx, ny, nz, int(bool(inverse)))
     return out
 
 

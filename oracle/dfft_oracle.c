@@ -375,6 +375,64 @@ void or_irfft3d(const double* half, int64_t nx, int64_t ny, int64_t nz, double* 
     free(a);
 }
 
+/* ------------------------------------------------------------------ real-to-real (DCT) */
+
+/*
+ * R2R transforms (P:403 lists C2C, R2C and R2R; the algorithm is unstated — reading R21):
+ * the forward R2R is the DCT-II along every axis (FFTW REDFT10, the transform of a Bounded /
+ * Neumann direction):  X_k = 2 Σ_{n<N} x_n cos(π k (2n+1) / (2N)),  k < N;
+ * the inverse is the DCT-III along every axis divided by 2N (so inverse(forward(x)) = x):
+ *   x_n = (X_0 + 2 Σ_{0<k<N} X_k cos(π k (2n+1) / (2N))) / (2N).
+ * Written as the definitions (O(N) per output, cosines in long double), one axis at a time
+ * (the 3D transform is separable exactly like the DFT).
+ */
+static void or_dct_line(const double* x, int64_t xs, int64_t n, int inverse, double* y, int64_t ys,
+                        const double* c /* cos(π m / (2n)), m < 4n */) {
+    for (int64_t a = 0; a < n; ++a) {
+        long double acc = 0.0L;
+        if (!inverse) {
+            for (int64_t b = 0; b < n; ++b) acc += (long double)x[b * xs] * c[(a * (2 * b + 1)) % (4 * n)];
+            y[a * ys] = (double)(2.0L * acc);
+        } else {
+            acc = (long double)x[0];
+            for (int64_t b = 1; b < n; ++b) acc += 2.0L * (long double)x[b * xs] * c[(b * (2 * a + 1)) % (4 * n)];
+            y[a * ys] = (double)(acc / (long double)(2 * n));
+        }
+    }
+}
+
+static void or_dct_axis(double* a, int64_t nx, int64_t ny, int64_t nz, int axis, int inverse) {
+    int64_t n = axis == 0 ? nx : axis == 1 ? ny : nz;
+    int64_t stride = axis == 0 ? 1 : axis == 1 ? nx : nx * ny;
+    int64_t lines = nx * ny * nz / n;
+    double* c = (double*)malloc(sizeof(double) * 4 * (size_t)n);
+    for (int64_t m = 0; m < 4 * n; ++m)
+        c[m] = (double)cosl(3.14159265358979323846264338327950288L * (long double)m / (long double)(2 * n));
+#pragma omp parallel
+    {
+        double* in = (double*)malloc(sizeof(double) * (size_t)n);
+        double* out = (double*)malloc(sizeof(double) * (size_t)n);
+#pragma omp for schedule(static)
+        for (int64_t l = 0; l < lines; ++l) {
+            int64_t base;
+            if (axis == 0) base = l * nx;
+            else if (axis == 1) base = (l % nx) + (l / nx) * nx * ny;
+            else base = l;
+            for (int64_t t = 0; t < n; ++t) in[t] = a[base + t * stride];
+            or_dct_line(in, 1, n, inverse, out, 1, c);
+            for (int64_t t = 0; t < n; ++t) a[base + t * stride] = out[t];
+        }
+        free(in);
+        free(out);
+    }
+    free(c);
+}
+
+/* 3D DCT-II (forward) / DCT-III / (2N) (inverse), in place on a real (nx, ny, nz) array. */
+void or_dct3d(double* a, int64_t nx, int64_t ny, int64_t nz, int inverse) {
+    for (int axis = 0; axis < 3; ++axis) or_dct_axis(a, nx, ny, nz, inverse ? 2 - axis : axis, inverse);
+}
+
 /* ------------------------------------------------------------------ periodic Poisson solve */
 
 /*

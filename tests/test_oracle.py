@@ -259,3 +259,34 @@ def test_poisson_single_mode_closed_form(oracle_mod):
     assert np.abs(phi - f / lam).max() < 1e-13
     lx = oracle_mod.poisson_eigen(nx, 0.5)
     assert lx[0] == 0.0 and abs(lx[nx // 2] + 16.0) < 1e-13  # -(2/h)^2 at the Nyquist mode
+
+
+# ------------------------------------------------------------------ R2R: DCT-II / DCT-III (f4)
+@pytest.mark.parametrize("shape", [(8, 6, 4), (16, 12, 10), (32, 8, 24)])
+def test_dct3d_vs_scipy(oracle_mod, shape):
+    # P:403 (R2R), reading R21: DCT-II per axis = scipy.fft.dctn(type=2) (pocketfft, an
+    # independent library), inverse = DCT-III/(2N) per axis = scipy.fft.idctn(type=2)
+    import scipy.fft as sf
+    a = oracle_mod.gen_real(41, shape)
+    X = oracle_mod.dct3d(a)
+    assert np.allclose(X, sf.dctn(a, type=2), rtol=0, atol=1e-12 * np.abs(X).max())
+    assert np.allclose(oracle_mod.dct3d(X, inverse=True), a, rtol=0, atol=1e-13)
+    assert np.allclose(oracle_mod.dct3d(X, inverse=True), sf.idctn(X, type=2), rtol=0, atol=1e-13)
+
+
+def test_dct3d_closed_forms(oracle_mod):
+    # cos(π m (2n+1) / (2N)) along each axis is a DCT-II basis vector: X = 8·Nx·Ny·Nz/8 at (mx,my,mz)
+    # for m > 0 (orthogonality, textbook); a constant c gives 8·N·c at DC only
+    nx, ny, nz = 12, 8, 6
+    m = (5, 3, 1)
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    f = (np.cos(np.pi * m[0] * (2 * x + 1) / (2 * nx)) * np.cos(np.pi * m[1] * (2 * y + 1) / (2 * ny))
+         * np.cos(np.pi * m[2] * (2 * z + 1) / (2 * nz)))
+    X = oracle_mod.dct3d(f)
+    ref = np.zeros_like(X)
+    ref[m[2], m[1], m[0]] = nx * ny * nz
+    assert np.abs(X - ref).max() < 1e-11
+    C = oracle_mod.dct3d(np.full((nz, ny, nx), 0.5))
+    ref = np.zeros_like(C)
+    ref[0, 0, 0] = 8 * nx * ny * nz * 0.5
+    assert np.abs(C - ref).max() < 1e-11
