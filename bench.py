@@ -43,7 +43,8 @@ def parse():
     p.add_argument("--precision", default="f32", choices=["f32", "f64"])
     p.add_argument("--strategy", default="pencil", choices=["pencil", "slab"])
     p.add_argument("--grid-p", default="", help="process grid P1,P2 (default by N)")
-    p.add_argument("--kind", default="c2c", choices=["c2c", "r2c"], help="r2c: real input, R2C forward + C2R inverse")
+    p.add_argument("--kind", default="c2c", choices=["c2c", "r2c", "r2r"],
+                   help="r2c: real input, R2C forward + C2R inverse; r2r: DCT-II forward + DCT-III inverse per axis")
     p.add_argument("--poisson", action="store_true",
                    help="periodic Poisson solve: R2C/C2C forward with the fused 1/λ(k) multiplier, then the inverse "
                         "(SURVEY §8(f) f3, P:606-620)")
@@ -62,7 +63,7 @@ def parse():
 def flops_fwd_inv(shape, kind="c2c"):
     """5·N·log2N per c2c transform; R2C/C2R with the real-data convention 2.5·N·log2N (reading Z9)."""
     N = shape[0] * shape[1] * shape[2]
-    return 2 * (2.5 if kind == "r2c" else 5.0) * N * math.log2(N)
+    return 2 * (2.5 if kind in ("r2c", "r2r") else 5.0) * N * math.log2(N)
 
 
 def load_peaks():
@@ -308,8 +309,8 @@ def main():
     P = grid[0] * grid[1]
     Nloc = shape[0] * shape[1] * shape[2] / P
     # complex elements per rank after stage 1 (R2C: nx/2+1 bins along x) and stage-1 bytes
-    Ncl = Nloc * ((shape[0] // 2 + 1) / shape[0] if args.kind == "r2c" else 1.0)
-    a_bytes = (Nloc * es / 2 if args.kind == "r2c" else Nloc * es) + Ncl * es
+    Ncl = Nloc * ((shape[0] // 2 + 1) / shape[0] if args.kind == "r2c" else 0.5 if args.kind == "r2r" else 1.0)
+    a_bytes = (Nloc * es / 2 if args.kind in ("r2c", "r2r") else Nloc * es) + Ncl * es
     t_hbm = 2 * (a_bytes + 4 * Ncl * es) / (hbm_peak * 1e9)
     p1, p2 = (1, P) if args.strategy == "slab" else grid
     nvl_bytes = Ncl * es * ((p1 - 1) / p1 + (p2 - 1) / p2)
@@ -362,10 +363,10 @@ def main():
             "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": {"workload": f"{shape[0]}x{shape[1]}x{shape[2]} "
                                    + (f"complex{'64' if es == 8 else '128'} c2c" if args.kind == "c2c" else
-                                      f"{'f32' if es == 8 else 'f64'} r2c")
+                                      f"{'f32' if es == 8 else 'f64'} {args.kind}")
                                    + f" {args.strategy} {grid[0]}x{grid[1]} "
                                    + ("Poisson solve (fwd + 1/λ fused + inv)" if args.poisson else "fwd+inv"),
-                       "flop_convention": "2.5·N·log2N per R2C/C2R" if args.kind == "r2c" else "5·N·log2N per c2c",
+                       "flop_convention": "2.5·N·log2N per real transform" if args.kind != "c2c" else "5·N·log2N per c2c",
                        "grid": list(shape), "proc_grid": list(grid), "chunks": fwd.chunks(),
                        "exchange": args.exchange if world > 1 else "none",
                        "overlap": not args.no_overlap,

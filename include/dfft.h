@@ -55,8 +55,15 @@ typedef enum {
 
 typedef enum { DFFT_SLAB = 1, DFFT_PENCIL = 2 } dfft_decomp_t;
 
-/* Transform type and precision.  R2C with direction INVERSE is the C2R transform. */
-typedef enum { DFFT_C2C_F32 = 1, DFFT_C2C_F64 = 2, DFFT_R2C_F32 = 3, DFFT_R2C_F64 = 4 } dfft_type_t;
+/* Transform type and precision.  R2C with direction INVERSE is the C2R transform.
+ * R2R (reading R21 in DESIGN.md): FORWARD = the DCT-II along every axis (FFTW REDFT10,
+ * X_k = 2 Σ x_n cos(πk(2n+1)/(2N))), INVERSE = the DCT-III along every axis divided by 2N per
+ * axis, so INVERSE(FORWARD(x)) = x.  Both boxes are real (float/double), x-fastest; every extent
+ * must be even and nx/2, ny, nz supported lengths; the x split of the D2/D3 layouts is in pairs
+ * of reals.  dfft_plan_set_poisson does not apply (UNSUPPORTED). */
+typedef enum {
+  DFFT_C2C_F32 = 1, DFFT_C2C_F64 = 2, DFFT_R2C_F32 = 3, DFFT_R2C_F64 = 4, DFFT_R2R_F32 = 5, DFFT_R2R_F64 = 6
+} dfft_type_t;
 
 /* Sign of the exponent: FORWARD = -1, INVERSE = +1 with the 1/N scale. */
 typedef enum { DFFT_FORWARD = -1, DFFT_INVERSE = 1 } dfft_direction_t;

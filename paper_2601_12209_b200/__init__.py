@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("DFFT_LIB", os.path.join(PKG, "libdfft.so"))  # DFFT_L
 
 FORWARD, INVERSE = -1, 1
 SLAB, PENCIL = 1, 2
-TYPES = {"c2c_f32": 1, "c2c_f64": 2, "r2c_f32": 3, "r2c_f64": 4}
+TYPES = {"c2c_f32": 1, "c2c_f64": 2, "r2c_f32": 3, "r2c_f64": 4, "r2r_f32": 5, "r2r_f64": 6}
 FLAG_NO_OVERLAP = 1 << 8
 FLAG_NCCL = 1 << 9
 FLAG_FUSED_STORE = 1 << 10
@@ -167,7 +167,8 @@ class Comm:
 
 # ---------------------------------------------------------------------------------- plan
 class Plan:
-    """A distributed 3D FFT plan (dfft_plan_create).  dtype: c2c_f32 | c2c_f64 | r2c_f32 | r2c_f64."""
+    """A distributed 3D FFT plan (dfft_plan_create).  dtype: c2c_f32 | c2c_f64 | r2c_f32 | r2c_f64 |
+    r2r_f32 | r2r_f64 (DCT-II forward / DCT-III/(2N) inverse per axis, real boxes)."""
 
     def __init__(self, comm: Comm, shape: Sequence[int], decomp: str = "pencil", grid: Sequence[int] = (1, 1),
                  dtype: str = "c2c_f32", direction: int = FORWARD, chunks: int = 0, overlap: bool = True,
@@ -205,7 +206,7 @@ class Plan:
         import torch
 
         f64 = self.dtype.endswith("f64")
-        real = self.dtype.startswith("r2c") and ((which == 0) == (self.direction == FORWARD))
+        real = self.dtype.startswith("r2r") or (self.dtype.startswith("r2c") and ((which == 0) == (self.direction == FORWARD)))
         if real:
             return torch.float64 if f64 else torch.float32
         return torch.complex128 if f64 else torch.complex64

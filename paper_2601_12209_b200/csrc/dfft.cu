@@ -147,7 +147,9 @@ CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP
 bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
 bool g_use_tma2 = getenv("DFFT_TMA2") != nullptr;  // two-group variant: correct, not faster
 bool g_use_bulk = getenv("DFFT_NO_BULK") == nullptr;  // bulk-copy epilogue for blocked segmented outputs
-bool g_tst_work = getenv("DFFT_TST_WORK") != nullptr;  // TMA-store kernels: r01 work-buffer flow (A/B)
+// TMA-store kernels: the work-buffer flow (OM 1) is the default; the stage-as-output flow (OM 3,
+// two barriers per tile but a one-tile prefetch distance) measured 3-10 % slower
+bool g_tst_work = getenv("DFFT_TST_STAGEOUT") == nullptr;
 
 // R2C/C2R split twiddles: w^k = exp(dir·2πi·k/(2N)), k ∈ [0, N), long double once each.
 dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void** out) {
@@ -177,7 +179,40 @@ dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void**
   return DFFT_SUCCESS;
 }
 
-inline bool is_contig(int family) { return family != kStrided; }
+inline bool is_contig(int family) { return family != kStrided && family != kStridedDct; }
+
+// R2R (DCT) post/pre twiddles: c_k = exp(dir·iπk/(2L)), k ∈ [0, L), long double once each.
+dfft_status_t get_dct_twiddles(int L, bool f64, int dir, int dev, const void** out) {
+  static std::map<TwKey, void*> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  TwKey key{L, f64, dir, dev, -2};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return DFFT_SUCCESS;
+  }
+  const size_t es = f64 ? 16 : 8;
+  std::vector<unsigned char> h((size_t)L * es);
+  for (int k = 0; k < L; ++k) {
+    const long double a = (long double)dir * 3.14159265358979323846264338327950288L * (long double)k / (2.0L * L);
+    const long double c = cosl(a), sn = sinl(a);
+    if (f64) {
+      reinterpret_cast<double*>(h.data())[2 * k] = (double)c;
+      reinterpret_cast<double*>(h.data())[2 * k + 1] = (double)sn;
+    } else {
+      reinterpret_cast<float*>(h.data())[2 * k] = (float)c;
+      reinterpret_cast<float*>(h.data())[2 * k + 1] = (float)sn;
+    }
+  }
+  void* d = nullptr;
+  CU(cudaSetDevice(dev));
+  CU(cudaMalloc(&d, h.size()));
+  CU(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
+  cache[key] = d;
+  *out = d;
+  return DFFT_SUCCESS;
+}
 
 dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
   bool ok = f64 ? lookup_kernel_f64(family, n, dir, k) : lookup_kernel_f32(family, n, dir, k);
@@ -287,6 +322,7 @@ struct dfft_plan_s {
   int64_t nx = 0, ny = 0, nz = 0;
   int P1 = 1, P2 = 1, K = 1, dir = -1;
   bool f64 = false, r2c = false, overlap = true;
+  bool r2r = false;  // DCT-II forward / DCT-III inverse along every axis (reading R21)
   size_t es = 8;  // complex element bytes
   std::vector<RankPlan> ranks;
   ncclComm_t row = nullptr, col = nullptr;
@@ -319,6 +355,12 @@ struct dfft_plan_s {
 };
 
 namespace {
+
+// x lines are real (R2C/C2R, R2R): nx reals per line = nx/2 complex elements on the kernel side
+inline bool xreal(const dfft_plan_s* pl) { return pl->r2c || pl->r2r; }
+inline int fam_x_fwd(const dfft_plan_s* pl) { return pl->r2c ? kContigR2C : pl->r2r ? kContigDct : kContig; }
+inline int fam_x_inv(const dfft_plan_s* pl) { return pl->r2c ? kContigC2R : pl->r2r ? kContigDct : kContig; }
+inline int fam_s(const dfft_plan_s* pl) { return pl->r2r ? kStridedDct : kStrided; }
 
 // ------------------------------------------------------------------------------ stage builders
 dfft_status_t upload_table(const std::vector<longlong2>& h, void** d) {
@@ -409,7 +451,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   if (s.in_bases.size() > (size_t)kMaxBases || s.out_bases.size() > (size_t)kMaxBases)
     return fail(DFFT_ERR_UNSUPPORTED, "more than %d segment bases", kMaxBases);
   if (in_segs && linearize(*in_segs, n, s.in, s.in_bases, s.a.in, (long long)pl->es)) in_segs = nullptr;
-  if (in_segs && is_contig(family) && family != kContigC2R && !getenv("DFFT_NO_TBLOCK") &&
+  if (in_segs && family == kContig && !getenv("DFFT_NO_TBLOCK") &&
       linearize_tblocked(*in_segs, s.in, s.in_bases, s.a.in, (long long)pl->es))
     in_segs = nullptr;
   if (out_segs && linearize(*out_segs, n, s.out, s.out_bases, s.a.out, (long long)pl->es)) out_segs = nullptr;
@@ -431,8 +473,10 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   }
   ST(get_kernel(family, n, pl->f64, pl->dir, &s.k));
   ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw));
-  if (family == kContigR2C || family == kContigC2R)
+  if (family == kContigR2C || family == kContigC2R || family == kContigDct)
     ST(get_split_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw2));
+  if (family == kContigDct || family == kStridedDct)  // c_k over the real line length L
+    ST(get_dct_twiddles(family == kContigDct ? 2 * n : n, pl->f64, pl->dir, pl->comm->device, &s.a.tw3));
   if (in_tab) ST(upload_table(*in_tab, &s.in_tab));
   if (out_tab) ST(upload_table(*out_tab, &s.out_tab));
   s.a.in.ttab = (const SegEnt*)s.in_tab;
@@ -613,8 +657,8 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       if (q != j) acc += g.Y3n(q);
     return L.S2 + Xn * (g.z0(j, k) * (g.ny - Y3n) + g.zc(j, k) * acc);
   };
-  const long long nxl = pl->r2c ? g.nx / 2 : g.nx;  // input line length in (complex) elements
-  const long long in_es = pl->r2c ? es / 2 : es;
+  const long long nxl = xreal(pl) ? g.nx / 2 : g.nx;  // input line length in (complex) elements
+  const long long in_es = xreal(pl) ? es / 2 : es;
   rp.A.resize(K);
   rp.B.resize(K);
   rp.E1.resize(K);
@@ -644,7 +688,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       }
     }
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, pl->r2c ? kContigR2C : kContig, (int)nxl, Y1n, zc, nullptr, &aseg));
+    ST(finish_stage(pl, A, fam_x_fwd(pl), (int)nxl, Y1n, zc, nullptr, &aseg));
     // ---- exchange 1 (row group)
     Exchange& E1 = rp.E1[k];
     E1.comm = 0;
@@ -696,7 +740,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       B.a.out.mT = g.nz;
     }
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, kStrided, (int)g.ny, Xn, zc, nullptr, &bseg));
+    ST(finish_stage(pl, B, fam_s(pl), (int)g.ny, Xn, zc, nullptr, &bseg));
     // ---- exchange 2 (column group)
     Exchange& E2 = rp.E2[k];
     E2.comm = 1;
@@ -743,7 +787,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   C.last_fwd = true;  // t = z, l0 = x, l1 = y
   C.gax[0] = 2, C.gax[1] = 0, C.gax[2] = 1;
   C.glo[1] = g.Xlo(i), C.glo[2] = g.Y3lo(j);
-  ST(finish_stage(pl, C, kStrided, (int)g.nz, Xn, Y3n, nullptr, nullptr));
+  ST(finish_stage(pl, C, fam_s(pl), (int)g.nz, Xn, Y3n, nullptr, nullptr));
   return DFFT_SUCCESS;
 }
 
@@ -756,7 +800,7 @@ dfft_status_t build_forward_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
   const FwdLayout L = fwd_layout(g, i, j, 2);
   add_flags(pl, g, rp, L.end, true);
-  const long long nxl = pl->r2c ? g.nx / 2 : g.nx;
+  const long long nxl = xreal(pl) ? g.nx / 2 : g.nx;
   rp.A.resize(K);
   rp.B.resize(K);
   rp.E1.resize(K);
@@ -776,7 +820,7 @@ dfft_status_t build_forward_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     aseg.push_back({1 + (int)ip, g.Xlo(ip), xn, Lr.R1 + g.Y1lo(i) * xn, 1, xn, g.ny * xn});
   }
   A.a.scale = 1.0;
-  ST(finish_stage(pl, A, pl->r2c ? kContigR2C : kContig, (int)nxl, Y1n, Zn, nullptr, &aseg));
+  ST(finish_stage(pl, A, fam_x_fwd(pl), (int)nxl, Y1n, Zn, nullptr, &aseg));
   for (long long k = 1; k < K; ++k) rp.A[k].empty = true;
   rp.E1[0].comm = 0;
   rp.E1[0].fused = true;
@@ -801,7 +845,7 @@ dfft_status_t build_forward_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     B.a.out.bw = (int)g.wy;
     B.a.out.mT = g.nz;
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, kStrided, (int)g.ny, xc, Zn, nullptr, &bseg));
+    ST(finish_stage(pl, B, fam_s(pl), (int)g.ny, xc, Zn, nullptr, &bseg));
     Exchange& E2 = rp.E2[k];
     E2.comm = 1;
     E2.fused = true;
@@ -820,7 +864,7 @@ dfft_status_t build_forward_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.last_fwd = true;  // t = z, l0 = x - x0, l1 = y
     C.gax[0] = 2, C.gax[1] = 0, C.gax[2] = 1;
     C.glo[1] = g.Xlo(i) + x0, C.glo[2] = g.Y3lo(j);
-    ST(finish_stage(pl, C, kStrided, (int)g.nz, xc, Y3n, nullptr, nullptr));
+    ST(finish_stage(pl, C, fam_s(pl), (int)g.nz, xc, Y3n, nullptr, nullptr));
   }
   return DFFT_SUCCESS;
 }
@@ -833,7 +877,7 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long Xn = g.Xn(i), Y1n = g.Y1n(i), Zn = g.Zn(j), Y3n = g.Y3n(j);
   const InvLayout L = inv_layout(g, i, j, 2);
   add_flags(pl, g, rp, L.end, false);
-  const long long nxl = pl->r2c ? g.nx / 2 : g.nx;
+  const long long nxl = xreal(pl) ? g.nx / 2 : g.nx;
   rp.A.resize(K);
   rp.B.resize(K);
   rp.E1.resize(K);
@@ -855,7 +899,7 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   A.a.out.bw = (int)g.wz;
   A.a.out.mT = g.ny;
   A.a.scale = 1.0;
-  ST(finish_stage(pl, A, kStrided, (int)g.nz, Xn, Y3n, nullptr, &aseg));
+  ST(finish_stage(pl, A, fam_s(pl), (int)g.nz, Xn, Y3n, nullptr, &aseg));
   for (long long k = 1; k < K; ++k) rp.A[k].empty = true;
   rp.E1[0].comm = 1;
   rp.E1[0].fused = true;
@@ -884,7 +928,7 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     B.a.out.bw = (int)g.wy;
     B.a.out.mT = Zn;
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, kStrided, (int)g.ny, Xn, zc, nullptr, &bseg));
+    ST(finish_stage(pl, B, fam_s(pl), (int)g.ny, Xn, zc, nullptr, &bseg));
     Exchange& E2 = rp.E2[k];
     E2.comm = 0;
     E2.fused = true;
@@ -906,8 +950,8 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     }
     C.out = {kUserOut, z0 * Y1n * nxl * es};  // C2R: nxl = nx/2 complex = nx reals per line
     set_side(C.a.out, 1, nxl, Y1n * nxl);
-    C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)g.nx * (double)g.ny * (double)g.nz);
-    ST(finish_stage(pl, C, pl->r2c ? kContigC2R : kContig, (int)nxl, Y1n, zc, &cseg, nullptr));
+    C.a.scale = (xreal(pl) ? 2.0 : 1.0) / ((double)g.nx * (double)g.ny * (double)g.nz);
+    ST(finish_stage(pl, C, fam_x_inv(pl), (int)nxl, Y1n, zc, &cseg, nullptr));
   }
   return DFFT_SUCCESS;
 }
@@ -937,12 +981,13 @@ bool single_blocked_ok(dfft_plan_t pl, const Geo& g) {
   const long long w = ky.tma_w;
   // the inverse c2c uses `out` as the L2 scratch: no padding room there
   if (pl->dir == DFFT_INVERSE && !pl->r2c && g.nxc % w != 0) return false;
+  if (pl->r2r) return false;
   return g.ny * (long long)pl->es % 16 == 0 && g.nxc * (long long)pl->es % 16 == 0;
 }
 
 dfft_status_t build_single_blocked(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
-  const long long nxl = pl->r2c ? nx / 2 : nx;
+  const long long nxl = xreal(pl) ? nx / 2 : nx;
   KernelInfo ky;
   if (!(pl->f64 ? lookup_kernel_f64(kStrided, (int)ny, pl->dir, &ky) : lookup_kernel_f32(kStrided, (int)ny, pl->dir, &ky)))
     return fail(DFFT_ERR_INTERNAL, "no strided kernel for ny");
@@ -973,13 +1018,13 @@ dfft_status_t build_single_blocked(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     A.out = {kUserOut, 0};
     set_l1_lines(A.a.out);
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, pl->r2c ? kContigR2C : kContig, (int)nxl, ny, nz, nullptr, nullptr));
+    ST(finish_stage(pl, A, fam_x_fwd(pl), (int)nxl, ny, nz, nullptr, nullptr));
     B.in = {kUserOut, 0};  // z-pass: columns (l0 = x, l1 = y) of L1 -> L2
     set_side(B.a.in, nxc, 1, nz * nxc);
     B.out = {kWs, 0};
     set_l2_zpass(B.a.out);
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, kStrided, (int)nz, nxc, ny, nullptr, nullptr));
+    ST(finish_stage(pl, B, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr));
     C.in = {kWs, 0};  // y-pass: columns (l0 = x, l1 = z) of L2 -> natural `out`
     set_l2_ypass(C.a.in);
     C.out = {kUserOut, 0};
@@ -987,7 +1032,7 @@ dfft_status_t build_single_blocked(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.a.scale = 1.0;
     C.last_fwd = true;  // t = y, l0 = x, l1 = z
     C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
-    ST(finish_stage(pl, C, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
+    ST(finish_stage(pl, C, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
   } else {
     // scratch: c2c: L2 in `out` (nxc % w == 0 checked), L1 in ws;  c2r: both in ws
     rp.ws_bytes = (size_t)((c2r ? Wb + W : W) * es);
@@ -998,26 +1043,26 @@ dfft_status_t build_single_blocked(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     A.out = l2;
     set_l2_ypass(A.a.out);
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
+    ST(finish_stage(pl, A, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
     B.in = l2;  // z-pass: columns (l0 = x, l1 = y) of L2 -> L1
     set_l2_zpass(B.a.in);
     B.out = l1;
     set_side(B.a.out, nxc, 1, nz * nxc);
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, kStrided, (int)nz, nxc, ny, nullptr, nullptr));
+    ST(finish_stage(pl, B, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr));
     C.in = l1;  // x-pass: lines (l0 = y, l1 = z) of L1 -> natural `out`, ×1/N
     set_l1_lines(C.a.in);
     C.out = {kUserOut, 0};
     set_side(C.a.out, 1, nxl, ny * nxl);
-    C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
-    ST(finish_stage(pl, C, c2r ? kContigC2R : kContig, (int)nxl, ny, nz, nullptr, nullptr));
+    C.a.scale = (xreal(pl) ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
+    ST(finish_stage(pl, C, fam_x_inv(pl), (int)nxl, ny, nz, nullptr, nullptr));
   }
   return DFFT_SUCCESS;
 }
 
 dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
-  const long long nxl = pl->r2c ? nx / 2 : nx;
+  const long long nxl = xreal(pl) ? nx / 2 : nx;
   const long long W = nxc * ny * nz;
   const bool c2r = pl->r2c && pl->dir == DFFT_INVERSE;  // the real `out` cannot hold a complex stage
   rp.ws_bytes = (size_t)((c2r ? 2 : 1) * W * es);
@@ -1033,7 +1078,7 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Z.out = {kWs, c2r ? W * es : 0};
     set_side(Z.a.out, nxc, 1, nz * nxc);
     Z.a.scale = 1.0;
-    return finish_stage(pl, Z, kStrided, (int)nz, nxc, ny, nullptr, nullptr);
+    return finish_stage(pl, Z, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr);
   };
   if (pl->dir == DFFT_FORWARD) {
     A.in = {kUserIn, 0};  // lines (l0 = y, l1 = z)
@@ -1041,7 +1086,7 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     A.out = {kUserOut, 0};
     set_side(A.a.out, 1, nxc, ny * nxc);
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, pl->r2c ? kContigR2C : kContig, (int)nxl, ny, nz, nullptr, nullptr));
+    ST(finish_stage(pl, A, fam_x_fwd(pl), (int)nxl, ny, nz, nullptr, nullptr));
     ST(zpass(B));
     C.in = {kWs, 0};  // columns (l0 = x, l1 = z)
     set_side(C.a.in, nz * nxc, 1, nxc);
@@ -1050,21 +1095,21 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.a.scale = 1.0;
     C.last_fwd = true;  // t = y, l0 = x, l1 = z
     C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
-    ST(finish_stage(pl, C, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
+    ST(finish_stage(pl, C, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
   } else {
     A.in = {kUserIn, 0};  // columns (l0 = x, l1 = z)
     set_side(A.a.in, nxc, 1, ny * nxc);
     A.out = c2r ? Ref{kWs, 0} : Ref{kUserOut, 0};
     set_side(A.a.out, nxc, 1, ny * nxc);
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, kStrided, (int)ny, nxc, nz, nullptr, nullptr));
+    ST(finish_stage(pl, A, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
     ST(zpass(B));
     C.in = {kWs, c2r ? W * es : 0};  // lines (l0 = y, l1 = z) of ws [y][z][x]
     set_side(C.a.in, 1, nz * nxc, nxc);
     C.out = {kUserOut, 0};
     set_side(C.a.out, 1, nxl, ny * nxl);
-    C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
-    ST(finish_stage(pl, C, c2r ? kContigC2R : kContig, (int)nxl, ny, nz, nullptr, nullptr));
+    C.a.scale = (xreal(pl) ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
+    ST(finish_stage(pl, C, fam_x_inv(pl), (int)nxl, ny, nz, nullptr, nullptr));
   }
   return DFFT_SUCCESS;
 }
@@ -1093,7 +1138,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   auto r1off = [&](const InvLayout& Lr, long long ir, long long is, long long k) {
     return Lr.R1 + Zn * g.Y1n(ir) * (g.Xlo(is) + g.x0(is, k));
   };
-  const long long nxl = pl->r2c ? g.nx / 2 : g.nx;
+  const long long nxl = xreal(pl) ? g.nx / 2 : g.nx;
   rp.A.resize(K);
   rp.B.resize(K);
   rp.E1.resize(K);
@@ -1125,7 +1170,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       A.a.out.mT = g.ny;
     }
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, kStrided, (int)g.nz, xc, Y3n, nullptr, &aseg));
+    ST(finish_stage(pl, A, fam_s(pl), (int)g.nz, xc, Y3n, nullptr, &aseg));
     // first exchange of the inverse = T2⁻¹ on the column group
     Exchange& E1 = rp.E1[k];
     E1.comm = 1;
@@ -1178,7 +1223,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       B.a.out.mT = Zn;
     }
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, kStrided, (int)g.ny, xc, Zn, nullptr, &bseg));
+    ST(finish_stage(pl, B, fam_s(pl), (int)g.ny, xc, Zn, nullptr, &bseg));
     // second exchange of the inverse = T1⁻¹ on the row group
     Exchange& E2 = rp.E2[k];
     E2.comm = 0;
@@ -1219,8 +1264,8 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   }
   C.out = {kUserOut, 0};
   set_side(C.a.out, 1, nxl, Y1n * nxl);
-  C.a.scale = (pl->r2c ? 2.0 : 1.0) / ((double)g.nx * (double)g.ny * (double)g.nz);
-  ST(finish_stage(pl, C, pl->r2c ? kContigC2R : kContig, (int)nxl, Y1n, Zn, &cseg, nullptr));
+  C.a.scale = (xreal(pl) ? 2.0 : 1.0) / ((double)g.nx * (double)g.ny * (double)g.nz);
+  ST(finish_stage(pl, C, fam_x_inv(pl), (int)nxl, Y1n, Zn, &cseg, nullptr));
   return DFFT_SUCCESS;
 }
 
@@ -1818,7 +1863,7 @@ static dfft_status_t validate(int P, int64_t nx, int64_t ny, int64_t nz, dfft_de
   int p1 = *p1p, p2 = *p2p;
   if (nx <= 0 || ny <= 0 || nz <= 0) return fail(DFFT_ERR_INVALID_VALUE, "grid extents must be positive");
   if (direction != DFFT_FORWARD && direction != DFFT_INVERSE) return fail(DFFT_ERR_INVALID_VALUE, "bad direction");
-  if (type < DFFT_C2C_F32 || type > DFFT_R2C_F64) return fail(DFFT_ERR_INVALID_VALUE, "bad type");
+  if (type < DFFT_C2C_F32 || type > DFFT_R2R_F64) return fail(DFFT_ERR_INVALID_VALUE, "bad type");
   if (decomp == DFFT_SLAB) {
     if (p2 != 1 || p1 != P) return fail(DFFT_ERR_INVALID_VALUE, "slab needs proc grid (nranks, 1)");
     p1 = 1;  // slab == pencil 1×P internally (z-slabs -> y-slabs)
@@ -1829,9 +1874,12 @@ static dfft_status_t validate(int P, int64_t nx, int64_t ny, int64_t nz, dfft_de
   if (p1 < 1 || p2 < 1 || (long long)p1 * p2 != P)
     return fail(DFFT_ERR_INVALID_VALUE, "proc grid %d x %d != nranks %d", p1, p2, P);
   bool r2c = type == DFFT_R2C_F32 || type == DFFT_R2C_F64;
+  bool r2r = type == DFFT_R2R_F32 || type == DFFT_R2R_F64;
   if (r2c && nx % 2) return fail(DFFT_ERR_UNSUPPORTED, "R2C needs even nx");
-  long long nxc = r2c ? nx / 2 + 1 : nx;
-  long long nfft_x = r2c ? nx / 2 : nx;
+  if (r2r && (nx % 2 || ny % 2 || nz % 2))
+    return fail(DFFT_ERR_UNSUPPORTED, "R2R (DCT via Makhoul's permutation) needs even extents");
+  long long nxc = r2c ? nx / 2 + 1 : r2r ? nx / 2 : nx;
+  long long nfft_x = (r2c || r2r) ? nx / 2 : nx;
   if (!length_ok(nfft_x) || !length_ok(ny) || !length_ok(nz))
     return fail(DFFT_ERR_UNSUPPORTED, "axis lengths (%lld,%lld,%lld): need 2^a 3^b 5^c 7^d from the instantiated set",
                 (long long)nfft_x, (long long)ny, (long long)nz);
@@ -1851,10 +1899,12 @@ dfft_status_t dfft_decomp_box(int64_t nx, int64_t ny, int64_t nz, dfft_decomp_t 
   ST(validate(P, nx, ny, nz, decomp, &p1, &p2, type, direction));
   if (rank < 0 || rank >= P) return fail(DFFT_ERR_INVALID_VALUE, "rank %d out of range", rank);
   bool r2c = type == DFFT_R2C_F32 || type == DFFT_R2C_F64;
-  Geo g{nx, ny, nz, r2c ? nx / 2 + 1 : nx, p1, p2, 1};
+  bool r2r = type == DFFT_R2R_F32 || type == DFFT_R2R_F64;
+  Geo g{nx, ny, nz, r2c ? nx / 2 + 1 : r2r ? nx / 2 : nx, p1, p2, 1};
   long long i = rank / p2, j = rank % p2;
+  const long long xs = r2r ? 2 : 1;  // R2R: x split in pairs of reals (complex-pair columns)
   int64_t d1lo[3] = {0, g.Y1lo(i), g.Zlo(j)}, d1n[3] = {nx, g.Y1n(i), g.Zn(j)};
-  int64_t d3lo[3] = {g.Xlo(i), g.Y3lo(j), 0}, d3n[3] = {g.Xn(i), g.Y3n(j), nz};
+  int64_t d3lo[3] = {xs * g.Xlo(i), g.Y3lo(j), 0}, d3n[3] = {xs * g.Xn(i), g.Y3n(j), nz};
   bool d1 = (which == 0) == (direction == DFFT_FORWARD);
   memcpy(lo, d1 ? d1lo : d3lo, sizeof d1lo);
   memcpy(n, d1 ? d1n : d3n, sizeof d1n);
@@ -1870,8 +1920,9 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   int P = comm->nranks;
   ST(validate(P, nx, ny, nz, decomp, &p1, &p2, type, direction));
   bool r2c = type == DFFT_R2C_F32 || type == DFFT_R2C_F64;
-  bool f64 = type == DFFT_C2C_F64 || type == DFFT_R2C_F64;
-  long long nxc = r2c ? nx / 2 + 1 : nx;
+  bool r2r = type == DFFT_R2R_F32 || type == DFFT_R2R_F64;
+  bool f64 = type == DFFT_C2C_F64 || type == DFFT_R2C_F64 || type == DFFT_R2R_F64;
+  long long nxc = r2c ? nx / 2 + 1 : r2r ? nx / 2 : nx;
   int Kreq = (int)(flags & 0xff);
   bool overlap = !(flags & DFFT_FLAG_NO_OVERLAP);
   long long kmax = direction == DFFT_FORWARD ? nz / p2 : nxc / p1;  // chunk axis extent
@@ -1917,6 +1968,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   pl->dir = direction;
   pl->f64 = f64;
   pl->r2c = r2c;
+  pl->r2r = r2r;
   pl->overlap = overlap;
   pl->es = f64 ? 16 : 8;
   // exchange over NVLink peer memory unless asked for NCCL (flag or DFFT_EXCHANGE=nccl)
@@ -1975,10 +2027,12 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
     rp.j = rp.rank % p2;
     // D1 = (x whole, y by i, z by j);  D3 = (x by i, y by j, z whole)
     int64_t d1lo[3] = {0, g.Y1lo(rp.i), g.Zlo(rp.j)}, d1n[3] = {nx, g.Y1n(rp.i), g.Zn(rp.j)};
-    int64_t d3lo[3] = {g.Xlo(rp.i), g.Y3lo(rp.j), 0}, d3n[3] = {g.Xn(rp.i), g.Y3n(rp.j), nz};
+    // R2R boxes are real on both sides; x splits in pairs (complex-pair columns of the kernels)
+    const long long xs = r2r ? 2 : 1;
+    int64_t d3lo[3] = {xs * g.Xlo(rp.i), g.Y3lo(rp.j), 0}, d3n[3] = {xs * g.Xn(rp.i), g.Y3n(rp.j), nz};
     size_t real_es = pl->es / 2;
-    size_t d1b = (size_t)(d1n[0] * d1n[1] * d1n[2]) * (r2c ? real_es : pl->es);
-    size_t d3b = (size_t)(d3n[0] * d3n[1] * d3n[2]) * pl->es;
+    size_t d1b = (size_t)(d1n[0] * d1n[1] * d1n[2]) * ((r2c || r2r) ? real_es : pl->es);
+    size_t d3b = (size_t)(d3n[0] * d3n[1] * d3n[2]) * (r2r ? real_es : pl->es);
     if (direction == DFFT_FORWARD) {
       memcpy(rp.in_lo, d1lo, sizeof d1lo);
       memcpy(rp.in_n, d1n, sizeof d1n);
@@ -2126,6 +2180,7 @@ dfft_status_t dfft_execute_sim(dfft_plan_t pl, const void* const* ins, void* con
 dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double dz) {
   if (!pl) return fail(DFFT_ERR_INVALID_VALUE, "null plan");
   if (pl->dir != DFFT_FORWARD) return fail(DFFT_ERR_INVALID_VALUE, "the Poisson multiplier belongs to a forward plan");
+  if (pl->r2r) return fail(DFFT_ERR_UNSUPPORTED, "the periodic Poisson multiplier applies to C2C/R2C plans");
   const bool on = dx > 0 && dy > 0 && dz > 0;
   if (!on && (dx != 0 || dy != 0 || dz != 0))
     return fail(DFFT_ERR_INVALID_VALUE, "grid spacings must all be > 0 (or all 0 to switch the multiplier off)");

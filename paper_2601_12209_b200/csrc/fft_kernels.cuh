@@ -353,6 +353,7 @@ struct PassArgs {
   SideMap in, out;
   const void* tw;    // per-pass twiddle tables (complex), sched_twoff layout
   const void* tw2;   // R2C/C2R: w^k = exp(DIR·2πi·k/(2N)), k < N (the split/merge twiddles)
+  const void* tw3;   // R2R (DCT): c_k = exp(DIR·iπk/(2L)), k < L, L = the real line length
   long long L0, L1;  // line grid: lines (l0, l1), l0 < L0, l1 < L1 (strided: l0 = the column)
   double scale;      // applied to the outputs of the last pass (1 = none)
   // persistent strided kernels: tile order.  Tiles run in groups of g0 column tiles × all L1
@@ -500,6 +501,18 @@ template <typename C, bool UNIT_T = false, bool SPEC = false, bool TB = false> s
     }
     return *seg_ptr<const C>(*mi, t, i0, i1);
   }
+  // R2R lines are real: real element r of a line is component r&1 of complex element r>>1
+  __device__ __forceinline__ R load_real(int r) const {
+    const int t = r >> 1;
+    const C* p = mi->ttab == nullptr ? in + (UNIT_T ? lin + t : (long long)t * mi->tstride + lin)
+                                     : seg_ptr<const C>(*mi, t, i0, i1);
+    return reinterpret_cast<const R*>(p)[r & 1];
+  }
+  __device__ __forceinline__ void store_real(int r, R v) const {
+    const int t = r >> 1;
+    C* p = mo->ttab == nullptr ? out + (UNIT_T ? lout + t : (long long)t * mo->tstride + lout) : seg_ptr<C>(*mo, t, o0, o1);
+    reinterpret_cast<R*>(p)[r & 1] = v * scale;
+  }
   __device__ __forceinline__ void store(int t, C v) const {
     if (scale != 1) { v.x *= scale; v.y *= scale; }
     v = apply_spec(t, v);
@@ -548,6 +561,46 @@ template <typename C, int N> struct C2RIO : GIO<C, true> {
   }
 };
 
+// R2R (reading R21; DCT-II forward, DCT-III/(2L) inverse along every axis) by Makhoul's
+// permutation: a real line x of even length L is reordered v_n = x_{2n}, v_{L-1-n} = x_{2n+1}
+// (n < L/2), V = DFT_L(v), and X_k = 2·Re(c_k V_k), c_k = exp(-iπk/(2L)).  The inverse builds
+// V_k = ½·conj(c_k)·(X_k − i·X_{L−k}) (X_L = 0), v = IDFT_L(V), x_{perm(n)} = v_n.
+__host__ __device__ constexpr int dct_perm(int n, int L) { return n < L / 2 ? 2 * n : 2 * (L - 1 - n) + 1; }
+
+// x lines (contig, MODE 3/4): L = 2N reals per line; the N-point complex FFT runs on the packed
+// z_m = v_{2m} + i·v_{2m+1} (the R2C trick), so V comes from the R2C split / goes in through the
+// C2R merge.  MODE 3 loads the permuted reals; MODE 4 loads X and builds the merged spectrum.
+template <typename C, int N> struct DctXFwdIO : GIO<C, true> {
+  C* zb;
+  __device__ __forceinline__ C load(int t) const {
+    return {this->load_real(dct_perm(2 * t, 2 * N)), this->load_real(dct_perm(2 * t + 1, 2 * N))};
+  }
+  __device__ __forceinline__ void store(int t, C v) const { zb[t] = v; }
+};
+template <typename C, int N> struct DctXInvIO : GIO<C, true> {
+  using R = decltype(C{}.x);
+  const C* tw2;  // exp(+2πi t / 2N)
+  const C* tw3;  // exp(+iπk / (4N)), k < 2N
+  __device__ __forceinline__ C vk(int k) const {  // V_k = ½·conj(c_k)·(X_k − i·X_{L−k}), k ≤ N
+    const R xk = this->load_real(k), xl = k == 0 ? R(0) : this->load_real(2 * N - k);
+    const C c = __ldg(tw3 + k);
+    const C d = {xk * R(0.5), -xl * R(0.5)};
+    return cmul(c, d);
+  }
+  __device__ __forceinline__ C load(int t) const {
+    const C xt = vk(t), xn = vk(N - t);
+    const C w = __ldg(tw2 + t);
+    const C e = {(xt.x + xn.x) * R(0.5), (xt.y - xn.y) * R(0.5)};
+    const C d = {(xt.x - xn.x) * R(0.5), (xt.y + xn.y) * R(0.5)};
+    const C o = cmul(d, w);
+    return {e.x - o.y, e.y + o.x};  // E + i·O  (IDFT_N of it = v_{2m} + i·v_{2m+1}, times N)
+  }
+  __device__ __forceinline__ void store(int t, C v) const {
+    this->store_real(dct_perm(2 * t, 2 * N), v.x);
+    this->store_real(dct_perm(2 * t + 1, 2 * N), v.y);
+  }
+};
+
 template <typename Real, int N, int DIR, int MODE, bool TB = false>
 __global__ void __launch_bounds__(ContigCfg<N>::THREADS)
 fft_contig_kernel(const __grid_constant__ PassArgs a) {
@@ -586,10 +639,41 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
         io.GIO<C, true>::store(k, cadd(e, cmul(w, o)));
       }
     }
-  } else {
+  } else if constexpr (MODE == 2) {
     C2RIO<C, N> io;
     io.init(a.in, a.out, l0, l1, a.scale);
     io.tw2 = reinterpret_cast<const C*>(a.tw2);
+    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+  } else if constexpr (MODE == 3) {  // forward DCT-II of real x-lines of length 2N
+    using R = Real;
+    DctXFwdIO<C, N> io;
+    io.init(a.in, a.out, l0, l1, a.scale);
+    C* zb = smem + li * Cfg::LS;
+    io.zb = zb;
+    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+    __syncthreads();
+    if (active) {
+      const C* tw2 = reinterpret_cast<const C*>(a.tw2);  // exp(-2πi k / 2N)
+      const C* tw3 = reinterpret_cast<const C*>(a.tw3);  // exp(-iπk / (4N)), k < 2N
+      for (int k = j; k <= N; k += Cfg::S.T) {
+        const C zk = zb[k == N ? 0 : k], zn = zb[k == 0 ? 0 : N - k];
+        const C e = {(zk.x + zn.x) * R(0.5), (zk.y - zn.y) * R(0.5)};
+        const C o = {(zk.y + zn.y) * R(0.5), (zn.x - zk.x) * R(0.5)};
+        const C w = k == N ? C{-1, 0} : __ldg(tw2 + k);
+        const C v = cadd(e, cmul(w, o));  // V_k of the real permuted line, k <= N
+        const C ck = __ldg(tw3 + k);
+        io.store_real(k, R(2) * (ck.x * v.x - ck.y * v.y));  // X_k = 2 Re(c_k V_k)
+        if (k > 0 && k < N) {  // X_{2N-k} = 2 Re(c_{2N-k} conj V_k)
+          const C cl = __ldg(tw3 + 2 * N - k);
+          io.store_real(2 * N - k, R(2) * (cl.x * v.x + cl.y * v.y));
+        }
+      }
+    }
+  } else {  // MODE 4: inverse DCT-III of real x-lines of length 2N (scale folded by the host)
+    DctXInvIO<C, N> io;
+    io.init(a.in, a.out, l0, l1, a.scale);
+    io.tw2 = reinterpret_cast<const C*>(a.tw2);
+    io.tw3 = reinterpret_cast<const C*>(a.tw3);
     stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
   }
 }
@@ -638,6 +722,80 @@ fft_strided_kernel(const __grid_constant__ PassArgs a) {
   io.spectral(a, active ? l0 : 0, l1);
   StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
   stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
+}
+
+// Strided R2R stage (y or z DCT, reading R21): the real array is viewed as complex pairs of
+// adjacent x columns, so one complex column holds two real columns a (re) and b (im) and one
+// N-point complex FFT serves both.  Forward: z_t = column[perm(t)], Z = DFT_N(z),
+//   Va_k = (Z_k + conj Z_{N−k})/2, Vb_k = (Z_k − conj Z_{N−k})/(2i),
+//   X_k = (2 Re(c_k Va_k), 2 Re(c_k Vb_k))  — the last pass goes to shared memory and each thread
+// finishes the pairs (k, N−k).  Inverse: Z_t = Va_t + i·Vb_t with V from rows t and N−t, z =
+// IDFT_N(Z) (unnormalised; the host folds 1/N), row perm(t) = z_t.
+template <typename C, int N, int DIR> struct DctStridedIO : GIO<C> {
+  using R = decltype(C{}.x);
+  const C* tw3;  // c_k = exp(DIR·iπk/(2N)), k < N
+  C* tile;       // forward: the last pass's outputs, dense [t][W] at column c
+  int W, c;
+  __device__ __forceinline__ C load(int t) const {
+    if constexpr (DIR < 0) {
+      return GIO<C>::load(dct_perm(t, N));
+    } else {
+      const C xt = GIO<C>::load(t);
+      const C xl = t == 0 ? C{0, 0} : GIO<C>::load(N - t);
+      const C cc = __ldg(tw3 + t);  // conj(c_t) for the inverse table
+      const C da = {xt.x * R(0.5), -xl.x * R(0.5)}, db = {xt.y * R(0.5), -xl.y * R(0.5)};
+      const C va = cmul(cc, da), vb = cmul(cc, db);
+      return {va.x - vb.y, va.y + vb.x};  // Va + i·Vb
+    }
+  }
+  __device__ __forceinline__ void store(int t, C v) const {
+    if constexpr (DIR < 0) tile[t * W + c] = v;
+    else GIO<C>::store(dct_perm(t, N), v);
+  }
+};
+
+template <typename Real, int N, int DIR>
+__global__ void __launch_bounds__(StridedCfg<Real, N>::THREADS)
+fft_strided_dct_kernel(const __grid_constant__ PassArgs a) {
+  using C = typename CT<Real>::type;
+  using R = Real;
+  using Cfg = StridedCfg<Real, N>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* smem = reinterpret_cast<C*>(smem_raw);
+  C* tile = smem;  // dense [t][W] (forward): aliases the pass buffer (the last pass reads it first)
+  const int c = threadIdx.x % Cfg::W;
+  const int j = threadIdx.x / Cfg::W;
+  const long long ntile = (a.L0 + Cfg::W - 1) / Cfg::W;
+  const long long l1 = blockIdx.x / ntile;
+  const long long l0 = (blockIdx.x - l1 * ntile) * Cfg::W + c;
+  const bool active = l0 < a.L0;
+  DctStridedIO<C, N, DIR> io;
+  io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
+  io.tw3 = reinterpret_cast<const C*>(a.tw3);
+  io.tile = tile;
+  io.W = Cfg::W;
+  io.c = c;
+  StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
+  stockham_pass<C, N, DIR, 0>(io, sm, smem, reinterpret_cast<const C*>(a.tw), j, active);
+  if constexpr (DIR < 0) {
+    __syncthreads();
+    if (active) {
+      const C* tw3 = reinterpret_cast<const C*>(a.tw3);
+      for (int k = j; k <= N / 2; k += Cfg::S.T) {
+        const C zk = tile[k * Cfg::W + c], zn = tile[(k == 0 ? 0 : N - k) * Cfg::W + c];
+        // s = Z_k + conj Z_{N-k} (= 2 Va_k),  d = Z_k − conj Z_{N-k} (= 2i Vb_k)
+        const C sk = {zk.x + zn.x, zk.y - zn.y}, dk = {zk.x - zn.x, zk.y + zn.y};
+        const C ck = __ldg(tw3 + k);
+        // X^a_k = Re(c_k s), X^b_k = Re(c_k d / i) = Im(c_k d)
+        io.GIO<C>::store(k, C{ck.x * sk.x - ck.y * sk.y, ck.x * dk.y + ck.y * dk.x});
+        if (k > 0 && 2 * k != N) {  // the partner row N−k: s' = conj s, d' = −conj d
+          const C cl = __ldg(tw3 + N - k);
+          const C sl = {sk.x, -sk.y}, dl = {-dk.x, dk.y};
+          io.GIO<C>::store(N - k, C{cl.x * sl.x - cl.y * sl.y, cl.x * dl.y + cl.y * dl.x});
+        }
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------ strided family, TMA-staged

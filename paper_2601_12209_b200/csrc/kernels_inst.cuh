@@ -13,7 +13,18 @@ KernelInfo make_contig() {
   if constexpr (MODE == 0) k.fn_tb = (const void*)&fft_contig_kernel<Real, N, DIR, 0, true>;
   k.threads = Cfg::THREADS;
   k.per_cta = Cfg::LPC;
-  k.smem = (Cfg::S.npass > 1 || MODE == 1) ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
+  k.smem = (Cfg::S.npass > 1 || MODE == 1 || MODE == 3) ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
+  k.twlen = sched_twlen(Cfg::S);
+  return k;
+}
+template <typename Real, int N, int DIR>
+KernelInfo make_strided_dct() {
+  using Cfg = StridedCfg<Real, N>;
+  KernelInfo k;
+  k.fn = (const void*)&fft_strided_dct_kernel<Real, N, DIR>;
+  k.threads = Cfg::THREADS;
+  k.per_cta = Cfg::W;
+  k.smem = (size_t)Cfg::SMEM_ELEMS * sizeof(Real) * 2;
   k.twlen = sched_twlen(Cfg::S);
   return k;
 }
@@ -33,7 +44,7 @@ KernelInfo make_strided() {
     k.tma_st_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 3>;   // stage-as-output flow
     k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1>;  // work-buffer flow (A/B)
     k.tma_bk_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 2>;
-    if constexpr (DIR < 0) k.tma_st_spec_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 3, true>;
+    if constexpr (DIR < 0) k.tma_st_spec_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, true>;
     k.tma_threads = TC::THREADS;
     k.tma_w = TC::W;
     k.tma_boxr = TC::BOXR;
@@ -61,6 +72,8 @@ bool DFFT_LOOKUP(int family, int n, int dir, KernelInfo* out) {
     if (family == kContig) *out = dir < 0 ? make_contig<DFFT_REAL, N, -1>() : make_contig<DFFT_REAL, N, 1>(); \
     else if (family == kContigR2C) *out = make_contig<DFFT_REAL, N, -1, 1>();                  \
     else if (family == kContigC2R) *out = make_contig<DFFT_REAL, N, 1, 2>();                   \
+    else if (family == kContigDct) *out = dir < 0 ? make_contig<DFFT_REAL, N, -1, 3>() : make_contig<DFFT_REAL, N, 1, 4>(); \
+    else if (family == kStridedDct) *out = dir < 0 ? make_strided_dct<DFFT_REAL, N, -1>() : make_strided_dct<DFFT_REAL, N, 1>(); \
     else *out = dir < 0 ? make_strided<DFFT_REAL, N, -1>() : make_strided<DFFT_REAL, N, 1>();    \
     return true;
   switch (n) {

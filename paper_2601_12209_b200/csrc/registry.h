@@ -8,7 +8,7 @@
 
 namespace dfft {
 
-enum Family { kContig = 0, kStrided = 1, kContigR2C = 2, kContigC2R = 3 };
+enum Family { kContig = 0, kStrided = 1, kContigR2C = 2, kContigC2R = 3, kContigDct = 4, kStridedDct = 5 };
 
 struct KernelInfo {
   const void* fn = nullptr;
@@ -21,7 +21,7 @@ struct KernelInfo {
   // strided family only: persistent TMA-staged variant (null if not instantiable for n)
   const void* tma_fn = nullptr;
   const void* tma_st_fn = nullptr;  // same, with TMA stores (unsegmented output side)
-  const void* tma_st1_fn = nullptr;  // same, the r01 work-buffer flow (DFFT_TST_WORK=1)
+  const void* tma_st1_fn = nullptr;  // same, the work-buffer flow (default; tma_st_fn = OM 3, opt-in)
   const void* tma_bk_fn = nullptr;  // same, with bulk-copy stores (column-blocked segmented output)
   const void* tma_st_spec_fn = nullptr;  // TMA stores + Poisson multiplier (forward only)
   // two-warp-group variant (preferred when it fits): in-place padded stage buffers

@@ -458,3 +458,69 @@ def test_poisson_cfg5_box_f64(oracle_mod):
     # the paper's application shape class (Oceananigans periodic box, BASELINE configs[4])
     e = _poisson_case(oracle_mod, (768, 768, 384), "pencil", (1, 1), "f64", (1.0, 1.0, 1.0), "r2c", seed=260112209 + 5)
     assert e <= 1e-12, e
+
+
+# ------------------------------------------------------------------------------ R2R (f4)
+def _r2r_case(oracle_mod, shape, decomp, grid, prec, exchange="auto", chunks=0, seed=23):
+    """R2R forward (DCT-II per axis) vs oracle.dct3d, inverse of the oracle's spectrum (DCT-III /
+    2N per axis) vs oracle.dct3d(inverse=True), round trip (reading R21)."""
+    nx, ny, nz = shape
+    P = grid[0] * grid[1]
+    comm = dfft.Comm.simulated(P, 0) if P > 1 else dfft.Comm.create(nranks=1, rank=0, device=0)
+    dt = "r2r_" + prec
+    fwd = dfft.Plan(comm, shape, decomp, grid, dt, dfft.FORWARD, chunks=chunks, exchange=exchange)
+    inv = dfft.Plan(comm, shape, decomp, grid, dt, dfft.INVERSE, chunks=chunks, exchange=exchange)
+    f32 = prec == "f32"
+    a = oracle_mod.gen_real(seed, shape, f32=f32)
+    X = oracle_mod.dct3d(a)
+    H = inputs.gen_real_np(seed + 1, shape, f32=f32)
+    xs, ys, hs, zs, ws = [], [], [], [], []
+    for r in range(P):
+        lo, n = fwd.box(0, r)
+        x = fwd.alloc_in(r)
+        inputs.fill_box_cuda(x, seed, shape, lo, n, False)
+        xs.append(x)
+        ys.append(fwd.alloc_out(r))
+        lo, n = inv.box(0, r)
+        hs.append(torch.from_numpy(np.ascontiguousarray(box_slice(H, lo, n))).to(
+            torch.float32 if f32 else torch.float64).cuda())
+        zs.append(inv.alloc_out(r))
+        ws.append(inv.alloc_out(r))
+    if P > 1:
+        fwd.execute_sim(xs, ys)
+        inv.execute_sim(hs, zs)
+        inv.execute_sim(ys, ws)
+    else:
+        fwd.execute(xs[0], ys[0])
+        inv.execute(hs[0], zs[0])
+        inv.execute(ys[0], ws[0])
+    torch.cuda.synchronize()
+    Y, Z, Wr = np.zeros_like(X), np.zeros_like(X), np.zeros_like(X)
+    for r in range(P):
+        lo, n = fwd.box(1, r)
+        box_slice(Y, lo, n)[...] = ys[r].cpu().numpy()
+        lo, n = inv.box(1, r)
+        box_slice(Z, lo, n)[...] = zs[r].cpu().numpy()
+        box_slice(Wr, lo, n)[...] = ws[r].cpu().numpy()
+    return (oracle_mod.rel_l2(Y, X), oracle_mod.rel_l2(Z, oracle_mod.dct3d(H, inverse=True)),
+            oracle_mod.rel_l2(Wr, a))
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,decomp,grid,exchange", [
+    ((16, 12, 8), "pencil", (1, 1), "auto"),
+    ((64, 48, 32), "pencil", (1, 1), "auto"),
+    ((24, 16, 12), "pencil", (2, 4), "nccl"),
+    ((24, 16, 12), "pencil", (2, 4), "p2p"),   # fused-store layouts, B->C chunks
+    ((48, 24, 12), "slab", (4, 1), "p2p"),
+    ((48, 24, 12), "pencil", (5, 2), "nccl"),  # uneven pair splits
+])
+def test_r2r_dct(oracle_mod, shape, decomp, grid, exchange, prec):
+    ef, ei, er = _r2r_case(oracle_mod, shape, decomp, grid, prec, exchange)
+    assert ef <= GATE[prec] and ei <= GATE[prec] and er <= GATE[prec], (ef, ei, er)
+    assert ef <= QUALITY[prec] and ei <= QUALITY[prec], (ef, ei, er)
+
+
+def test_r2r_dct_256_f64_single_gpu(oracle_mod):
+    ef, ei, er = _r2r_case(oracle_mod, (256, 128, 64), "pencil", (1, 1), "f64")
+    assert ef <= 1e-12 and ei <= 1e-12 and er <= 1e-12, (ef, ei, er)
