@@ -155,8 +155,11 @@ dfft_status_t dfft_plan_chunks(dfft_plan_t plan, int* chunks);
  * `out` its output box (forward: D3; inverse: D1), both device pointers on the plan's
  * GPU, 16-byte aligned, dense as described above, non-overlapping; `in` is never written.
  * Stream-ordered and asynchronous: work is enqueued after everything already on `stream`
- * and `stream` waits for its completion; no host synchronisation; capturable in a CUDA
- * graph.  Collective: all ranks execute matching plans in the same order.
+ * and `stream` waits for its completion; no host synchronisation.  Single-rank plans (and
+ * NCCL-transport plans) are capturable in a CUDA graph; plans with the IPC-window transports
+ * (fused stores / copy engine, the P > 1 default) are not: their flag words carry a per-execute
+ * epoch fixed at enqueue time, so a replayed graph would wait on stale values.
+ * Collective: all ranks execute matching plans in the same order.
  * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  */
 dfft_status_t dfft_execute(dfft_plan_t plan, const void* in, void* out, void* stream);

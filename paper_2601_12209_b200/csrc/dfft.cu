@@ -1080,7 +1080,31 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Z.a.scale = 1.0;
     return finish_stage(pl, Z, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr);
   };
-  if (pl->dir == DFFT_FORWARD) {
+  if (pl->dir == DFFT_FORWARD && !getenv("DFFT_SINGLE_FWD_ZREAD")) {
+    // forward with one large-pitch side in total (r01 session 2): the x-pass writes [y][z][x],
+    // the z-pass reads it at a small pitch and writes natural order (the one large-pitch side),
+    // and the y-pass runs natural -> natural (both sides at the x-row pitch: 3.08 vs 3.75 ms)
+    A.in = {kUserIn, 0};  // lines (l0 = y, l1 = z)
+    set_side(A.a.in, 1, nxl, ny * nxl);
+    A.out = {kUserOut, 0};  // [y][z][x]
+    set_side(A.a.out, 1, nz * nxc, nxc);
+    A.a.scale = 1.0;
+    ST(finish_stage(pl, A, fam_x_fwd(pl), (int)nxl, ny, nz, nullptr, nullptr));
+    B.in = {kUserOut, 0};  // z-pass: columns (l0 = x, l1 = y) of [y][z][x] -> ws natural
+    set_side(B.a.in, nxc, 1, nz * nxc);
+    B.out = {kWs, 0};
+    set_side(B.a.out, ny * nxc, 1, nxc);
+    B.a.scale = 1.0;
+    ST(finish_stage(pl, B, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr));
+    C.in = {kWs, 0};  // y-pass: columns (l0 = x, l1 = z), natural -> natural
+    set_side(C.a.in, nxc, 1, ny * nxc);
+    C.out = {kUserOut, 0};
+    set_side(C.a.out, nxc, 1, ny * nxc);
+    C.a.scale = 1.0;
+    C.last_fwd = true;  // t = y, l0 = x, l1 = z
+    C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
+    ST(finish_stage(pl, C, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
+  } else if (pl->dir == DFFT_FORWARD) {
     A.in = {kUserIn, 0};  // lines (l0 = y, l1 = z)
     set_side(A.a.in, 1, nxl, ny * nxl);
     A.out = {kUserOut, 0};
@@ -1096,6 +1120,27 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.last_fwd = true;  // t = y, l0 = x, l1 = z
     C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
     ST(finish_stage(pl, C, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
+  } else if (!c2r && getenv("DFFT_SINGLE_INV_YWRITE")) {
+    // inverse with the large-pitch side on a store: y-pass natural -> [y][z][x] (in `out`),
+    // z-pass [y][z][x] -> ws [y][z][x] (both small), x-pass ws -> natural (A/B option)
+    A.in = {kUserIn, 0};  // y-pass: columns (l0 = x, l1 = z)
+    set_side(A.a.in, nxc, 1, ny * nxc);
+    A.out = {kUserOut, 0};
+    set_side(A.a.out, nz * nxc, 1, nxc);
+    A.a.scale = 1.0;
+    ST(finish_stage(pl, A, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
+    B.in = {kUserOut, 0};  // z-pass: columns (l0 = x, l1 = y)
+    set_side(B.a.in, nxc, 1, nz * nxc);
+    B.out = {kWs, 0};
+    set_side(B.a.out, nxc, 1, nz * nxc);
+    B.a.scale = 1.0;
+    ST(finish_stage(pl, B, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr));
+    C.in = {kWs, 0};  // x-pass: lines (l0 = y, l1 = z) of [y][z][x]
+    set_side(C.a.in, 1, nz * nxc, nxc);
+    C.out = {kUserOut, 0};
+    set_side(C.a.out, 1, nxl, ny * nxl);
+    C.a.scale = (xreal(pl) ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
+    ST(finish_stage(pl, C, fam_x_inv(pl), (int)nxl, ny, nz, nullptr, nullptr));
   } else {
     A.in = {kUserIn, 0};  // columns (l0 = x, l1 = z)
     set_side(A.a.in, nxc, 1, ny * nxc);

@@ -13,7 +13,7 @@ KernelInfo make_contig() {
   if constexpr (MODE == 0) k.fn_tb = (const void*)&fft_contig_kernel<Real, N, DIR, 0, true>;
   k.threads = Cfg::THREADS;
   k.per_cta = Cfg::LPC;
-  k.smem = (Cfg::S.npass > 1 || MODE == 1 || MODE == 3) ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
+  k.smem = (Cfg::S.npass > 1 || MODE == 1 || MODE >= 3) ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
   k.twlen = sched_twlen(Cfg::S);
   return k;
 }

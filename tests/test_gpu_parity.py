@@ -524,3 +524,30 @@ def test_r2r_dct(oracle_mod, shape, decomp, grid, exchange, prec):
 def test_r2r_dct_256_f64_single_gpu(oracle_mod):
     ef, ei, er = _r2r_case(oracle_mod, (256, 128, 64), "pencil", (1, 1), "f64")
     assert ef <= 1e-12 and ei <= 1e-12 and er <= 1e-12, (ef, ei, er)
+
+
+def test_cuda_graph_capture_single_gpu(oracle_mod):
+    """dfft_execute is stream-ordered and capturable for single-rank plans: capture fwd+inv once,
+    replay on new input, compare with the oracle (launch-bound small configs use this)."""
+    shape = (64, 64, 64)
+    comm = dfft.Comm.create(nranks=1, rank=0, device=0)
+    fwd = dfft.Plan(comm, shape, "slab", (1, 1), "c2c_f64", dfft.FORWARD)
+    inv = dfft.Plan(comm, shape, "slab", (1, 1), "c2c_f64", dfft.INVERSE)
+    x, y, z = fwd.alloc_in(), fwd.alloc_out(), inv.alloc_out()
+    inputs.fill_box_cuda(x, 3, shape, (0, 0, 0), shape, True)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up outside the capture (lazy init)
+        fwd.execute(x, y, stream=s)
+        inv.execute(y, z, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fwd.execute(x, y, stream=s)
+        inv.execute(y, z, stream=s)
+    inputs.fill_box_cuda(x, 7, shape, (0, 0, 0), shape, True)
+    g.replay()
+    torch.cuda.synchronize()
+    a = oracle_mod.gen_complex(7, shape)
+    assert oracle_mod.rel_l2(y.cpu().numpy(), oracle_mod.fft3d(a, -1)) <= 1e-12
+    assert oracle_mod.rel_l2(z.cpu().numpy(), a) <= 1e-12
