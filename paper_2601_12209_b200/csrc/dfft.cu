@@ -1990,12 +1990,20 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   // chunks pipeline the transfers against the FFTs; with fused stores the transfer happens
   // inside the FFT kernels themselves, so one chunk is the default there
   long long K = Kreq > 0 ? Kreq : (P > 1 && !p2p_mode ? (nccl_mode ? 4 : 8) : 1);
-  // fused stores: with a 1×P2 grid the x-FFT is local and overlaps the NVLink-bound y-FFT of the
-  // previous chunk (two streams); with P1 > 1 both are NVLink-bound, so one chunk
-  const bool bc_mode = p2p_mode && p1 > 1 && p2 > 1;
-  // r01 sweeps: fused stores need most SMs, so A(k+1)‖B(k) overlap does not pay
-  // (one chunk); with both exchanges remote, B(k)‖C(k-1) with B on 100 SMs does (2x2: 9.0 -> 8.6 ms)
-  if (p2p_mode && Kreq == 0) K = bc_mode ? 4 : 1;
+  // B→C pipeline whenever stage B stores to peers and stage C is local: both exchanges remote,
+  // or a 1×P2 forward (x-FFT local, y-FFT to the column peers, z-FFT local); DFFT_NO_BC=1 off
+  const bool bc_mode = p2p_mode && !getenv("DFFT_NO_BC") && p2 > 1 &&
+                       (p1 > 1 || (direction == DFFT_FORWARD && !getenv("DFFT_NO_BC_1XP")));
+  // r01 sweeps: with bulk-copy epilogues the NVLink-bound stage of a pair keeps
+  // ~95 % of its rate on 80 SMs, so pairing it with a local stage pays: B(k)‖C(k−1) when both
+  // exchanges are remote (2x2: 9.0 -> 8.1 ms) or on a 1×P2 forward
+  // chunks cost launches and flag round trips: pipeline only boxes of >= 256 MiB per rank
+  // (1024^3 c64 on 2-8 GPUs: 1-4 GiB), small problems (cfg2/cfg3) run one chunk
+  const double local_bytes = (double)nxc * ny * nz / P * (f64 ? 16.0 : 8.0);
+  // 1×P2 grids also pipeline the inverse (z-IFFT to the peers ‖ local y-IFFT, two streams):
+  // 1x2 1024^3 c64 fwd+inv 14.6 -> 12.6 ms with K = 4 and the NVLink stage on 80 SMs
+  if (p2p_mode && Kreq == 0)
+    K = ((bc_mode || (p1 == 1 && p2 > 1)) && local_bytes >= 256.0 * (1 << 20)) ? 4 : 1;
   if (bc_mode) kmax = direction == DFFT_FORWARD ? nxc / p1 : nz / p2;
   K = std::max<long long>(1, std::min<long long>(K, kmax));
   if (P == 1) K = 1;  // nothing to overlap
