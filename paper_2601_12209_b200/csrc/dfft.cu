@@ -225,8 +225,9 @@ dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
   if (k->tma_fn && k->tma_smem > 48 * 1024) {
     CU(cudaFuncSetAttribute(k->tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     CU(cudaFuncSetAttribute(k->tma_st_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
-    CU(cudaFuncSetAttribute(k->tma_bk_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
-    CU(cudaFuncSetAttribute(k->tma_st1_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
+    if (k->tma_bk_fn) CU(cudaFuncSetAttribute(k->tma_bk_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
+    if (k->tma_st1_fn)
+      CU(cudaFuncSetAttribute(k->tma_st1_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     if (k->tma_st_spec_fn)
       CU(cudaFuncSetAttribute(k->tma_st_spec_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
   }
@@ -501,7 +502,8 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   if (is_contig(family)) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
   else s.grid = ((L0 + s.k.per_cta - 1) / s.k.per_cta) * L1;
   if (s.grid >= (1LL << 31)) return fail(DFFT_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", s.grid);
-  if (family == kStrided && (s.k.tma_fn || s.k.tma2_fn) && g_use_tma && !in_tab && tensor_map_encoder()) {
+  if ((family == kStrided || family == kStridedDct) && (s.k.tma_fn || s.k.tma2_fn) && g_use_tma && !in_tab &&
+      tensor_map_encoder()) {
     const long long es = (long long)pl->es;
     bool ok = s.a.in.s0 == 1 && (s.a.in.tstride * es) % 16 == 0 && (L1 == 1 || (s.a.in.s1 * es) % 16 == 0) &&
               2 * L0 < (1LL << 32) && L1 < (1LL << 31);
@@ -1383,6 +1385,7 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
       void* targs[] = {&tin, &tout, &a};
       const long long grid = s.sm_cap > 0 ? std::min<long long>(s.tma_grid, (long long)s.sm_cap * s.tma_occ) : s.tma_grid;
       if (spec && !(use_st && s.tma_variant == 1 && s.k.tma_st_spec_fn)) goto plain;  // multiplier: TST or plain
+      if (s.k.tma_st_only && !use_st) goto plain;  // R2R: the TMA variant needs TMA stores
       if (spec)
         CU(cudaLaunchKernel(s.k.tma_st_spec_fn, dim3((unsigned)grid), dim3(s.k.tma_threads), targs, s.k.tma_smem, st));
       else if (s.tma_variant == 2)

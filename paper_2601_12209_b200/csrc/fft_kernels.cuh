@@ -924,7 +924,10 @@ template <typename Real, int N> struct TmaCfg {
 // buffer (drained by pass 0), the TMA store reads it from there, and thread 0 refills the
 // previous tile's stage right after its own pass-0 loads — two CTA barriers per tile instead
 // of four (ncu r01: barrier stalls were the top stall reason at 8 warps/SM).
-template <typename C, int W, int OM, bool SPEC = false> struct TmaIO : GIO<C, false, SPEC> {
+// DCT (R2R strided stages on the TMA kernel, OM 1 only): -1 forward (permuted loads from the
+// stage; the (k, N−k) post-processing runs on the output tile before the TMA store), +1 inverse
+// (V from stage rows t and N−t in the loads, permuted rows in the stores).
+template <typename C, int W, int OM, bool SPEC = false, int N_ = 0, int DCT = 0> struct TmaIO : GIO<C, false, SPEC> {
   static constexpr bool kSyncAfterLoad = OM != 3;
   static constexpr bool kRefillNoSync = OM == 3;
   static constexpr bool kLastBar = OM != 3;
@@ -938,11 +941,26 @@ template <typename C, int W, int OM, bool SPEC = false> struct TmaIO : GIO<C, fa
   int next_c0, next_l1, nbox, boxr, in_bw;
   uint32_t bytes;
   bool refill;
-  __device__ __forceinline__ C load(int t) const { return stage[t * W + c]; }
+  const C* tw3 = nullptr;  // DCT: c_k = exp(DCT·iπk/(2N))
+  __device__ __forceinline__ C load(int t) const {
+    if constexpr (DCT < 0) {
+      return stage[dct_perm(t, N_) * W + c];
+    } else if constexpr (DCT > 0) {
+      using R = decltype(C{}.x);
+      const C xt = stage[t * W + c];
+      const C xl = t == 0 ? C{0, 0} : stage[(N_ - t) * W + c];
+      const C cc = __ldg(tw3 + t);
+      const C da = {xt.x * R(0.5), -xl.x * R(0.5)}, db = {xt.y * R(0.5), -xl.y * R(0.5)};
+      const C va = cmul(cc, da), vb = cmul(cc, db);
+      return {va.x - vb.y, va.y + vb.x};
+    } else {
+      return stage[t * W + c];
+    }
+  }
   __device__ __forceinline__ void store(int t, C v) const {
     if constexpr (OM != 0) {
       if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
-      obuf[t * W + c] = this->apply_spec(t, v);
+      obuf[(DCT > 0 ? dct_perm(t, N_) : t) * W + c] = this->apply_spec(t, v);
     } else {
       GIO<C, false, SPEC>::store(t, v);
     }
@@ -969,7 +987,7 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
 // stores at a large stride from the SMs throttles the LSU (r01 ncu: lg_throttle); 2 = the
 // output is segmented into column-blocked windows (possibly peers' over NVLink) and each
 // segment of a tile leaves as one contiguous cp.async.bulk copy.
-template <typename Real, int N, int DIR, int OM, bool SPEC = false>
+template <typename Real, int N, int DIR, int OM, bool SPEC = false, int DCT = 0>
 __global__ void __launch_bounds__(TmaCfg<Real, N>::THREADS)
 fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
                        const __grid_constant__ PassArgs a) {
@@ -1014,7 +1032,8 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     const long long l0 = tx * Cfg::W + c;
     const bool active = l0 < a.L0;
     if (TST && !SOUT && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
-    TmaIO<C, Cfg::W, OM, SPEC> io;
+    TmaIO<C, Cfg::W, OM, SPEC, N, DCT> io;
+    io.tw3 = reinterpret_cast<const C*>(a.tw3);
     io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
     io.spectral(a, active ? l0 : 0, l1);
     io.stage = stages + s * Cfg::STAGE_ELEMS;
@@ -1041,6 +1060,23 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     mbar_wait(&bars[s], parity);
     StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
     stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, work, reinterpret_cast<const C*>(a.tw), j, active);
+    if constexpr (DCT < 0) {  // forward R2R: finish the row pairs (k, N−k) of the output tile
+      __syncthreads();
+      if (active) {
+        const C* tw3 = reinterpret_cast<const C*>(a.tw3);
+        for (int k = j; k <= N / 2; k += Cfg::S.T) {
+          const C zk = work[k * Cfg::W + c], zn = work[(k == 0 ? 0 : N - k) * Cfg::W + c];
+          const C sk = {zk.x + zn.x, zk.y - zn.y}, dk = {zk.x - zn.x, zk.y + zn.y};
+          const C ck = __ldg(tw3 + k);
+          work[k * Cfg::W + c] = C{ck.x * sk.x - ck.y * sk.y, ck.x * dk.y + ck.y * dk.x};
+          if (k > 0 && 2 * k != N) {
+            const C cl = __ldg(tw3 + N - k);
+            const C sl = {sk.x, -sk.y}, dl = {-dk.x, dk.y};
+            work[(N - k) * Cfg::W + c] = C{cl.x * sl.x - cl.y * sl.y, cl.x * dl.y + cl.y * dl.x};
+          }
+        }
+      }
+    }
     if constexpr (TST) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
       __syncthreads();

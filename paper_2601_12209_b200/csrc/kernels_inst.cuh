@@ -26,6 +26,16 @@ KernelInfo make_strided_dct() {
   k.per_cta = Cfg::W;
   k.smem = (size_t)Cfg::SMEM_ELEMS * sizeof(Real) * 2;
   k.twlen = sched_twlen(Cfg::S);
+  using TC = TmaCfg<Real, N>;
+  if constexpr (TC::OK) {  // TMA-staged variant, TMA stores only (unsegmented outputs)
+    k.tma_fn = k.tma_st_fn = k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, false, DIR>;
+    k.tma_st_only = true;
+    k.tma_threads = TC::THREADS;
+    k.tma_w = TC::W;
+    k.tma_boxr = TC::BOXR;
+    k.tma_maxr = TC::MAXR;
+    k.tma_smem = TC::SMEM;
+  }
   return k;
 }
 template <typename Real, int N, int DIR>

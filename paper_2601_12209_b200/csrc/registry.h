@@ -24,6 +24,7 @@ struct KernelInfo {
   const void* tma_st1_fn = nullptr;  // same, the work-buffer flow (default; tma_st_fn = OM 3, opt-in)
   const void* tma_bk_fn = nullptr;  // same, with bulk-copy stores (column-blocked segmented output)
   const void* tma_st_spec_fn = nullptr;  // TMA stores + Poisson multiplier (forward only)
+  bool tma_st_only = false;              // the TMA variant exists only with TMA stores (R2R)
   // two-warp-group variant (preferred when it fits): in-place padded stage buffers
   const void* tma2_fn = nullptr;
   const void* tma2_st_fn = nullptr;
