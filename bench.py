@@ -248,10 +248,12 @@ def main():
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = dfft.kernel_launches()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
     ev1.record(stream)
+    n_launch = dfft.kernel_launches() - n_launch0
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
@@ -320,7 +322,7 @@ def main():
     breakdown.update({f"inv_{k}": v[0] / args.steps for k, v in pi.items() if v[1]})
     launches_per_step = sum(v[1] for v in pf.values() if v[1]) + sum(v[1] for v in pi.values() if v[1])
     exch = sum(pf[k][1] + pi[k][1] for k in ("exchange_1", "exchange_2"))
-    gpu_launches = (launches_per_step - exch)  # our FFT kernels only (NCCL kernels excluded)
+    gpu_launches = n_launch  # our kernels (FFT stages + flag signals) in the timed region, counted by libdfft
 
     # --- e2e: host pinned input -> device -> fwd+inv -> host, through the public API
     e2e = None

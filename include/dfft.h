@@ -201,6 +201,11 @@ dfft_status_t dfft_plan_set_profiling(dfft_plan_t plan, int on);
 dfft_status_t dfft_plan_phase_times(dfft_plan_t plan, double ms[5], long long launches[5], int reset);
 dfft_status_t dfft_plan_stage_bytes(dfft_plan_t plan, double bytes[5]);
 
+/* Number of kernels this library has launched in the process so far (FFT stages and flag
+ * signals; NCCL's own kernels and copy-engine transfers are not kernels of ours).  Monotonic;
+ * the bench reads it around its timed region. */
+long long dfft_kernel_launches(void);
+
 /* Synchronises the plan's internal streams, then frees everything the plan owns. */
 dfft_status_t dfft_destroy(dfft_plan_t plan);
 

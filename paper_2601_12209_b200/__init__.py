@@ -34,7 +34,7 @@ EXPORTS = [
     "dfft_comm_init_sim", "dfft_comm_destroy", "dfft_plan_create", "dfft_plan_box", "dfft_plan_box_rank",
     "dfft_plan_bytes", "dfft_decomp_box", "dfft_plan_chunks", "dfft_execute", "dfft_execute_host", "dfft_execute_sim",
     "dfft_destroy", "dfft_fft1d", "dfft_plan_set_profiling", "dfft_plan_phase_times", "dfft_plan_stage_bytes",
-    "dfft_plan_set_poisson",
+    "dfft_plan_set_poisson", "dfft_kernel_launches",
 ]
 PHASES = ["stage_A", "exchange_1", "stage_B", "exchange_2", "stage_C"]
 
@@ -60,6 +60,8 @@ def lib():
             raise DfftError(f"{LIB_PATH} not built; run __graft_entry__.build()")
         L = ctypes.CDLL(LIB_PATH)
         L.dfft_version.restype = _int
+        if hasattr(L, "dfft_kernel_launches"):
+            L.dfft_kernel_launches.restype = ctypes.c_longlong
         L.dfft_status_string.restype = ctypes.c_char_p
         L.dfft_status_string.argtypes = [_int]
         L.dfft_last_error.restype = ctypes.c_char_p
@@ -87,7 +89,7 @@ def lib():
         L.dfft_plan_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), _int]
         L.dfft_plan_stage_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
         for name in EXPORTS:
-            if name not in ("dfft_version", "dfft_status_string", "dfft_last_error") and hasattr(L, name):
+            if name not in ("dfft_version", "dfft_status_string", "dfft_last_error", "dfft_kernel_launches") and hasattr(L, name):
                 getattr(L, name).restype = _int  # (every symbol exists in the in-tree build: test_abi)
         _lib = L
     return _lib
@@ -306,3 +308,8 @@ def fft1d(x, y, sign: int = FORWARD, stream=None):
     _check(lib().dfft_fft1d(_vp(x.data_ptr()), _vp(y.data_ptr()), n, x.numel() // n, int(f64), sign,
                             _stream_ptr(stream, x.device)), "dfft_fft1d")
     return y
+
+
+def kernel_launches() -> int:
+    """Kernels libdfft has launched in this process so far (dfft_kernel_launches)."""
+    return int(lib().dfft_kernel_launches())

@@ -21,6 +21,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -140,6 +141,7 @@ dfft_status_t get_twiddles(int n, bool f64, int dir, int dev, const void** out, 
   return DFFT_SUCCESS;
 }
 
+std::atomic<long long> g_launches{0};  // library kernel launches, process-wide (dfft_kernel_launches)
 bool g_use_tma = getenv("DFFT_NO_TMA") == nullptr;  // env switch for the A/B ablation
 CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
                                      : getenv("DFFT_TMA_PROMO128") ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
@@ -1336,6 +1338,7 @@ void* resolve(const Ref& r, const Ctx& c) {
 
 dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
   if (s.empty) return DFFT_SUCCESS;
+  g_launches.fetch_add(1, std::memory_order_relaxed);  // exactly one kernel per stage launch
   PassArgs a = s.a;
   a.in.base = resolve(s.in, c);
   a.out.base = resolve(s.out, c);
@@ -1527,6 +1530,7 @@ dfft_status_t p2p_signal(dfft_plan_t pl, int arr, int e, int k, const std::vecto
                flag_index(pl, arr, e, k, me);
   void* args[] = {&a};
   CU(cudaLaunchKernel((const void*)dfft_signal_kernel, dim3(1), dim3(32), args, 0, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return DFFT_SUCCESS;
 }
 
@@ -1836,6 +1840,8 @@ dfft_status_t apply_sm_caps(dfft_plan_t pl, RankPlan& rp) {
 extern "C" {
 
 int dfft_version(void) { return DFFT_VERSION; }
+
+long long dfft_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* dfft_status_string(dfft_status_t s) {
   switch (s) {
