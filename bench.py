@@ -134,6 +134,7 @@ def oracle_sample(shape_full, seconds_budget=20.0):
     import oracle
 
     oracle.build()
+    oracle.set_threads(len(os.sched_getaffinity(0)))  # every host core (torchrun sets OMP_NUM_THREADS=1)
     edge = min(512, min(shape_full))
     shp = (edge, edge, edge)
     a = oracle.gen_complex(1, shp)
@@ -160,6 +161,7 @@ def run_reference(args):
     import oracle
 
     oracle.build()
+    oracle.set_threads(len(os.sched_getaffinity(0)))  # every host core (torchrun sets OMP_NUM_THREADS=1)
     edge = 512 if (args.steps + args.warmup) <= 20 else 256
     edge = min(edge, min(shape))
     shp = (edge, edge, edge)

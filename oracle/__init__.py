@@ -55,6 +55,7 @@ def _load():
         lib.or_poisson3d.argtypes = [_dp, _i64, _i64, _i64, _d, _d, _d, _dp]
         lib.or_laplacian7.argtypes = [_dp, _i64, _i64, _i64, _d, _d, _d, _dp]
         lib.or_dct3d.argtypes = [_dp, _i64, _i64, _i64, _int]
+        lib.or_set_threads.argtypes = [_int]
         lib.or_dft3d_bin_seeded.argtypes = [_u64, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64, _dp]
         lib.or_err_sums.argtypes = [_dp, _dp, _i64, _dp]
         lib.or_num_threads.restype = _int
@@ -73,6 +74,11 @@ def _i3(v):
 
 def num_threads() -> int:
     return int(_load().or_num_threads())
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle (timing legs use every host core; torchrun sets 1 per rank)."""
+    _load().or_set_threads(int(n))
 
 
 # ----------------------------------------------------------------- generator

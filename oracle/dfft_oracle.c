@@ -572,3 +572,12 @@ int or_num_threads(void) {
     return 1;
 #endif
 }
+
+/* Thread count for the timing legs (torchrun sets OMP_NUM_THREADS=1 per rank). */
+void or_set_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
