@@ -572,9 +572,11 @@ __host__ __device__ constexpr int dct_perm(int n, int L) { return n < L / 2 ? 2 
 // C2R merge.  MODE 3 loads the permuted reals; MODE 4 loads X and builds the merged spectrum.
 // The line is staged through shared memory in its natural order (coalesced 16 B accesses on the
 // global side); the permutation and the X_k / X_{L-k} pairing then read shared memory.
-// (forward: the permuted reals are read straight from global memory — staging the line through
-// shared memory measured slower for MODE 3, 1.59 vs 2.5 ms at 768x768x384 f64 — while the
-// inverse stages its input and output, 2.5 -> 2.1 ms)
+// The inverse stages its line through shared memory with coalesced 16 B global accesses and does
+// Makhoul's permutation on the shared-memory side with unit-stride (conflict-free) indices:
+// complex element q of the line holds (x_{2q}, x_{2q+1}) = (v_q, v_{L-1-q}).
+// (the forward reads its permuted reals straight from global memory: staging its line the same
+// way measured slower, 1.58 vs 2.36 ms at 768x768x384 f64; the inverse gains, 2.07 -> 1.98 ms)
 template <typename C, int N> struct DctXFwdIO : GIO<C, true> {
   C* zb;  // the last pass's outputs
   __device__ __forceinline__ C load(int t) const {
@@ -588,7 +590,7 @@ template <typename C, int N> struct DctXInvIO : GIO<C, true> {
   const C* tw2;  // exp(+2πi t / 2N)
   const C* tw3;  // exp(+iπk / (4N)), k < 2N
   const R* xr;   // the staged input line (2N reals)
-  R* yr;         // the output line (2N reals, permuted scatter), written back coalesced
+  C* zb;         // the last pass's outputs z_t = (v_{2t}, v_{2t+1}) (times N)
   __device__ __forceinline__ C vk(int k) const {  // V_k = ½·conj(c_k)·(X_k − i·X_{L−k}), k ≤ N
     const R xk = xr[k], xl = k == 0 ? R(0) : xr[2 * N - k];
     const C c = __ldg(tw3 + k);
@@ -603,10 +605,7 @@ template <typename C, int N> struct DctXInvIO : GIO<C, true> {
     const C o = cmul(d, w);
     return {e.x - o.y, e.y + o.x};  // E + i·O  (IDFT_N of it = v_{2m} + i·v_{2m+1}, times N)
   }
-  __device__ __forceinline__ void store(int t, C v) const {
-    yr[dct_perm(2 * t, 2 * N)] = v.x;
-    yr[dct_perm(2 * t + 1, 2 * N)] = v.y;
-  }
+  __device__ __forceinline__ void store(int t, C v) const { zb[t] = v; }
 };
 
 template <typename Real, int N, int DIR, int MODE, bool TB = false>
@@ -685,14 +684,16 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
     io.tw3 = reinterpret_cast<const C*>(a.tw3);
     C* zb = smem + li * Cfg::LS;
     io.xr = reinterpret_cast<const R*>(zb);
-    io.yr = reinterpret_cast<R*>(zb);
+    io.zb = zb;
     if (active)
       for (int t = j; t < N; t += Cfg::S.T) zb[t] = io.GIO<C, true>::load(t);
     __syncthreads();
     stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
     __syncthreads();
-    if (active)
-      for (int t = j; t < N; t += Cfg::S.T) io.GIO<C, true>::store(t, zb[t]);
+    if (active) {  // output element q = (x_{2q}, x_{2q+1}) = (v_q, v_{2N-1-q}); coalesced stores
+      const R* vr = reinterpret_cast<const R*>(zb);
+      for (int q = j; q < N; q += Cfg::S.T) io.GIO<C, true>::store(q, C{vr[q], vr[2 * N - 1 - q]});
+    }
   }
 }
 
