@@ -107,3 +107,31 @@ def test_r2c_odd_nx_unsupported():
     with pytest.raises(dfft.DfftError) as ei:
         dfft.decomp_box((9, 8, 8), "pencil", (1, 1), "r2c_f64", -1, 0, 0)
     assert "(3)" in str(ei.value)
+
+
+@pytest.mark.parametrize("shape,decomp,grid", [((16, 12, 8), "pencil", (1, 1)), ((24, 16, 12), "pencil", (2, 4)),
+                                               ((48, 24, 12), "pencil", (5, 2)), ((48, 24, 12), "slab", (4, 1))])
+def test_r2r_boxes_are_real_and_split_in_pairs(shape, decomp, grid):
+    # R2R (reading R21): real boxes on both sides; the x split of D2/D3 is in pairs of reals
+    import numpy as np
+
+    P = grid[0] * grid[1]
+    for direction in (dfft.FORWARD, dfft.INVERSE):
+        for which in (0, 1):
+            cover = np.zeros(shape[::-1], dtype=np.int32)
+            for r in range(P):
+                lo, n = dfft.decomp_box(shape, decomp, grid, "r2r_f64", direction, r, which)
+                assert lo[0] % 2 == 0 and n[0] % 2 == 0
+                cover[lo[2]:lo[2] + n[2], lo[1]:lo[1] + n[1], lo[0]:lo[0] + n[0]] += 1
+            assert (cover == 1).all()
+
+
+@pytest.mark.parametrize("shape", [(9, 8, 8), (8, 9, 8), (8, 8, 6 + 1)])
+def test_r2r_odd_extents_unsupported(shape):
+    with pytest.raises(dfft.DfftError) as ei:
+        dfft.decomp_box(shape, "pencil", (1, 1), "r2r_f32", -1, 0, 0)
+    assert "(3)" in str(ei.value)
+
+
+def test_kernel_launch_counter_exported():
+    assert dfft.kernel_launches() >= 0
