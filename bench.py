@@ -372,7 +372,8 @@ def main():
                                    + ("Poisson solve (fwd + 1/λ fused + inv)" if args.poisson else "fwd+inv"),
                        "flop_convention": "2.5·N·log2N per real transform" if args.kind != "c2c" else "5·N·log2N per c2c",
                        "grid": list(shape), "proc_grid": list(grid), "chunks": fwd.chunks(),
-                       "exchange": args.exchange if world > 1 else "none",
+                       "exchange": ("fused stores into peer IPC windows (auto)" if args.exchange == "auto" else
+                                    args.exchange) if world > 1 else "none",
                        "overlap": not args.no_overlap,
                        "l2": f"inputs larger than L2 ({Nloc * es / 2**30:.2f} GiB per GPU)"
                              if Nloc * es > 2 * 126e6 else "inputs L2-resident (flagged)",
