@@ -37,7 +37,7 @@ def log(*a):
 def main():
     import faulthandler
 
-    faulthandler.dump_traceback_later(int(os.environ.get("MP_WATCHDOG", "240")), exit=True)
+    faulthandler.dump_traceback_later(int(os.environ.get("MP_WATCHDOG", "600")), exit=True)
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -176,6 +176,54 @@ def main():
                 for (_, _, a0), (_, _, a1) in zip(results[0][0], ys):
                     assert np.array_equal(a0, a1), ("schedule changed bits", decomp, grid, shape, prec)
             n_ok += 1
+        dist.barrier()
+    # the bench's launch configuration at full size (BASELINE configs[3], default transport and
+    # chunking): sampled bins vs the oracle's direct sums, round trip, Parseval
+    if os.environ.get("MP_FULL", "1") == "1":
+        shape, seed = (1024, 1024, 1024), 260112209 + 4
+        grid = {2: (1, 2), 4: (2, 2)}[P]
+        log("full size", shape, grid)
+        fwd = dfft.Plan(comm, shape, "pencil", grid, "c2c_f32", dfft.FORWARD)
+        inv = dfft.Plan(comm, shape, "pencil", grid, "c2c_f32", dfft.INVERSE)
+        lo, n = fwd.box(0)
+        x = fwd.alloc_in()
+        inputs.fill_box_cuda(x, seed, shape, lo, n, True)
+        y = fwd.alloc_out()
+        for _ in range(2):
+            fwd.execute(x, y)
+        torch.cuda.synchronize()
+        rng = np.random.default_rng(2)
+        ks = [(0, 0, 0), (1023, 1023, 1023), (511, 512, 3)] + [tuple(int(v) for v in rng.integers(0, 1024, 3))
+                                                                for _ in range(5)]
+        olo, on = fwd.box(1)
+        mine = []
+        for k in ks:
+            if all(olo[d] <= k[d] < olo[d] + on[d] for d in range(3)):
+                mine.append((k, complex(y[k[2] - olo[2], k[1] - olo[1], k[0] - olo[0]].item())))
+        got = [None] * P
+        dist.all_gather_object(got, mine)
+        z = inv.alloc_out()
+        inv.execute(y, z)
+        torch.cuda.synchronize()
+        sums = torch.tensor([(z - x).abs().double().pow(2).sum().item(), x.abs().double().pow(2).sum().item(),
+                             y.abs().double().pow(2).sum().item()], dtype=torch.float64, device="cuda")
+        dist.all_reduce(sums)
+        if rank == 0:
+            oracle.set_threads(len(os.sched_getaffinity(0)))  # torchrun sets OMP_NUM_THREADS=1
+            vals = dict(kv for part in got for kv in part)
+            assert len(vals) == len(ks), (len(vals), len(ks))
+            N = float(np.prod(shape))
+            err2 = sum(abs(vals[k] - oracle.dft3d_bin_seeded(seed, shape, k, f32=True)) ** 2 for k in ks)
+            rms_rel = np.sqrt(err2 / len(ks)) / np.sqrt(2 * N / 3)
+            assert rms_rel <= GATE["f32"], ("full-size bins", rms_rel)
+            d, sx, sX = sums.tolist()
+            assert np.sqrt(d / sx) <= GATE["f32"], ("full-size round trip", np.sqrt(d / sx))
+            assert abs(sX / (N * sx) - 1) < 1e-5, ("Parseval", sX / (N * sx))
+            n_ok += 1
+        fwd.destroy()
+        inv.destroy()
+        del x, y, z
+        torch.cuda.empty_cache()
         dist.barrier()
     if rank == 0:
         print(f"MP_OK {n_ok}", flush=True)
