@@ -211,6 +211,15 @@ def test_simulated_ranks_fused_store_chunked(oracle_mod, shape, decomp, grid, ch
     assert ef <= QUALITY[prec], ef
 
 
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,grid", [((480, 96, 48), (2, 2)), ((96, 720, 48), (1, 2)), ((48, 96, 840), (2, 4))])
+def test_simulated_ranks_fused_store_radix57(oracle_mod, shape, grid, prec):
+    # the paper's GPU shapes' lengths (radix 5/7, f1) through the multi-GPU default layouts
+    ef, er, _ = _run_sim(oracle_mod, shape, "pencil", grid, prec, 0, exchange="p2p")
+    assert ef <= GATE[prec] and er <= GATE[prec], (ef, er)
+    assert ef <= QUALITY[prec], ef
+
+
 def test_fused_store_bitwise_equals_nccl_layouts(oracle_mod):
     # same kernels and radix schedules, different exchange layouts => identical bits
     shape = (32, 24, 16)
