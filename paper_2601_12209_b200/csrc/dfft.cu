@@ -2011,8 +2011,12 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   const double local_bytes = (double)nxc * ny * nz / P * (f64 ? 16.0 : 8.0);
   // 1×P2 grids also pipeline the inverse (z-IFFT to the peers ‖ local y-IFFT, two streams):
   // 1x2 1024^3 c64 fwd+inv 14.6 -> 12.6 ms with K = 4 and the NVLink stage on 80 SMs
+  // (sweep: 4 chunks from 1 GiB per rank, 2 from 256 MiB — cfg5 2x2 2.63 -> 2.50 ms — else 1)
   if (p2p_mode && Kreq == 0)
-    K = ((bc_mode || (p1 == 1 && p2 > 1)) && local_bytes >= 256.0 * (1 << 20)) ? 4 : 1;
+    K = !(bc_mode || (p1 == 1 && p2 > 1)) ? 1
+        : local_bytes >= 1024.0 * (1 << 20) ? 4
+        : local_bytes >= 256.0 * (1 << 20)  ? 2
+                                             : 1;
   if (bc_mode) kmax = direction == DFFT_FORWARD ? nxc / p1 : nz / p2;
   K = std::max<long long>(1, std::min<long long>(K, kmax));
   if (P == 1) K = 1;  // nothing to overlap
