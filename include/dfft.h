@@ -46,11 +46,16 @@ typedef enum {
   DFFT_SUCCESS = 0,
   DFFT_ERR_INVALID_VALUE = 1,     /* bad argument: sizes <= 0, p1*p2 != nranks, null/misaligned ptr, in == out */
   DFFT_ERR_INFEASIBLE_DECOMP = 2, /* some rank would own an empty block in some layout */
-  DFFT_ERR_UNSUPPORTED = 3,       /* axis length with a prime factor outside {2,3,5,7}, > 4096, odd Nx for R2C */
+  DFFT_ERR_UNSUPPORTED = 3,       /* an FFT axis length the library has no kernel for (not one of the
+                                     lengths listed at dfft_plan_create), odd Nx for R2C, odd extents for R2R */
   DFFT_ERR_ALLOC = 4,             /* cudaMalloc failed */
   DFFT_ERR_CUDA = 5,              /* a CUDA runtime call failed (detail in dfft_last_error) */
-  DFFT_ERR_NCCL = 6,              /* an NCCL call failed or the communicator reported an async error */
-  DFFT_ERR_INTERNAL = 7
+  DFFT_ERR_NCCL = 6,              /* an NCCL call failed or the communicator reported an async error
+                                     (ncclCommGetAsyncError, checked at every execute of an NCCL plan) */
+  DFFT_ERR_INTERNAL = 7,
+  DFFT_ERR_PEER = 8               /* the plan has failed: an execute made no progress within the watchdog
+                                     timeout (a peer never signalled; its waits were released and the
+                                     results are invalid) or an enqueue failed part-way.  Destroy it. */
 } dfft_status_t;
 
 typedef enum { DFFT_SLAB = 1, DFFT_PENCIL = 2 } dfft_decomp_t;
@@ -70,26 +75,36 @@ typedef enum { DFFT_FORWARD = -1, DFFT_INVERSE = 1 } dfft_direction_t;
 
 /*
  * flags (bit field, 0 = defaults):
- *   bits 0-7  DFFT_FLAG_CHUNKS(k): pipeline chunk count K (0 = automatic).  The stage-1/2
- *             work and both exchanges are split into K chunks along the axis no exchange
- *             touches (z forward, x inverse) and run as a two-stream pipeline (P:115-126,
- *             Fig. 1 "progressive per-chunk pipelining"; Alg. 2 phases 3/5).
- *   DFFT_FLAG_NO_OVERLAP: one stream, each exchange completes before the next stage starts
- *             (the "SimpleMPIFFT" static-barrier ablation of P:438).  Results are bitwise
+ *   bits 0-7  DFFT_FLAG_CHUNKS(k): pipeline chunk count K (0 = automatic).  The work and the
+ *             exchanges are split into K chunks and run as a two-stream pipeline (P:115-126,
+ *             Fig. 1 "progressive per-chunk pipelining"; Alg. 2 phases 3/5): NCCL / CE plans chunk
+ *             stages A, B and both exchanges along the axis no exchange touches (z forward, x
+ *             inverse); fused-store plans with both exchanges remote (p1 > 1 and p2 > 1, and the
+ *             1×P2 forward) run stage A whole and chunk stages B and C (x forward, z inverse) so
+ *             the local C(k) overlaps the NVLink-bound B(k+1).  Automatic K: NCCL 4, CE 8, fused
+ *             stores 4 from 1 GiB per rank, 2 from 256 MiB, else 1.
+ *   DFFT_FLAG_NO_OVERLAP: the same steps on the caller's stream alone, each exchange completing
+ *             before the next stage starts and every stage on the whole GPU (the "SimpleMPIFFT"
+ *             static-barrier ablation of P:438), for every transport.  Results are bitwise
  *             identical to the pipelined schedule.
  *   Exchange transport for P > 1 (same kernels and bitwise-identical results in every mode).
  *   Every rank's workspace is a CUDA IPC window exchanged at plan creation; flag words in the
- *   windows (system-scope release stores, cuStreamWaitValue32) order producer and consumer per
- *   chunk, and consumer -> producer for buffer reuse across executes.
- *     DFFT_FLAG_FUSED_STORE: each FFT epilogue stores its off-rank elements straight into the
- *               peers' windows over NVLink (pack + send + unpack fused into the FFT's stores).
+ *   windows order producer and consumer per chunk (READY) and consumer -> producer for buffer
+ *   reuse across executes (DONE): a flag kernel resets the words this rank waited on and then
+ *   publishes its own with system-scope release stores; waits are cuStreamWaitValue32 for the
+ *   constant value 1, so every schedule can be captured in a CUDA graph and replayed.
+ *     DFFT_FLAG_FUSED_STORE (the default for P > 1): each FFT epilogue stores its off-rank
+ *               elements straight into the peers' windows over NVLink (pack + send + unpack
+ *               fused into the FFT's stores; bulk copies per tile from the strided stages).
  *     DFFT_FLAG_CE: the FFT epilogue packs each off-rank block into a local send block and the
  *               comm stream's copy engine moves it into the receiver's window, K chunks
  *               pipelined against the FFTs (no SM time on transfers).
  *     DFFT_FLAG_HYBRID: fused stores for the forward x-FFT (long x-runs), CE elsewhere.
- *     default: fused stores when p1 > 1, CE with 8 chunks for a 1×P2 grid (measured best).
  *     DFFT_FLAG_NCCL: grouped ncclSend/ncclRecv of the send blocks (baseline/ablation).
- *   Env DFFT_EXCHANGE=ce|p2p|nccl overrides.
+ *   Env overrides (read at plan creation, real communicators only; every rank must resolve the
+ *   same plan, which plan creation checks): DFFT_EXCHANGE=p2p|ce|hybrid|nccl, DFFT_NO_BC=1 (no
+ *   B→C pipeline), DFFT_NO_BC_1XP=1 (no B→C pipeline on 1×P2 forwards), DFFT_NVL_SMS=n (SMs of
+ *   the NVLink-bound stage of a pipelined pair, default 80).
  */
 #define DFFT_FLAG_CHUNKS(k) ((uint64_t)((k) & 0xff))
 #define DFFT_FLAG_NO_OVERLAP ((uint64_t)1 << 8)
@@ -122,6 +137,9 @@ dfft_status_t dfft_comm_init_sim(dfft_comm_t* comm, int nranks, int cuda_device)
 dfft_status_t dfft_comm_destroy(dfft_comm_t comm);
 
 /* ------------------------------------------------------------------ plans
+ * Supported FFT axis lengths (each of nx — nx/2 for R2C / R2R — ny, nz): 2^a for 2 ≤ 2^a ≤ 4096,
+ * 3·2^a for 3 ≤ 3·2^a ≤ 3072, 5, 7, and the paper's GPU shapes 480, 720, 840; any other
+ * length returns DFFT_ERR_UNSUPPORTED.
  * Collective over comm (every rank calls it with the same arguments).  Builds the stage
  * geometry, twiddle tables, per-stage address tables, work buffers, sub-communicators
  * (row = ranks with the same j, column = same i), streams and events once; execution
@@ -155,11 +173,15 @@ dfft_status_t dfft_plan_chunks(dfft_plan_t plan, int* chunks);
  * `out` its output box (forward: D3; inverse: D1), both device pointers on the plan's
  * GPU, 16-byte aligned, dense as described above, non-overlapping; `in` is never written.
  * Stream-ordered and asynchronous: work is enqueued after everything already on `stream`
- * and `stream` waits for its completion; no host synchronisation.  Single-rank plans (and
- * NCCL-transport plans) are capturable in a CUDA graph; plans with the IPC-window transports
- * (fused stores / copy engine, the P > 1 default) are not: their flag words carry a per-execute
- * epoch fixed at enqueue time, so a replayed graph would wait on stale values.
- * Collective: all ranks execute matching plans in the same order.
+ * and `stream` waits for its completion; no host synchronisation.  Capturable in a CUDA graph
+ * for every transport (the IPC-window flag protocol waits for constant values; NCCL plans follow
+ * NCCL's own capture rules).
+ * Collective: all ranks execute matching plans in the same order.  A multi-rank execute that
+ * makes no progress for the watchdog timeout (dfft_set_timeout_ms, env DFFT_TIMEOUT_MS, default
+ * 120 s) is reported on stderr, its waits are released so the streams drain, and the plan fails:
+ * this and later calls return DFFT_ERR_PEER.  If an enqueue fails part-way, the remaining flag
+ * waits and signals are still issued (peers stay in step), the error is returned and the plan
+ * fails likewise.
  * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  */
 dfft_status_t dfft_execute(dfft_plan_t plan, const void* in, void* out, void* stream);
@@ -171,7 +193,29 @@ dfft_status_t dfft_execute(dfft_plan_t plan, const void* in, void* out, void* st
  */
 dfft_status_t dfft_execute_host(dfft_plan_t plan, const void* in_host, void* out_host, void* stream);
 
-/* Simulated comm only: ins[r] / outs[r] are rank r's device boxes, r < nranks. */
+/*
+ * End to end through a chain of plans (e.g. forward then inverse, or the Poisson solve's forward
+ * with the 1/λ multiplier then the C2R inverse): host `in` → device → plans[0] → … →
+ * plans[nplans-1] → host `out`, with the intermediate results kept on the device.  Plan q's output
+ * box must be plan q+1's input box (same bytes).  The host→device copy runs on a plan-owned copy
+ * stream and the device→host copy on another, with double-buffered device staging (owned by
+ * plans[0], reused while the chain stays the same), so with async != 0 the host→device copy of the
+ * next call overlaps this call's transforms and device→host copy.  `stream` completes when `out`
+ * holds the result.  async == 0: returns after synchronising `stream` (any host memory); async != 0:
+ * returns after enqueueing — both host buffers must then be page-locked (else INVALID_VALUE) and
+ * stay untouched until `stream` completes.  Collective like dfft_execute.
+ */
+dfft_status_t dfft_execute_host_chain(const dfft_plan_t* plans, int nplans, const void* in_host, void* out_host,
+                                      void* stream, int async);
+
+/* Simulated comm only: ins[r] / outs[r] are rank r's device boxes, r < nranks.
+ * Plans with an IPC-window transport (DFFT_FLAG_FUSED_STORE / _CE / _HYBRID on a simulated comm)
+ * run every rank's own execute schedule as a real rank does — its stream pair, the flag words in
+ * its workspace (which stands in for its IPC window), chunks, the B→C pipeline and SM caps —
+ * issued interleaved, so all ranks run concurrently on the one GPU; ins[r] == NULL means rank r
+ * does not take part (a failed peer: the others wait until the watchdog releases them).
+ * Otherwise (NCCL layouts) every rank's stages run in stream order with device copies of the
+ * blocks NCCL would move. */
 dfft_status_t dfft_execute_sim(dfft_plan_t plan, const void* const* ins, void* const* outs, void* stream);
 
 /*
@@ -200,6 +244,22 @@ dfft_status_t dfft_plan_set_poisson(dfft_plan_t plan, double dx, double dy, doub
 dfft_status_t dfft_plan_set_profiling(dfft_plan_t plan, int on);
 dfft_status_t dfft_plan_phase_times(dfft_plan_t plan, double ms[5], long long launches[5], int reset);
 dfft_status_t dfft_plan_stage_bytes(dfft_plan_t plan, double bytes[5]);
+/* Timeline of the profiled executes (Fig. 9 per-chunk analog): one span per stage launch or
+ * exchange step, on stream 0 (compute X) or 1 (Y), with its chunk and rank, in milliseconds
+ * relative to the origin event its execute recorded on the caller's stream (exec numbers count
+ * the executes since the last read).  Synchronises.  cap = 0 returns the count in *n; otherwise up
+ * to cap spans are copied and removed (dfft_plan_phase_times with reset != 0 discards them). */
+typedef struct {
+  int phase, stream, chunk, rank, exec;
+  double t0_ms, t1_ms;
+} dfft_span_t;
+dfft_status_t dfft_plan_timeline(dfft_plan_t plan, dfft_span_t* spans, int cap, int* n);
+
+/* Watchdog timeout for multi-rank executes, process-wide (ms > 0). */
+dfft_status_t dfft_set_timeout_ms(long long ms);
+/* DFFT_SUCCESS while the plan is usable; DFFT_ERR_PEER once it failed; DFFT_ERR_NCCL if its NCCL
+ * communicator reports an asynchronous error. */
+dfft_status_t dfft_plan_status(dfft_plan_t plan);
 
 /* Number of kernels this library has launched in the process so far (FFT stages and flag
  * signals; NCCL's own kernels and copy-engine transfers are not kernels of ours).  Monotonic;

@@ -34,7 +34,8 @@ EXPORTS = [
     "dfft_comm_init_sim", "dfft_comm_destroy", "dfft_plan_create", "dfft_plan_box", "dfft_plan_box_rank",
     "dfft_plan_bytes", "dfft_decomp_box", "dfft_plan_chunks", "dfft_execute", "dfft_execute_host", "dfft_execute_sim",
     "dfft_destroy", "dfft_fft1d", "dfft_plan_set_profiling", "dfft_plan_phase_times", "dfft_plan_stage_bytes",
-    "dfft_plan_set_poisson", "dfft_kernel_launches",
+    "dfft_plan_set_poisson", "dfft_kernel_launches", "dfft_plan_timeline", "dfft_set_timeout_ms", "dfft_plan_status",
+    "dfft_execute_host_chain",
 ]
 PHASES = ["stage_A", "exchange_1", "stage_B", "exchange_2", "stage_C"]
 
@@ -45,7 +46,16 @@ _int = ctypes.c_int
 
 
 class DfftError(RuntimeError):
-    pass
+    def __init__(self, msg, status=None):
+        super().__init__(msg)
+        self.status = status
+
+
+class Span(ctypes.Structure):
+    """dfft_span_t: one stage launch / exchange step of a profiled execute (times in ms relative
+    to its execute's origin event)."""
+    _fields_ = [("phase", ctypes.c_int), ("stream", ctypes.c_int), ("chunk", ctypes.c_int), ("rank", ctypes.c_int),
+                ("exec", ctypes.c_int), ("t0_ms", ctypes.c_double), ("t1_ms", ctypes.c_double)]
 
 
 def flag_chunks(k: int) -> int:
@@ -80,6 +90,7 @@ def lib():
         L.dfft_plan_chunks.argtypes = [_vp, ctypes.POINTER(_int)]
         L.dfft_execute.argtypes = [_vp, _vp, _vp, _vp]
         L.dfft_execute_host.argtypes = [_vp, _vp, _vp, _vp]
+        L.dfft_execute_host_chain.argtypes = [ctypes.POINTER(_vp), _int, _vp, _vp, _vp, _int]
         L.dfft_execute_sim.argtypes = [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]
         L.dfft_destroy.argtypes = [_vp]
         L.dfft_fft1d.argtypes = [_vp, _vp, _i64, _i64, _int, _int, _vp]
@@ -88,6 +99,9 @@ def lib():
             L.dfft_plan_set_poisson.argtypes = [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double]
         L.dfft_plan_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), _int]
         L.dfft_plan_stage_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
+        L.dfft_plan_timeline.argtypes = [_vp, ctypes.POINTER(Span), _int, ctypes.POINTER(_int)]
+        L.dfft_set_timeout_ms.argtypes = [ctypes.c_longlong]
+        L.dfft_plan_status.argtypes = [_vp]
         for name in EXPORTS:
             if name not in ("dfft_version", "dfft_status_string", "dfft_last_error", "dfft_kernel_launches") and hasattr(L, name):
                 getattr(L, name).restype = _int  # (every symbol exists in the in-tree build: test_abi)
@@ -98,7 +112,7 @@ def lib():
 def _check(rc: int, what: str):
     if rc != 0:
         L = lib()
-        raise DfftError(f"{what}: {L.dfft_status_string(rc).decode()} ({rc}): {L.dfft_last_error().decode()}")
+        raise DfftError(f"{what}: {L.dfft_status_string(rc).decode()} ({rc}): {L.dfft_last_error().decode()}", rc)
 
 
 def _stream_ptr(stream, device):
@@ -245,23 +259,28 @@ class Plan:
         """End-to-end: host buffers (numpy arrays or pinned CPU tensors) in and out; synchronises."""
         import torch
 
-        def ptr(a):
-            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
         dev = torch.device("cuda", self.comm.device)
-        _check(lib().dfft_execute_host(self.h, _vp(ptr(x_host)), _vp(ptr(y_host)), _stream_ptr(stream, dev)),
+        _check(lib().dfft_execute_host(self.h, _vp(_host_ptr(x_host)), _vp(_host_ptr(y_host)), _stream_ptr(stream, dev)),
                "dfft_execute_host")
         return y_host
 
     def execute_sim(self, xs, ys, stream=None):
-        """Simulated comm: xs[r], ys[r] are rank r's boxes."""
+        """Simulated comm: xs[r], ys[r] are rank r's boxes (xs[r] None: rank r does not take part —
+        a failed peer, IPC-window plans only)."""
         P = self.comm.nranks
         for r in range(P):
-            self._check_tensor(xs[r], 0, r)
-            self._check_tensor(ys[r], 1, r)
-        ins = (_vp * P)(*[x.data_ptr() for x in xs])
-        outs = (_vp * P)(*[y.data_ptr() for y in ys])
-        _check(lib().dfft_execute_sim(self.h, ins, outs, _stream_ptr(stream, xs[0].device)), "dfft_execute_sim")
+            if xs[r] is not None:
+                self._check_tensor(xs[r], 0, r)
+                self._check_tensor(ys[r], 1, r)
+        ins = (_vp * P)(*[None if x is None else x.data_ptr() for x in xs])
+        outs = (_vp * P)(*[None if y is None else y.data_ptr() for y in ys])
+        dev = next(x for x in xs if x is not None).device
+        _check(lib().dfft_execute_sim(self.h, ins, outs, _stream_ptr(stream, dev)), "dfft_execute_sim")
         return ys
+
+    def status(self) -> int:
+        """0 while usable; DFFT_ERR_PEER (8) once the plan failed (dfft_plan_status)."""
+        return int(lib().dfft_plan_status(self.h))
 
     # periodic Poisson solve (fused spectral divide; forward plans) ------------------
     def set_poisson(self, spacing=(1.0, 1.0, 1.0)):
@@ -280,6 +299,17 @@ class Plan:
         ms, n = (ctypes.c_double * 5)(), (ctypes.c_longlong * 5)()
         _check(lib().dfft_plan_phase_times(self.h, ms, n, int(reset)), "dfft_plan_phase_times")
         return {PHASES[q]: (ms[q], n[q]) for q in range(5)}
+
+    def timeline(self):
+        """Spans of the profiled executes since the last read: list of dicts (dfft_plan_timeline)."""
+        n = _int()
+        _check(lib().dfft_plan_timeline(self.h, None, 0, ctypes.byref(n)), "dfft_plan_timeline")
+        if n.value == 0:
+            return []
+        buf = (Span * n.value)()
+        _check(lib().dfft_plan_timeline(self.h, buf, n.value, ctypes.byref(n)), "dfft_plan_timeline")
+        return [{"phase": PHASES[s.phase], "stream": s.stream, "chunk": s.chunk, "rank": s.rank, "exec": s.exec,
+                 "t0_ms": s.t0_ms, "t1_ms": s.t1_ms} for s in buf[:n.value]]
 
     def stage_bytes(self):
         b = (ctypes.c_double * 5)()
@@ -308,6 +338,29 @@ def fft1d(x, y, sign: int = FORWARD, stream=None):
     _check(lib().dfft_fft1d(_vp(x.data_ptr()), _vp(y.data_ptr()), n, x.numel() // n, int(f64), sign,
                             _stream_ptr(stream, x.device)), "dfft_fft1d")
     return y
+
+
+def _host_ptr(a):
+    import torch
+
+    return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+
+
+def execute_host_chain(plans, x_host, y_host, stream=None, async_: bool = False):
+    """Host x -> plans[0] -> ... -> plans[-1] -> host y (dfft_execute_host_chain).  async_: return
+    after enqueueing (pinned host buffers; the stream completes when y holds the result)."""
+    import torch
+
+    hs = (_vp * len(plans))(*[p.h.value for p in plans])
+    dev = torch.device("cuda", plans[0].comm.device)
+    _check(lib().dfft_execute_host_chain(hs, len(plans), _vp(_host_ptr(x_host)), _vp(_host_ptr(y_host)),
+                                         _stream_ptr(stream, dev), int(bool(async_))), "dfft_execute_host_chain")
+    return y_host
+
+
+def set_timeout_ms(ms: int) -> None:
+    """Watchdog timeout of multi-rank executes (process-wide, dfft_set_timeout_ms)."""
+    _check(lib().dfft_set_timeout_ms(int(ms)), "dfft_set_timeout_ms")
 
 
 def kernel_launches() -> int:

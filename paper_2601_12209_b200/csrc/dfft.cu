@@ -22,9 +22,12 @@
 #include <cstdio>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <map>
+#include <numeric>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dfft.h"
@@ -147,11 +150,7 @@ CUtensorMapL2promotion g_tma_promo = getenv("DFFT_TMA_PROMO256") ? CU_TENSOR_MAP
                                      : getenv("DFFT_TMA_PROMO128") ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                                                    : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 bool g_tma_store = getenv("DFFT_NO_TMA_STORE") == nullptr;
-bool g_use_tma2 = getenv("DFFT_TMA2") != nullptr;  // two-group variant: correct, not faster
 bool g_use_bulk = getenv("DFFT_NO_BULK") == nullptr;  // bulk-copy epilogue for blocked segmented outputs
-// TMA-store kernels: the work-buffer flow (OM 1) is the default; the stage-as-output flow (OM 3,
-// two barriers per tile but a one-tile prefetch distance) measured 3-10 % slower
-bool g_tst_work = getenv("DFFT_TST_STAGEOUT") == nullptr;
 
 // R2C/C2R split twiddles: w^k = exp(dir·2πi·k/(2N)), k ∈ [0, N), long double once each.
 dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void** out) {
@@ -226,16 +225,11 @@ dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
   }
   if (k->tma_fn && k->tma_smem > 48 * 1024) {
     CU(cudaFuncSetAttribute(k->tma_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
-    CU(cudaFuncSetAttribute(k->tma_st_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     if (k->tma_bk_fn) CU(cudaFuncSetAttribute(k->tma_bk_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     if (k->tma_st1_fn)
       CU(cudaFuncSetAttribute(k->tma_st1_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
     if (k->tma_st_spec_fn)
       CU(cudaFuncSetAttribute(k->tma_st_spec_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
-  }
-  if (k->tma2_fn && k->tma2_smem > 48 * 1024) {
-    CU(cudaFuncSetAttribute(k->tma2_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma2_smem));
-    CU(cudaFuncSetAttribute(k->tma2_st_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma2_smem));
   }
   return DFFT_SUCCESS;
 }
@@ -274,7 +268,7 @@ struct Stage {
   int tma_occ = 0;         // resident CTAs per SM of the TMA variant
   int sm_cap = 0;          // > 0: run the persistent variant on at most this many SMs (leaves the
                            // rest to a concurrently running HBM-bound stage)
-  int tma_variant = 0;     // 1 = single-group TMA kernel, 2 = two-group in-place kernel
+  int tma_variant = 0;     // 1 = the persistent TMA kernel is used
   const void* tw_tma = nullptr;  // twiddles of the TMA variant's radix schedule
   bool empty = false;
   // last forward stage: which global axis (0 x, 1 y, 2 z) its t / l0 / l1 run along and the
@@ -300,6 +294,35 @@ struct Exchange {
   bool empty() const { return sends.empty() && recvs.empty() && peers.empty(); }
 };
 
+// Flag words in every IPC window (CE / fused-store transports): READY[e][k][src] is set to 1 by
+// producer src once its chunk-k blocks of exchange e have landed in this window; DONE[e][k][dst]
+// is set to 1 by consumer dst once it has finished reading what this rank stored into dst's
+// window (so the producer may overwrite it).  Each side resets the word it waited on back to 0
+// (READY to 0, DONE to 0) in the same flag kernel that publishes its own signal, before the
+// signal: the values every wait compares against are the constant 1, so a schedule captured in a
+// CUDA graph replays correctly (DONE starts at 1 = "buffer free").
+enum FlagArr { kReady = 0, kDone = 1 };
+struct FlagRef {
+  int arr, e, k;
+  std::vector<int> ranks;  // wait / clear: the writers of the word (own window); set: the targets
+};
+
+// One step of a rank's execute.  The schedule is built once per plan (plan once,
+// execute many) and interpreted by run_schedule; every rank of a plan has a schedule of the same
+// length and shape, which is what lets simulated ranks issue them interleaved position by position.
+enum OpKind { kOpLaunch, kOpWait, kOpSignal, kOpRecord, kOpStreamWait, kOpNccl, kOpCeCopy };
+struct Op {
+  int kind = kOpLaunch;
+  int s = 0;       // stream: 0 = X (compute), 1 = Y (second compute / comm)
+  int phase = 0;   // profiling phase (0 A, 1 E1, 2 B, 3 E2, 4 C)
+  int chunk = 0;
+  const Stage* st = nullptr;       // kOpLaunch
+  const Exchange* x = nullptr;     // kOpNccl / kOpCeCopy
+  FlagRef wait;                    // kOpWait
+  std::vector<FlagRef> set, clr;   // kOpSignal
+  int ev = -1;                     // kOpRecord / kOpStreamWait: schedule event index
+};
+
 struct RankPlan {
   int rank = 0, i = 0, j = 0;
   int64_t in_lo[3], in_n[3], out_lo[3], out_n[3];
@@ -309,6 +332,11 @@ struct RankPlan {
   std::vector<Exchange> E1, E2;  // first / second exchange (each names its comm group)
   Stage C;
   std::vector<Stage> Cc;  // B→C pipelined plans (dfft_plan_s::bc): stage C per chunk, C unused
+  std::vector<Op> sched;  // the execute, as built by build_schedule
+  int nev = 0;            // schedule events
+  cudaStream_t sX = nullptr, sY = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
 };
 
 }  // namespace
@@ -329,11 +357,21 @@ struct dfft_plan_s {
   size_t es = 8;  // complex element bytes
   std::vector<RankPlan> ranks;
   ncclComm_t row = nullptr, col = nullptr;
-  cudaStream_t s_comp = nullptr, s_comm = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join_comp = nullptr, ev_join_comm = nullptr;
-  std::vector<cudaEvent_t> evA, evE1, evB, evE2;
-  void* stage_in = nullptr;  // dfft_execute_host staging buffers
-  void* stage_out = nullptr;
+  // dfft_execute_host / _chain staging (kept on the chain's first plan): double-buffered device
+  // copies of the host input and output, intermediate buffers between the chained plans, and
+  // the two copy streams that let one call's device->host copy run beside the next call's
+  // host->device copy
+  struct HostChain {
+    std::vector<dfft_plan_s*> plans;
+    void* in_dev[2] = {nullptr, nullptr};
+    void* out_dev[2] = {nullptr, nullptr};
+    std::vector<void*> mid;
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t in_ready[2] = {nullptr, nullptr}, in_free[2] = {nullptr, nullptr};
+    cudaEvent_t out_ready[2] = {nullptr, nullptr}, out_done[2] = {nullptr, nullptr};
+    unsigned long long calls = 0;
+  };
+  HostChain* host = nullptr;
   // P2P exchange (default for P > 1): every rank's workspace is an IPC window; the FFT epilogues
   // store straight into the peers' receive regions over NVLink; flags in the windows order it
   bool p2p = false;
@@ -346,15 +384,27 @@ struct dfft_plan_s {
   std::vector<void*> peer_ws;        // by global rank (own rank = own workspace), null if not a peer
   void* spec_tab = nullptr;          // dfft_plan_set_poisson: λ tables [nx | ny | nz] (Real)
   size_t flag_off = 0;               // byte offset of the flag block in every workspace
-  unsigned int epoch = 0;            // executes so far (flag values)
+  unsigned long long hash = 0;       // resolved plan state (cross-rank consistency check)
+  // failure state: an enqueue error, or the watchdog found an execute that did not complete (a
+  // peer never signalled) and released its waits; the plan refuses further executes
+  std::atomic<int> failed{0};
+  std::string fail_msg;
   // per-phase profiling (dfft_plan_set_profiling): timing events around every stage launch
-  // and exchange, on the stream that runs it; accumulated by dfft_plan_phase_times
+  // and exchange, on the stream that runs it; accumulated by dfft_plan_phase_times, and a
+  // timeline of spans relative to each execute's origin event (dfft_plan_timeline)
   bool prof = false;
-  std::vector<cudaEvent_t> prof_ev;                 // pool, pairs (start, stop)
-  std::vector<int> prof_phase;                      // phase id per recorded pair
-  size_t prof_used = 0;                             // pairs recorded since the last read
+  struct ProfRec {
+    int phase, stream, chunk, rank;
+    size_t exec;
+  };
+  std::vector<cudaEvent_t> prof_ev;  // pool, pairs (start, stop)
+  std::vector<ProfRec> prof_rec;     // one per recorded pair
+  size_t prof_used = 0;              // pairs recorded since the last read
+  std::vector<cudaEvent_t> prof_origin;  // one per execute since the last read
+  size_t prof_nexec = 0;
   double prof_ms[5] = {0, 0, 0, 0, 0};
   long long prof_n[5] = {0, 0, 0, 0, 0};
+  std::vector<dfft_span_t> prof_spans;  // resolved timeline spans not yet read
 };
 
 namespace {
@@ -504,30 +554,28 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   if (is_contig(family)) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
   else s.grid = ((L0 + s.k.per_cta - 1) / s.k.per_cta) * L1;
   if (s.grid >= (1LL << 31)) return fail(DFFT_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", s.grid);
-  if ((family == kStrided || family == kStridedDct) && (s.k.tma_fn || s.k.tma2_fn) && g_use_tma && !in_tab &&
+  if ((family == kStrided || family == kStridedDct) && s.k.tma_fn && g_use_tma && !in_tab &&
       tensor_map_encoder()) {
     const long long es = (long long)pl->es;
     bool ok = s.a.in.s0 == 1 && (s.a.in.tstride * es) % 16 == 0 && (L1 == 1 || (s.a.in.s1 * es) % 16 == 0) &&
               2 * L0 < (1LL << 32) && L1 < (1LL << 31);
     if (s.a.in.bw > 0) ok = ok && s.k.tma_fn && s.a.in.bw % s.k.tma_w == 0 && (s.a.in.mT * s.a.in.s1 * es) % 16 == 0;
     if (ok) {
-      const bool v2 = g_use_tma2 && s.k.tma2_fn;
-      const void* fn = v2 ? s.k.tma2_fn : s.k.tma_fn;
-      const int thr = v2 ? s.k.tma2_threads : s.k.tma_threads, w = v2 ? s.k.tma2_w : s.k.tma_w;
-      const size_t sm = v2 ? s.k.tma2_smem : s.k.tma_smem;
+      const void* fn = s.k.tma_fn;
+      const int thr = s.k.tma_threads, w = s.k.tma_w;
+      const size_t sm = s.k.tma_smem;
       int occ = 0, dev = pl->comm->device, sms = 0;
       CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, thr, sm));
       CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
       long long tiles = ((L0 + w - 1) / w) * L1;
       if (occ > 0) {
-        s.tma_variant = v2 ? 2 : 1;
+        s.tma_variant = 1;
         s.tma_grid = std::min<long long>(tiles, (long long)sms * occ);
         s.tma_occ = occ;
-        ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, v2 ? s.k.tma2_maxr : s.k.tma_maxr));
+        ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, s.k.tma_maxr));
       }
       if (getenv("DFFT_DEBUG"))
-        fprintf(stderr, "dfft: strided n=%d L0=%lld L1=%lld tma variant %d grid %lld (occ %d, tma2_fn %p)\n", n, L0, L1,
-                s.tma_variant, s.tma_grid, occ, s.k.tma2_fn);
+        fprintf(stderr, "dfft: strided n=%d L0=%lld L1=%lld tma grid %lld (occ %d)\n", n, L0, L1, s.tma_grid, occ);
     }
   }
   return DFFT_SUCCESS;
@@ -962,108 +1010,10 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
 
 // Single GPU (P = 1, any decomposition): no exchange, so the axis order is free (the 3D DFT is
 // separable).  Order the stages so no stage both reads and writes at a large stride:
-//   forward: x (in -> out, natural), z (out -> ws as [y][z][x]), y (ws -> out, natural)
-//   inverse: y (in -> out, natural), z (out -> ws as [y][z][x]), x (ws -> out, natural, ×1/N)
-// Single GPU, blocked middle layout (r01 session 2): every pass keeps both sides at a small
-// pitch, so a 1024-row column spans a few 2 MB pages instead of one page per row.
-//   forward: x (in -> L1 = [y][z][x] in `out`), z (L1 -> L2 = [xb][z][y][w] in ws),
-//            y (L2 -> `out`, natural)
-//   inverse: y (in -> L2), z (L2 -> L1), x (L1 -> `out`, natural, ×1/N)
-// L2 is column-blocked with the strided TMA tile width w (a y-pass tile = one contiguous
-// 64 KB block; the z-pass writes it with 4D TMA stores).  Needs the TMA kernel for ny and nz
-// with equal tile widths; otherwise build_single (the natural-layout order) is used.
-bool single_blocked_ok(dfft_plan_t pl, const Geo& g) {
-  // opt-in (measured slower): the z-pass's 4D TMA stores at a 64 KB pitch ran at
-  // 3.3 TB/s and the blocked y-pass reads did not beat the 8 MB-pitch ones (1024^3 c64:
-  // fwd+inv 25.1 vs 22.8 ms on the same B200)
-  if (!getenv("DFFT_SINGLE_BLOCKED") || !g_use_tma || !g_tma_store) return false;
-  KernelInfo ky, kz;
-  const int dir = pl->dir;
-  const bool oky = pl->f64 ? lookup_kernel_f64(kStrided, (int)g.ny, dir, &ky) : lookup_kernel_f32(kStrided, (int)g.ny, dir, &ky);
-  const bool okz = pl->f64 ? lookup_kernel_f64(kStrided, (int)g.nz, dir, &kz) : lookup_kernel_f32(kStrided, (int)g.nz, dir, &kz);
-  if (!oky || !okz || !ky.tma_fn || !kz.tma_fn || ky.tma_w != kz.tma_w) return false;
-  const long long w = ky.tma_w;
-  // the inverse c2c uses `out` as the L2 scratch: no padding room there
-  if (pl->dir == DFFT_INVERSE && !pl->r2c && g.nxc % w != 0) return false;
-  if (pl->r2r) return false;
-  return g.ny * (long long)pl->es % 16 == 0 && g.nxc * (long long)pl->es % 16 == 0;
-}
-
-dfft_status_t build_single_blocked(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
-  const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
-  const long long nxl = xreal(pl) ? nx / 2 : nx;
-  KernelInfo ky;
-  if (!(pl->f64 ? lookup_kernel_f64(kStrided, (int)ny, pl->dir, &ky) : lookup_kernel_f32(kStrided, (int)ny, pl->dir, &ky)))
-    return fail(DFFT_ERR_INTERNAL, "no strided kernel for ny");
-  const long long w = ky.tma_w;
-  const long long W = nxc * ny * nz, Wb = round_up(nxc, w) * ny * nz;
-  const bool c2r = pl->r2c && pl->dir == DFFT_INVERSE;
-  rp.A.resize(1);
-  rp.B.resize(1);
-  rp.E1.resize(1);
-  rp.E2.resize(1);
-  Stage &A = rp.A[0], &B = rp.B[0], &C = rp.C;
-  // L1 [y][z][x]: (x, y, z) at x + nxc·(z + nz·y);  L2 [xb][z][y][w]: blocked, block stride ny·nz·w
-  auto set_l1_lines = [&](SideMap& m) { set_side(m, 1, nz * nxc, nxc); };  // contig: l0 = y, l1 = z
-  auto set_l2_zpass = [&](SideMap& m) {  // t = z, l0 = x, l1 = y
-    set_side(m, ny * w, 1, w);
-    m.bw = (int)w;
-    m.mT = nz * ny;
-  };
-  auto set_l2_ypass = [&](SideMap& m) {  // t = y, l0 = x, l1 = z
-    set_side(m, w, 1, ny * w);
-    m.bw = (int)w;
-    m.mT = nz;
-  };
-  if (pl->dir == DFFT_FORWARD) {
-    rp.ws_bytes = (size_t)(Wb * es);
-    A.in = {kUserIn, 0};  // x-pass: lines (l0 = y, l1 = z), natural in
-    set_side(A.a.in, 1, nxl, ny * nxl);
-    A.out = {kUserOut, 0};
-    set_l1_lines(A.a.out);
-    A.a.scale = 1.0;
-    ST(finish_stage(pl, A, fam_x_fwd(pl), (int)nxl, ny, nz, nullptr, nullptr));
-    B.in = {kUserOut, 0};  // z-pass: columns (l0 = x, l1 = y) of L1 -> L2
-    set_side(B.a.in, nxc, 1, nz * nxc);
-    B.out = {kWs, 0};
-    set_l2_zpass(B.a.out);
-    B.a.scale = 1.0;
-    ST(finish_stage(pl, B, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr));
-    C.in = {kWs, 0};  // y-pass: columns (l0 = x, l1 = z) of L2 -> natural `out`
-    set_l2_ypass(C.a.in);
-    C.out = {kUserOut, 0};
-    set_side(C.a.out, nxc, 1, ny * nxc);
-    C.a.scale = 1.0;
-    C.last_fwd = true;  // t = y, l0 = x, l1 = z
-    C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
-    ST(finish_stage(pl, C, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
-  } else {
-    // scratch: c2c: L2 in `out` (nxc % w == 0 checked), L1 in ws;  c2r: both in ws
-    rp.ws_bytes = (size_t)((c2r ? Wb + W : W) * es);
-    const Ref l2 = c2r ? Ref{kWs, 0} : Ref{kUserOut, 0};
-    const Ref l1 = c2r ? Ref{kWs, Wb * es} : Ref{kWs, 0};
-    A.in = {kUserIn, 0};  // y-pass: columns (l0 = x, l1 = z), natural in -> L2
-    set_side(A.a.in, nxc, 1, ny * nxc);
-    A.out = l2;
-    set_l2_ypass(A.a.out);
-    A.a.scale = 1.0;
-    ST(finish_stage(pl, A, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
-    B.in = l2;  // z-pass: columns (l0 = x, l1 = y) of L2 -> L1
-    set_l2_zpass(B.a.in);
-    B.out = l1;
-    set_side(B.a.out, nxc, 1, nz * nxc);
-    B.a.scale = 1.0;
-    ST(finish_stage(pl, B, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr));
-    C.in = l1;  // x-pass: lines (l0 = y, l1 = z) of L1 -> natural `out`, ×1/N
-    set_l1_lines(C.a.in);
-    C.out = {kUserOut, 0};
-    set_side(C.a.out, 1, nxl, ny * nxl);
-    C.a.scale = (xreal(pl) ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
-    ST(finish_stage(pl, C, fam_x_inv(pl), (int)nxl, ny, nz, nullptr, nullptr));
-  }
-  return DFFT_SUCCESS;
-}
-
+//   forward: x (in -> out as [y][z][x]), z ([y][z][x] -> ws natural: the one large-pitch side),
+//            y (ws -> out, natural -> natural)
+//   inverse: y (in -> out, natural), z (natural -> ws as [y][z][x]: the large-pitch read),
+//            x (ws -> out, natural, ×1/N)
 dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
   const long long nxl = xreal(pl) ? nx / 2 : nx;
@@ -1084,7 +1034,7 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Z.a.scale = 1.0;
     return finish_stage(pl, Z, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr);
   };
-  if (pl->dir == DFFT_FORWARD && !getenv("DFFT_SINGLE_FWD_ZREAD")) {
+  if (pl->dir == DFFT_FORWARD) {
     // forward with one large-pitch side in total (r01 session 2): the x-pass writes [y][z][x],
     // the z-pass reads it at a small pitch and writes natural order (the one large-pitch side),
     // and the y-pass runs natural -> natural (both sides at the x-row pitch: 3.08 vs 3.75 ms)
@@ -1108,43 +1058,6 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.last_fwd = true;  // t = y, l0 = x, l1 = z
     C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
     ST(finish_stage(pl, C, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
-  } else if (pl->dir == DFFT_FORWARD) {
-    A.in = {kUserIn, 0};  // lines (l0 = y, l1 = z)
-    set_side(A.a.in, 1, nxl, ny * nxl);
-    A.out = {kUserOut, 0};
-    set_side(A.a.out, 1, nxc, ny * nxc);
-    A.a.scale = 1.0;
-    ST(finish_stage(pl, A, fam_x_fwd(pl), (int)nxl, ny, nz, nullptr, nullptr));
-    ST(zpass(B));
-    C.in = {kWs, 0};  // columns (l0 = x, l1 = z)
-    set_side(C.a.in, nz * nxc, 1, nxc);
-    C.out = {kUserOut, 0};
-    set_side(C.a.out, nxc, 1, ny * nxc);
-    C.a.scale = 1.0;
-    C.last_fwd = true;  // t = y, l0 = x, l1 = z
-    C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
-    ST(finish_stage(pl, C, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
-  } else if (!c2r && getenv("DFFT_SINGLE_INV_YWRITE")) {
-    // inverse with the large-pitch side on a store: y-pass natural -> [y][z][x] (in `out`),
-    // z-pass [y][z][x] -> ws [y][z][x] (both small), x-pass ws -> natural (A/B option)
-    A.in = {kUserIn, 0};  // y-pass: columns (l0 = x, l1 = z)
-    set_side(A.a.in, nxc, 1, ny * nxc);
-    A.out = {kUserOut, 0};
-    set_side(A.a.out, nz * nxc, 1, nxc);
-    A.a.scale = 1.0;
-    ST(finish_stage(pl, A, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
-    B.in = {kUserOut, 0};  // z-pass: columns (l0 = x, l1 = y)
-    set_side(B.a.in, nxc, 1, nz * nxc);
-    B.out = {kWs, 0};
-    set_side(B.a.out, nxc, 1, nz * nxc);
-    B.a.scale = 1.0;
-    ST(finish_stage(pl, B, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr));
-    C.in = {kWs, 0};  // x-pass: lines (l0 = y, l1 = z) of [y][z][x]
-    set_side(C.a.in, 1, nz * nxc, nxc);
-    C.out = {kUserOut, 0};
-    set_side(C.a.out, 1, nxl, ny * nxl);
-    C.a.scale = (xreal(pl) ? 2.0 : 1.0) / ((double)nx * (double)ny * (double)nz);
-    ST(finish_stage(pl, C, fam_x_inv(pl), (int)nxl, ny, nz, nullptr, nullptr));
   } else {
     A.in = {kUserIn, 0};  // columns (l0 = x, l1 = z)
     set_side(A.a.in, nxc, 1, ny * nxc);
@@ -1352,9 +1265,7 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
       cuuint64_t dims[3] = {(cuuint64_t)(2 * a.L0), (cuuint64_t)s.n, (cuuint64_t)a.L1};
       cuuint64_t strides[2] = {(cuuint64_t)tstride * ces,
                                (cuuint64_t)(a.L1 > 1 ? lstride * ces : 16 * ((tstride * ces * s.n + 15) / 16))};
-      const bool v2 = s.tma_variant == 2;
-      cuuint32_t box[3] = {(cuuint32_t)(2 * (v2 ? s.k.tma2_w : s.k.tma_w)), (cuuint32_t)(v2 ? s.k.tma2_r0 : s.k.tma_boxr),
-                           1};
+      cuuint32_t box[3] = {(cuuint32_t)(2 * s.k.tma_w), (cuuint32_t)s.k.tma_boxr, 1};
       cuuint32_t estr[3] = {1, 1, 1};
       return tensor_map_encoder()(tm, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base,
                                   dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -1391,12 +1302,9 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
       if (s.k.tma_st_only && !use_st) goto plain;  // R2R: the TMA variant needs TMA stores
       if (spec)
         CU(cudaLaunchKernel(s.k.tma_st_spec_fn, dim3((unsigned)grid), dim3(s.k.tma_threads), targs, s.k.tma_smem, st));
-      else if (s.tma_variant == 2)
-        CU(cudaLaunchKernel(use_st ? s.k.tma2_st_fn : s.k.tma2_fn, dim3((unsigned)grid), dim3(s.k.tma2_threads),
-                            targs, s.k.tma2_smem, st));
       else
         CU(cudaLaunchKernel(a.out.nbulk > 0 ? s.k.tma_bk_fn
-                            : use_st        ? (g_tst_work ? s.k.tma_st1_fn : s.k.tma_st_fn)
+                            : use_st        ? s.k.tma_st1_fn
                                             : s.k.tma_fn,
                             dim3((unsigned)grid),
                             dim3(s.k.tma_threads), targs, s.k.tma_smem, st));
@@ -1421,7 +1329,444 @@ dfft_status_t exchange_nccl(dfft_plan_t pl, const Exchange& x, const Ctx& cx, cu
   return DFFT_SUCCESS;
 }
 
-// simulated ranks: rank r's send to peer q is matched with q's receive from r, in order
+// ------------------------------------------------------------------------------ profiling
+// phases: 0 stage A, 1 exchange 1, 2 stage B, 3 exchange 2, 4 stage C.  Every execute records an
+// origin event on the caller's stream; every profiled step a (start, stop) pair on its own stream.
+dfft_status_t prof_origin(dfft_plan_t pl, cudaStream_t st, size_t* exec) {
+  if (!pl->prof) return DFFT_SUCCESS;
+  const size_t i = pl->prof_nexec++;
+  while (pl->prof_origin.size() < pl->prof_nexec) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    pl->prof_origin.push_back(e);
+  }
+  *exec = i;
+  CU(cudaEventRecord(pl->prof_origin[i], st));
+  return DFFT_SUCCESS;
+}
+dfft_status_t prof_begin(dfft_plan_t pl, const dfft_plan_s::ProfRec& rec, cudaStream_t st, size_t* slot) {
+  if (!pl->prof) return DFFT_SUCCESS;
+  const size_t i = pl->prof_used++;
+  while (pl->prof_ev.size() < 2 * pl->prof_used) {
+    cudaEvent_t e;
+    CU(cudaEventCreate(&e));
+    pl->prof_ev.push_back(e);
+  }
+  if (pl->prof_rec.size() < pl->prof_used) pl->prof_rec.resize(pl->prof_used);
+  pl->prof_rec[i] = rec;
+  *slot = i;
+  CU(cudaEventRecord(pl->prof_ev[2 * i], st));
+  return DFFT_SUCCESS;
+}
+dfft_status_t prof_end(dfft_plan_t pl, size_t slot, cudaStream_t st) {
+  if (!pl->prof) return DFFT_SUCCESS;
+  CU(cudaEventRecord(pl->prof_ev[2 * slot + 1], st));
+  return DFFT_SUCCESS;
+}
+// synchronise the recorded events: per-phase sums and timeline spans (relative to the origin of
+// the execute each span belongs to)
+dfft_status_t prof_resolve(dfft_plan_t pl) {
+  for (size_t i = 0; i < pl->prof_used; ++i) {
+    const dfft_plan_s::ProfRec& r = pl->prof_rec[i];
+    CU(cudaEventSynchronize(pl->prof_ev[2 * i + 1]));
+    float t = 0, a = 0, b = 0;
+    CU(cudaEventElapsedTime(&t, pl->prof_ev[2 * i], pl->prof_ev[2 * i + 1]));
+    pl->prof_ms[r.phase] += t;
+    pl->prof_n[r.phase] += 1;
+    if (r.exec < pl->prof_nexec) {
+      CU(cudaEventElapsedTime(&a, pl->prof_origin[r.exec], pl->prof_ev[2 * i]));
+      CU(cudaEventElapsedTime(&b, pl->prof_origin[r.exec], pl->prof_ev[2 * i + 1]));
+      pl->prof_spans.push_back(dfft_span_t{r.phase, r.stream, r.chunk, r.rank, (int)r.exec, (double)a, (double)b});
+    }
+  }
+  pl->prof_used = 0;
+  pl->prof_nexec = 0;
+  return DFFT_SUCCESS;
+}
+
+// ------------------------------------------------------------------------------ flags
+constexpr int kMaxSig = 64;
+struct SignalArgs {
+  unsigned int* set[kMaxSig];
+  unsigned int* clr[kMaxSig];
+  int nset, nclr;
+};
+
+// One thread: reset the words this rank has waited on (its own window), make every earlier write
+// of this stream (the stage kernel's stores into the peers' windows, the resets) visible system
+// wide, then publish the signals with release stores into the targets' windows.
+__global__ void dfft_flag_kernel(const __grid_constant__ SignalArgs a) {
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < a.nclr; ++i) asm volatile("st.relaxed.sys.global.u32 [%0], 0;" ::"l"(a.clr[i]) : "memory");
+  __threadfence_system();
+  for (int i = 0; i < a.nset; ++i) asm volatile("st.release.sys.global.u32 [%0], 1;" ::"l"(a.set[i]) : "memory");
+}
+
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitFn stream_wait_value32() {
+  static WaitFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<WaitFn>(p);
+  }();
+  return fn;
+}
+
+// flag word: arr kReady / kDone; e = exchange (0 first, 1 second); k chunk; r writer rank
+inline size_t flag_index(const dfft_plan_s* pl, int arr, int e, int k, int r) {
+  const size_t P = (size_t)pl->P1 * pl->P2, K = (size_t)pl->K;
+  return (((size_t)arr * 2 + e) * K + k) * P + r;
+}
+inline unsigned int* own_flags(const dfft_plan_s* pl, const RankPlan& rp) {
+  return reinterpret_cast<unsigned int*>((char*)rp.ws + pl->flag_off);
+}
+// initial flag block: READY = 0 (nothing landed), DONE = 1 (every receive region free)
+std::vector<unsigned int> initial_flags(const dfft_plan_s* pl) {
+  const size_t half = (size_t)2 * pl->K * pl->P1 * pl->P2;
+  std::vector<unsigned int> h(2 * half, 0u);
+  for (size_t q = half; q < 2 * half; ++q) h[q] = 1u;
+  return h;
+}
+
+// ------------------------------------------------------------------------------ schedules
+// Builds a rank's execute as a list of steps on two streams (X = 0, Y = 1).  Without overlap
+// (DFFT_FLAG_NO_OVERLAP) the same list runs on the caller's stream alone: a valid serial order,
+// because every wait refers to a signal that comes earlier in every rank's list.
+struct SchedBuilder {
+  RankPlan& rp;
+  void push(Op o) { rp.sched.push_back(std::move(o)); }
+  void launch(int s, const Stage& st, int phase, int k) {
+    Op o;
+    o.kind = kOpLaunch, o.s = s, o.st = &st, o.phase = phase, o.chunk = k;
+    push(std::move(o));
+  }
+  void wait(int s, int arr, int e, int k, const std::vector<int>& from) {
+    Op o;
+    o.kind = kOpWait, o.s = s, o.chunk = k;
+    o.wait = FlagRef{arr, e, k, from};
+    push(std::move(o));
+  }
+  void signal(int s, std::vector<FlagRef> set, std::vector<FlagRef> clr) {
+    Op o;
+    o.kind = kOpSignal, o.s = s;
+    o.set = std::move(set);
+    o.clr = std::move(clr);
+    push(std::move(o));
+  }
+  int record(int s) {
+    Op o;
+    o.kind = kOpRecord, o.s = s, o.ev = rp.nev++;
+    push(o);
+    return o.ev;
+  }
+  void swait(int s, int ev) {
+    Op o;
+    o.kind = kOpStreamWait, o.s = s, o.ev = ev;
+    push(std::move(o));
+  }
+  void xfer(int kind, int s, const Exchange& x, int phase, int k) {
+    Op o;
+    o.kind = kind, o.s = s, o.x = &x, o.phase = phase, o.chunk = k;
+    push(std::move(o));
+  }
+};
+
+// Fused stores (the P > 1 default): the stage kernels store straight into the peers' windows;
+// flags order producer and consumer per chunk (Alg. 2's progressive receive) and the
+// two streams overlap the chunks (Fig. 1).
+void sched_p2p(dfft_plan_t pl, RankPlan& rp) {
+  SchedBuilder b{rp};
+  const int K = (int)rp.A.size();
+  if (pl->bc) {
+    // X: A (whole), then C(k) as chunk k of the second exchange completes; Y: B(k), k = 0..K-1
+    const std::vector<int>& p1 = rp.E1[0].peers;
+    b.wait(0, kDone, 0, 0, p1);  // the peers have read what I stored last execute
+    b.launch(0, rp.A[0], 0, 0);
+    b.signal(0, {{kReady, 0, 0, p1}}, {{kDone, 0, 0, p1}});
+    const int eA = b.record(0);
+    b.swait(1, eA);
+    b.wait(1, kReady, 0, 0, p1);
+    std::vector<int> eB(K);
+    for (int k = 0; k < K; ++k) {
+      const std::vector<int>& p2 = rp.E2[k].peers;
+      b.wait(1, kDone, 1, k, p2);
+      b.launch(1, rp.B[k], 2, k);
+      b.signal(1, {{kReady, 1, k, p2}}, {{kDone, 1, k, p2}});
+      eB[k] = b.record(1);
+    }
+    b.signal(1, {{kDone, 0, 0, p1}}, {{kReady, 0, 0, p1}});  // done reading my first-exchange window
+    for (int k = 0; k < K; ++k) {
+      const std::vector<int>& p2 = rp.E2[k].peers;
+      b.swait(0, eB[k]);
+      b.wait(0, kReady, 1, k, p2);
+      b.launch(0, rp.Cc[k], 4, k);
+      b.signal(0, {{kDone, 1, k, p2}}, {{kReady, 1, k, p2}});
+    }
+    return;
+  }
+  // X runs stage A chunk by chunk; Y runs stage B of each chunk as soon as its first exchange has
+  // landed, then stage C
+  std::vector<int> eA(K);
+  for (int k = 0; k < K; ++k) {
+    const std::vector<int>& p1 = rp.E1[k].peers;
+    b.wait(0, kDone, 0, k, p1);
+    b.launch(0, rp.A[k], 0, k);
+    b.signal(0, {{kReady, 0, k, p1}}, {{kDone, 0, k, p1}});
+    eA[k] = b.record(0);
+  }
+  for (int k = 0; k < K; ++k) {
+    const std::vector<int>&p1 = rp.E1[k].peers, &p2 = rp.E2[k].peers;
+    b.swait(1, eA[k]);  // my own block of chunk k
+    b.wait(1, kReady, 0, k, p1);
+    b.wait(1, kDone, 1, k, p2);
+    b.launch(1, rp.B[k], 2, k);
+    b.signal(1, {{kDone, 0, k, p1}, {kReady, 1, k, p2}}, {{kReady, 0, k, p1}, {kDone, 1, k, p2}});
+  }
+  for (int k = 0; k < K; ++k) b.wait(1, kReady, 1, k, rp.E2[k].peers);
+  b.launch(1, rp.C, 4, 0);
+  std::vector<FlagRef> set, clr;
+  for (int k = 0; k < K; ++k) {
+    set.push_back({kDone, 1, k, rp.E2[k].peers});
+    clr.push_back({kReady, 1, k, rp.E2[k].peers});
+  }
+  b.signal(1, set, clr);
+}
+
+// Copy-engine transport: the stage kernels pack into local send blocks; Y's copy engine moves
+// each block into the receiver's window (hybrid: the forward x-FFT stores fused instead).
+void sched_ce(dfft_plan_t pl, RankPlan& rp) {
+  (void)pl;
+  SchedBuilder b{rp};
+  const int K = (int)rp.A.size();
+  auto ce = [&](int e, int k, const Exchange& x) {
+    b.wait(1, kDone, e, k, x.peers);  // the receivers have read the previous execute's blocks
+    b.xfer(kOpCeCopy, 1, x, e == 0 ? 1 : 3, k);
+    b.signal(1, {{kReady, e, k, x.peers}}, {{kDone, e, k, x.peers}});
+  };
+  auto do_A = [&](int k) {
+    const Exchange& x = rp.E1[k];
+    if (x.fused) {
+      b.wait(0, kDone, 0, k, x.peers);
+      b.launch(0, rp.A[k], 0, k);
+      b.signal(0, {{kReady, 0, k, x.peers}}, {{kDone, 0, k, x.peers}});
+    } else {
+      b.launch(0, rp.A[k], 0, k);
+      b.swait(1, b.record(0));
+      ce(0, k, x);
+    }
+  };
+  do_A(0);
+  for (int k = 0; k < K; ++k) {
+    if (k + 1 < K) do_A(k + 1);
+    const Exchange &x1 = rp.E1[k], &x2 = rp.E2[k];
+    b.wait(0, kReady, 0, k, x1.peers);  // the peers' blocks of chunk k have landed
+    if (x2.fused) b.wait(0, kDone, 1, k, x2.peers);
+    b.launch(0, rp.B[k], 2, k);
+    b.signal(0, {{kDone, 0, k, x1.peers}}, {{kReady, 0, k, x1.peers}});  // done reading my first receive region
+    if (x2.fused) {
+      b.signal(0, {{kReady, 1, k, x2.peers}}, {{kDone, 1, k, x2.peers}});
+    } else {
+      b.swait(1, b.record(0));
+      ce(1, k, x2);
+    }
+  }
+  for (int k = 0; k < K; ++k) b.wait(0, kReady, 1, k, rp.E2[k].peers);
+  b.launch(0, rp.C, 4, 0);
+  std::vector<FlagRef> set, clr;
+  for (int k = 0; k < K; ++k) {
+    set.push_back({kDone, 1, k, rp.E2[k].peers});
+    clr.push_back({kReady, 1, k, rp.E2[k].peers});
+  }
+  b.signal(0, set, clr);
+}
+
+// NCCL transport (and P = 1): grouped send/recv on Y against the FFTs on X.  Host issue order is
+// a topological order of the chunk DAG:  A0 E1_0 | A1 E1_1 B0 E2_0 | A2 E1_2 B1 E2_1 | ...
+void sched_nccl(dfft_plan_t pl, RankPlan& rp) {
+  SchedBuilder b{rp};
+  const int K = (int)rp.A.size();
+  auto has = [](const Exchange& x) { return !x.sends.empty() || !x.recvs.empty(); };
+  if (!pl->overlap) {  // static-barrier ablation ("SimpleMPIFFT"): program order, one stream
+    for (int k = 0; k < K; ++k) b.launch(0, rp.A[k], 0, k);
+    for (int k = 0; k < K; ++k) b.xfer(kOpNccl, 0, rp.E1[k], 1, k);
+    for (int k = 0; k < K; ++k) b.launch(0, rp.B[k], 2, k);
+    for (int k = 0; k < K; ++k) b.xfer(kOpNccl, 0, rp.E2[k], 3, k);
+    b.launch(0, rp.C, 4, 0);
+    return;
+  }
+  std::vector<int> e1(K, -1), e2(K, -1);
+  auto do_A = [&](int k) {
+    b.launch(0, rp.A[k], 0, k);
+    if (has(rp.E1[k])) {
+      b.swait(1, b.record(0));
+      b.xfer(kOpNccl, 1, rp.E1[k], 1, k);
+      e1[k] = b.record(1);
+    }
+  };
+  do_A(0);
+  for (int k = 0; k < K; ++k) {
+    if (k + 1 < K) do_A(k + 1);
+    if (e1[k] >= 0) b.swait(0, e1[k]);
+    b.launch(0, rp.B[k], 2, k);
+    if (has(rp.E2[k])) {
+      b.swait(1, b.record(0));
+      b.xfer(kOpNccl, 1, rp.E2[k], 3, k);
+      e2[k] = b.record(1);
+    }
+  }
+  if (e2[K - 1] >= 0) b.swait(0, e2[K - 1]);  // same comm stream => the last record suffices
+  b.launch(0, rp.C, 4, 0);
+}
+
+void build_schedule(dfft_plan_t pl, RankPlan& rp) {
+  rp.sched.clear();
+  rp.nev = 0;
+  if (pl->p2p) sched_p2p(pl, rp);
+  else if (pl->ce) sched_ce(pl, rp);
+  else sched_nccl(pl, rp);
+}
+
+// ------------------------------------------------------------------------------ interpreter
+struct RunCtx {
+  Ctx cx;
+  cudaStream_t s[2];
+  size_t exec;
+};
+
+dfft_status_t issue_signal(dfft_plan_t pl, const RankPlan& rp, const Op& op, cudaStream_t st) {
+  SignalArgs a{};
+  unsigned int* own = own_flags(pl, rp);
+  for (const FlagRef& f : op.clr)
+    for (int r : f.ranks) {
+      if (a.nclr >= kMaxSig) return fail(DFFT_ERR_INTERNAL, "too many flag resets in one signal");
+      a.clr[a.nclr++] = own + flag_index(pl, f.arr, f.e, f.k, r);
+    }
+  for (const FlagRef& f : op.set)
+    for (int t : f.ranks) {
+      if (a.nset >= kMaxSig) return fail(DFFT_ERR_INTERNAL, "too many flag signals in one signal");
+      a.set[a.nset++] = reinterpret_cast<unsigned int*>((char*)pl->peer_ws[t] + pl->flag_off) +
+                        flag_index(pl, f.arr, f.e, f.k, rp.rank);
+    }
+  if (a.nset == 0 && a.nclr == 0) return DFFT_SUCCESS;
+  void* args[] = {&a};
+  CU(cudaLaunchKernel((const void*)dfft_flag_kernel, dim3(1), dim3(32), args, 0, st));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t issue_ce(dfft_plan_t pl, const Exchange& x, const Ctx& cx, cudaStream_t st) {
+  (void)pl;
+  for (const Xfer& t : x.sends) {
+    if (t.height > 1)
+      CU(cudaMemcpy2DAsync(resolve(t.remote, cx), t.dpitch, resolve(t.ref, cx), t.spitch, t.width, t.height,
+                           cudaMemcpyDeviceToDevice, st));
+    else
+      CU(cudaMemcpyAsync(resolve(t.remote, cx), resolve(t.ref, cx), t.bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t issue(dfft_plan_t pl, const RankPlan& rp, const Op& op, const RunCtx& rc) {
+  const cudaStream_t st = rc.s[op.s];
+  const bool two = rc.s[0] != rc.s[1];
+  switch (op.kind) {
+    case kOpLaunch:
+    case kOpNccl:
+    case kOpCeCopy: {
+      if (op.kind == kOpLaunch && op.st->empty) return DFFT_SUCCESS;
+      if (op.kind == kOpNccl && op.x->sends.empty() && op.x->recvs.empty()) return DFFT_SUCCESS;
+      if (op.kind == kOpCeCopy && op.x->sends.empty()) return DFFT_SUCCESS;
+      size_t slot = 0;
+      ST(prof_begin(pl, dfft_plan_s::ProfRec{op.phase, op.s, op.chunk, rp.rank, rc.exec}, st, &slot));
+      if (op.kind == kOpLaunch) ST(launch(*op.st, rc.cx, st));
+      else if (op.kind == kOpNccl) ST(exchange_nccl(pl, *op.x, rc.cx, st));
+      else ST(issue_ce(pl, *op.x, rc.cx, st));
+      return prof_end(pl, slot, st);
+    }
+    case kOpWait: {
+      unsigned int* own = own_flags(pl, rp);
+      for (int r : op.wait.ranks) {
+        const CUresult res = stream_wait_value32()(
+            (CUstream)st, (CUdeviceptr)(own + flag_index(pl, op.wait.arr, op.wait.e, op.wait.k, r)), 1,
+            CU_STREAM_WAIT_VALUE_GEQ);
+        if (res != CUDA_SUCCESS) return fail(DFFT_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)res);
+      }
+      return DFFT_SUCCESS;
+    }
+    case kOpSignal: return issue_signal(pl, rp, op, st);
+    case kOpRecord:
+      if (two) CU(cudaEventRecord(rp.ev[op.ev], st));
+      return DFFT_SUCCESS;
+    case kOpStreamWait:
+      if (two) CU(cudaStreamWaitEvent(st, rp.ev[op.ev], 0));
+      return DFFT_SUCCESS;
+  }
+  return fail(DFFT_ERR_INTERNAL, "bad schedule op");
+}
+
+// Issue step `pos` of a rank's schedule.  After a failure the remaining steps that move data are
+// skipped but every wait and signal is still issued, so the peers' flag protocol stays in step
+// (no rank is left waiting for a signal that will never come); the plan is marked failed.
+struct Runner {
+  dfft_plan_t pl;
+  dfft_status_t first = DFFT_SUCCESS;
+  std::string msg;
+  void step(const RankPlan& rp, size_t pos, const RunCtx& rc) {
+    const Op& op = rp.sched[pos];
+    const bool data = op.kind == kOpLaunch || op.kind == kOpNccl || op.kind == kOpCeCopy;
+    if (first != DFFT_SUCCESS && data) return;
+    const dfft_status_t st = issue(pl, rp, op, rc);
+    if (st != DFFT_SUCCESS && first == DFFT_SUCCESS) {
+      first = st;
+      msg = g_err;
+    }
+  }
+  dfft_status_t finish() {
+    if (first == DFFT_SUCCESS) return DFFT_SUCCESS;
+    pl->fail_msg = "enqueue failed: " + msg;
+    pl->failed.store(1);
+    return fail(first, "%s", msg.c_str());
+  }
+};
+
+bool two_streams(const dfft_plan_t pl) { return pl->overlap && (size_t)pl->P1 * pl->P2 > 1; }
+
+dfft_status_t fork_rank(dfft_plan_t pl, RankPlan& rp, cudaStream_t user, RunCtx& rc) {
+  if (!two_streams(pl)) {
+    rc.s[0] = rc.s[1] = user;
+    return DFFT_SUCCESS;
+  }
+  rc.s[0] = rp.sX;
+  rc.s[1] = rp.sY;
+  CU(cudaEventRecord(rp.ev_fork, user));
+  CU(cudaStreamWaitEvent(rp.sX, rp.ev_fork, 0));
+  CU(cudaStreamWaitEvent(rp.sY, rp.ev_fork, 0));
+  return DFFT_SUCCESS;
+}
+dfft_status_t join_rank(dfft_plan_t pl, RankPlan& rp, cudaStream_t user) {
+  if (!two_streams(pl)) return DFFT_SUCCESS;
+  CU(cudaEventRecord(rp.ev_join[0], rp.sX));
+  CU(cudaEventRecord(rp.ev_join[1], rp.sY));
+  CU(cudaStreamWaitEvent(user, rp.ev_join[0], 0));
+  CU(cudaStreamWaitEvent(user, rp.ev_join[1], 0));
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream_t user) {
+  RankPlan& rp = pl->ranks[0];
+  RunCtx rc{Ctx{in, out, rp.ws, pl->peer_ws.empty() ? nullptr : pl->peer_ws.data()}, {user, user}, 0};
+  ST(prof_origin(pl, user, &rc.exec));
+  ST(fork_rank(pl, rp, user, rc));
+  Runner run{pl};
+  for (size_t pos = 0; pos < rp.sched.size(); ++pos) run.step(rp, pos, rc);
+  ST(join_rank(pl, rp, user));
+  return run.finish();
+}
+
+// simulated ranks, NCCL layouts: rank r's send to peer q is matched with q's receive from r
 dfft_status_t exchange_sim(dfft_plan_t pl, bool second, size_t k, const void* const* ins, void* const* outs,
                            cudaStream_t st) {
   const int P = (int)pl->ranks.size();
@@ -1448,310 +1793,191 @@ dfft_status_t exchange_sim(dfft_plan_t pl, bool second, size_t k, const void* co
   return DFFT_SUCCESS;
 }
 
-// phases: 0 stage A, 1 exchange 1, 2 stage B, 3 exchange 2, 4 stage C
-dfft_status_t prof_begin(dfft_plan_t pl, int phase, cudaStream_t st, size_t* slot) {
-  if (!pl->prof) return DFFT_SUCCESS;
-  size_t i = pl->prof_used++;
-  while (pl->prof_ev.size() < 2 * pl->prof_used) {
-    cudaEvent_t e;
-    CU(cudaEventCreate(&e));
-    pl->prof_ev.push_back(e);
-  }
-  if (pl->prof_phase.size() < pl->prof_used) pl->prof_phase.resize(pl->prof_used);
-  pl->prof_phase[i] = phase;
-  *slot = i;
-  CU(cudaEventRecord(pl->prof_ev[2 * i], st));
-  return DFFT_SUCCESS;
-}
-dfft_status_t prof_end(dfft_plan_t pl, size_t slot, cudaStream_t st) {
-  if (!pl->prof) return DFFT_SUCCESS;
-  CU(cudaEventRecord(pl->prof_ev[2 * slot + 1], st));
-  return DFFT_SUCCESS;
-}
-dfft_status_t launch_p(dfft_plan_t pl, int phase, const Stage& s, const Ctx& c, cudaStream_t st) {
-  if (s.empty) return DFFT_SUCCESS;
-  size_t slot = 0;
-  ST(prof_begin(pl, phase, st, &slot));
-  ST(launch(s, c, st));
-  return prof_end(pl, slot, st);
-}
-dfft_status_t exchange_p(dfft_plan_t pl, int phase, const Exchange& x, const Ctx& c, cudaStream_t st) {
-  if (x.sends.empty() && x.recvs.empty()) return DFFT_SUCCESS;
-  size_t slot = 0;
-  ST(prof_begin(pl, phase, st, &slot));
-  ST(exchange_nccl(pl, x, c, st));
-  return prof_end(pl, slot, st);
-}
-
-// ---- P2P exchange: stage kernels store into the peers' windows; flags order the stages.
-struct SignalArgs {
-  unsigned int* ptr[2 * kMaxBases];
-  int n;
-  unsigned int value;
-};
-
-__global__ void dfft_signal_kernel(const __grid_constant__ SignalArgs a) {
-  // stream order puts this after the stage kernel whose stores it publishes; the system-scope
-  // fence + release store make them visible to the peer that acquires the flag
-  if ((int)threadIdx.x < a.n) {
-    __threadfence_system();
-    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.ptr[threadIdx.x]), "r"(a.value) : "memory");
-  }
-}
-
-using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-WaitFn stream_wait_value32() {
-  static WaitFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    return reinterpret_cast<WaitFn>(p);
-  }();
-  return fn;
-}
-
-// flag word: arr 0 = ready, 1 = done; e = exchange (0 first, 1 second); k chunk; r writer/reader rank
-inline size_t flag_index(const dfft_plan_s* pl, int arr, int e, int k, int r) {
-  const size_t P = (size_t)pl->P1 * pl->P2, K = (size_t)pl->K;
-  return (((size_t)arr * 2 + e) * K + k) * P + r;
-}
-
-dfft_status_t p2p_signal(dfft_plan_t pl, int arr, int e, int k, const std::vector<int>& targets, unsigned value,
-                         cudaStream_t st) {
-  if (targets.empty()) return DFFT_SUCCESS;
-  SignalArgs a{};
-  a.n = (int)targets.size();
-  a.value = value;
-  const int me = pl->comm->rank;
-  for (size_t q = 0; q < targets.size(); ++q)
-    a.ptr[q] = reinterpret_cast<unsigned int*>((char*)pl->peer_ws[targets[q]] + pl->flag_off) +
-               flag_index(pl, arr, e, k, me);
-  void* args[] = {&a};
-  CU(cudaLaunchKernel((const void*)dfft_signal_kernel, dim3(1), dim3(32), args, 0, st));
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return DFFT_SUCCESS;
-}
-
-dfft_status_t p2p_wait(dfft_plan_t pl, int arr, int e, int k, const std::vector<int>& from, unsigned value,
-                       cudaStream_t st) {
-  unsigned int* flags = reinterpret_cast<unsigned int*>((char*)pl->ranks[0].ws + pl->flag_off);
-  for (int r : from) {
-    CUresult res = stream_wait_value32()((CUstream)st, (CUdeviceptr)(flags + flag_index(pl, arr, e, k, r)), value,
-                                         CU_STREAM_WAIT_VALUE_GEQ);
-    if (res != CUDA_SUCCESS) return fail(DFFT_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)res);
-  }
-  return DFFT_SUCCESS;
-}
-
-// Two compute streams: X runs stage A chunk by chunk, Y runs stage B of each chunk as soon as
-// its first exchange has landed, then stage C.  So A(k+1) overlaps B(k) (Fig. 1, the
-// progressive per-chunk pipelining); when one of the two is NVLink-bound (fused remote stores)
-// it runs on at most sm_cap SMs so the HBM-bound one can co-reside (Stage::sm_cap).
-dfft_status_t execute_p2p(dfft_plan_t pl, const Ctx& cx, cudaStream_t user) {
-  RankPlan& rp = pl->ranks[0];
-  const int K = (int)rp.A.size();
-  const unsigned ep = ++pl->epoch;
-  cudaStream_t X = pl->s_comp, Y = pl->s_comm;
-  CU(cudaEventRecord(pl->ev_fork, user));
-  CU(cudaStreamWaitEvent(X, pl->ev_fork, 0));
-  CU(cudaStreamWaitEvent(Y, pl->ev_fork, 0));
-  if (pl->bc) {
-    // X: A (whole), then C(k) as chunk k of the second exchange completes; Y: B(k), k = 0..K-1
-    const std::vector<int>& p1 = rp.E1[0].peers;
-    if (ep > 1) ST(p2p_wait(pl, 1, 0, 0, p1, ep - 1, X));
-    ST(launch_p(pl, 0, rp.A[0], cx, X));
-    ST(p2p_signal(pl, 0, 0, 0, p1, ep, X));
-    CU(cudaEventRecord(pl->evA[0], X));
-    CU(cudaStreamWaitEvent(Y, pl->evA[0], 0));
-    ST(p2p_wait(pl, 0, 0, 0, p1, ep, Y));
-    for (int k = 0; k < K; ++k) {
-      if (ep > 1) ST(p2p_wait(pl, 1, 1, k, rp.E2[k].peers, ep - 1, Y));
-      ST(launch_p(pl, 2, rp.B[k], cx, Y));
-      ST(p2p_signal(pl, 0, 1, k, rp.E2[k].peers, ep, Y));
-      CU(cudaEventRecord(pl->evB[k], Y));
-    }
-    ST(p2p_signal(pl, 1, 0, 0, p1, ep, Y));  // done reading my first-exchange window
-    for (int k = 0; k < K; ++k) {
-      CU(cudaStreamWaitEvent(X, pl->evB[k], 0));
-      ST(p2p_wait(pl, 0, 1, k, rp.E2[k].peers, ep, X));
-      ST(launch_p(pl, 4, rp.Cc[k], cx, X));
-      ST(p2p_signal(pl, 1, 1, k, rp.E2[k].peers, ep, X));
-    }
-  } else {
-  for (int k = 0; k < K; ++k) {
-    // my epoch-1 stores into the first-exchange peers were consumed
-    if (ep > 1) ST(p2p_wait(pl, 1, 0, k, rp.E1[k].peers, ep - 1, X));
-    ST(launch_p(pl, 0, rp.A[k], cx, X));
-    ST(p2p_signal(pl, 0, 0, k, rp.E1[k].peers, ep, X));
-    CU(cudaEventRecord(pl->evA[k], X));
-  }
-  for (int k = 0; k < K; ++k) {
-    CU(cudaStreamWaitEvent(Y, pl->evA[k], 0));  // my own block of chunk k
-    ST(p2p_wait(pl, 0, 0, k, rp.E1[k].peers, ep, Y));
-    if (ep > 1) ST(p2p_wait(pl, 1, 1, k, rp.E2[k].peers, ep - 1, Y));
-    ST(launch_p(pl, 2, rp.B[k], cx, Y));
-    ST(p2p_signal(pl, 1, 0, k, rp.E1[k].peers, ep, Y));  // done reading my first-exchange window
-    ST(p2p_signal(pl, 0, 1, k, rp.E2[k].peers, ep, Y));  // ready: stored into the peers' second windows
-  }
-  for (int k = 0; k < K; ++k) ST(p2p_wait(pl, 0, 1, k, rp.E2[k].peers, ep, Y));
-  ST(launch_p(pl, 4, rp.C, cx, Y));
-  for (int k = 0; k < K; ++k) ST(p2p_signal(pl, 1, 1, k, rp.E2[k].peers, ep, Y));
-  }
-  CU(cudaEventRecord(pl->ev_join_comp, X));
-  CU(cudaEventRecord(pl->ev_join_comm, Y));
-  CU(cudaStreamWaitEvent(user, pl->ev_join_comp, 0));
-  CU(cudaStreamWaitEvent(user, pl->ev_join_comm, 0));
-  return DFFT_SUCCESS;
-}
-
-// ---- CE exchange: stage kernels pack into local send blocks (as for NCCL); the copy engine of
-// the comm stream moves each block into the receiver's window; flags order producer/consumer.
-dfft_status_t exchange_ce(dfft_plan_t pl, int e, int k, const Exchange& x, const Ctx& cx, unsigned ep,
-                          cudaStream_t st) {
-  if (x.peers.empty()) return DFFT_SUCCESS;
-  if (ep > 1) ST(p2p_wait(pl, 1, e, k, x.peers, ep - 1, st));  // receivers consumed epoch ep-1
-  for (const Xfer& t : x.sends) {
-    if (t.height > 1)
-      CU(cudaMemcpy2DAsync(resolve(t.remote, cx), t.dpitch, resolve(t.ref, cx), t.spitch, t.width, t.height,
-                           cudaMemcpyDeviceToDevice, st));
-    else
-      CU(cudaMemcpyAsync(resolve(t.remote, cx), resolve(t.ref, cx), t.bytes, cudaMemcpyDeviceToDevice, st));
-  }
-  return p2p_signal(pl, 0, e, k, x.peers, ep, st);
-}
-
-dfft_status_t execute_ce(dfft_plan_t pl, const Ctx& cx, cudaStream_t user) {
-  RankPlan& rp = pl->ranks[0];
-  const size_t K = rp.A.size();
-  const unsigned ep = ++pl->epoch;
-  cudaStream_t sc = pl->s_comp, sm = pl->s_comm;
-  CU(cudaEventRecord(pl->ev_fork, user));
-  CU(cudaStreamWaitEvent(sc, pl->ev_fork, 0));
-  CU(cudaStreamWaitEvent(sm, pl->ev_fork, 0));
-  // a fused exchange is produced inside the FFT kernel: WAR wait before it, ready signal after it,
-  // both on the compute stream; a CE exchange is a copy on the comm stream after the kernel
-  auto do_A = [&](size_t k) -> dfft_status_t {
-    const Exchange& x = rp.E1[k];
-    if (x.fused && ep > 1) ST(p2p_wait(pl, 1, 0, (int)k, x.peers, ep - 1, sc));
-    ST(launch_p(pl, 0, rp.A[k], cx, sc));
-    if (x.fused) return p2p_signal(pl, 0, 0, (int)k, x.peers, ep, sc);
-    CU(cudaEventRecord(pl->evA[k], sc));
-    CU(cudaStreamWaitEvent(sm, pl->evA[k], 0));
-    size_t slot = 0;
-    ST(prof_begin(pl, 1, sm, &slot));
-    ST(exchange_ce(pl, 0, (int)k, x, cx, ep, sm));
-    return prof_end(pl, slot, sm);
-  };
-  ST(do_A(0));
-  for (size_t k = 0; k < K; ++k) {
-    if (k + 1 < K) ST(do_A(k + 1));
-    const Exchange& x2 = rp.E2[k];
-    ST(p2p_wait(pl, 0, 0, (int)k, rp.E1[k].peers, ep, sc));  // peers' blocks of chunk k have landed
-    if (x2.fused && ep > 1) ST(p2p_wait(pl, 1, 1, (int)k, x2.peers, ep - 1, sc));
-    ST(launch_p(pl, 2, rp.B[k], cx, sc));
-    ST(p2p_signal(pl, 1, 0, (int)k, rp.E1[k].peers, ep, sc));  // done reading my first receive region
-    if (x2.fused) {
-      ST(p2p_signal(pl, 0, 1, (int)k, x2.peers, ep, sc));
-    } else {
-      CU(cudaEventRecord(pl->evB[k], sc));
-      CU(cudaStreamWaitEvent(sm, pl->evB[k], 0));
-      size_t slot = 0;
-      ST(prof_begin(pl, 3, sm, &slot));
-      ST(exchange_ce(pl, 1, (int)k, x2, cx, ep, sm));
-      ST(prof_end(pl, slot, sm));
-    }
-  }
-  for (size_t k = 0; k < K; ++k) ST(p2p_wait(pl, 0, 1, (int)k, rp.E2[k].peers, ep, sc));
-  ST(launch_p(pl, 4, rp.C, cx, sc));
-  for (size_t k = 0; k < K; ++k) ST(p2p_signal(pl, 1, 1, (int)k, rp.E2[k].peers, ep, sc));
-  CU(cudaEventRecord(pl->ev_join_comp, sc));
-  CU(cudaEventRecord(pl->ev_join_comm, sm));
-  CU(cudaStreamWaitEvent(user, pl->ev_join_comp, 0));
-  CU(cudaStreamWaitEvent(user, pl->ev_join_comm, 0));
-  return DFFT_SUCCESS;
-}
-
-dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream_t user) {
-  RankPlan& rp = pl->ranks[0];
-  const size_t K = rp.A.size();
-  const Ctx cx{in, out, rp.ws, pl->peer_ws.empty() ? nullptr : pl->peer_ws.data()};
-  if (pl->p2p) return execute_p2p(pl, cx, user);
-  if (pl->ce) return execute_ce(pl, cx, user);
-  if (!pl->overlap) {
-    // static-barrier ablation: every step in program order on the user's stream
-    for (size_t k = 0; k < K; ++k) ST(launch_p(pl, 0, rp.A[k], cx, user));
-    for (size_t k = 0; k < K; ++k) ST(exchange_p(pl, 1, rp.E1[k], cx, user));
-    for (size_t k = 0; k < K; ++k) ST(launch_p(pl, 2, rp.B[k], cx, user));
-    for (size_t k = 0; k < K; ++k) ST(exchange_p(pl, 3, rp.E2[k], cx, user));
-    return launch_p(pl, 4, rp.C, cx, user);
-  }
-  cudaStream_t sc = pl->s_comp, sm = pl->s_comm;
-  CU(cudaEventRecord(pl->ev_fork, user));
-  CU(cudaStreamWaitEvent(sc, pl->ev_fork, 0));
-  CU(cudaStreamWaitEvent(sm, pl->ev_fork, 0));
-  // host issue order is a topological order of the chunk DAG, so every wait refers to the
-  // record issued in this execute:  A0 E1_0 | A1 E1_1 B0 E2_0 | A2 E1_2 B1 E2_1 | ...
-  auto do_A = [&](size_t k) -> dfft_status_t {
-    ST(launch_p(pl, 0, rp.A[k], cx, sc));
-    if (!rp.E1[k].sends.empty() || !rp.E1[k].recvs.empty()) {
-      CU(cudaEventRecord(pl->evA[k], sc));
-      CU(cudaStreamWaitEvent(sm, pl->evA[k], 0));
-      ST(exchange_p(pl, 1, rp.E1[k], cx, sm));
-      CU(cudaEventRecord(pl->evE1[k], sm));
-    }
-    return DFFT_SUCCESS;
-  };
-  ST(do_A(0));
-  for (size_t k = 0; k < K; ++k) {
-    if (k + 1 < K) ST(do_A(k + 1));
-    if (!rp.E1[k].sends.empty() || !rp.E1[k].recvs.empty()) CU(cudaStreamWaitEvent(sc, pl->evE1[k], 0));
-    ST(launch_p(pl, 2, rp.B[k], cx, sc));
-    if (!rp.E2[k].sends.empty() || !rp.E2[k].recvs.empty()) {
-      CU(cudaEventRecord(pl->evB[k], sc));
-      CU(cudaStreamWaitEvent(sm, pl->evB[k], 0));
-      ST(exchange_p(pl, 3, rp.E2[k], cx, sm));
-      CU(cudaEventRecord(pl->evE2[k], sm));
-    }
-  }
-  // stage C needs every chunk of exchange 2 (same comm stream => the last record suffices)
-  if (!rp.E2[K - 1].sends.empty() || !rp.E2[K - 1].recvs.empty()) CU(cudaStreamWaitEvent(sc, pl->evE2[K - 1], 0));
-  ST(launch_p(pl, 4, rp.C, cx, sc));
-  CU(cudaEventRecord(pl->ev_join_comp, sc));
-  CU(cudaEventRecord(pl->ev_join_comm, sm));
-  CU(cudaStreamWaitEvent(user, pl->ev_join_comp, 0));
-  CU(cudaStreamWaitEvent(user, pl->ev_join_comm, 0));
-  return DFFT_SUCCESS;
-}
-
-dfft_status_t execute_sim(dfft_plan_t pl, const void* const* ins, void* const* outs, cudaStream_t st) {
-  const size_t P = pl->ranks.size(), K = pl->ranks[0].A.size();
-  if (pl->p2p) {
-    // fused-store layouts: every stage of every rank stores straight into the other ranks'
-    // workspaces; stream order replaces the ready/done flags
-    void* const* peers = pl->peer_ws.data();
-    auto cx = [&](size_t r) { return Ctx{ins[r], outs[r], pl->ranks[r].ws, peers}; };
-    for (size_t k = 0; k < K; ++k)
-      for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].A[k], cx(r), st));
-    for (size_t k = 0; k < K; ++k)
-      for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].B[k], cx(r), st));
+// Simulated ranks.  IPC-window transports (fused stores, copy engines): every rank runs its own
+// schedule exactly as a real rank does — its own stream pair, the flag words in its workspace
+// (the other ranks' workspaces stand in for the peers' IPC windows), the B→C / K-chunk pipeline
+// and the SM caps.  The schedules are issued interleaved position by position, a topological
+// order of the cross-rank flag dependencies, so the GPU can always make progress whatever the
+// mapping of streams onto hardware queues.  ins[r] == nullptr: rank r does not execute (a failed
+// peer; its partners then wait until the watchdog releases them).
+// NCCL layouts: the stage kernels per rank, exchanges by device copies of the blocks NCCL would
+// move, in stream order on the caller's stream.
+dfft_status_t execute_sim(dfft_plan_t pl, const void* const* ins, void* const* outs, cudaStream_t user) {
+  const size_t P = pl->ranks.size();
+  if (pl->p2p || pl->ce) {
+    size_t exec = 0;
+    ST(prof_origin(pl, user, &exec));
+    std::vector<RunCtx> rc(P);
     for (size_t r = 0; r < P; ++r) {
-      if (pl->bc)
-        for (size_t k = 0; k < K; ++k) ST(launch(pl->ranks[r].Cc[k], cx(r), st));
-      else
-        ST(launch(pl->ranks[r].C, cx(r), st));
+      rc[r] = RunCtx{Ctx{ins[r], outs[r], pl->ranks[r].ws, pl->peer_ws.data()}, {user, user}, exec};
+      if (ins[r]) ST(fork_rank(pl, pl->ranks[r], user, rc[r]));
     }
-    return DFFT_SUCCESS;
+    const size_t L = pl->ranks[0].sched.size();
+    for (size_t r = 1; r < P; ++r)
+      if (pl->ranks[r].sched.size() != L) return fail(DFFT_ERR_INTERNAL, "rank schedules differ in length");
+    Runner run{pl};
+    for (size_t pos = 0; pos < L; ++pos)
+      for (size_t r = 0; r < P; ++r)
+        if (ins[r]) run.step(pl->ranks[r], pos, rc[r]);
+    for (size_t r = 0; r < P; ++r)
+      if (ins[r]) ST(join_rank(pl, pl->ranks[r], user));
+    return run.finish();
   }
+  const size_t K = pl->ranks[0].A.size();
+  auto cx = [&](size_t r) { return Ctx{ins[r], outs[r], pl->ranks[r].ws, nullptr}; };
   for (size_t k = 0; k < K; ++k)
-    for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].A[k], Ctx{ins[r], outs[r], pl->ranks[r].ws, nullptr}, st));
-  for (size_t k = 0; k < K; ++k) ST(exchange_sim(pl, false, k, ins, outs, st));
+    for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].A[k], cx(r), user));
+  for (size_t k = 0; k < K; ++k) ST(exchange_sim(pl, false, k, ins, outs, user));
   for (size_t k = 0; k < K; ++k)
-    for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].B[k], Ctx{ins[r], outs[r], pl->ranks[r].ws, nullptr}, st));
-  for (size_t k = 0; k < K; ++k) ST(exchange_sim(pl, true, k, ins, outs, st));
-  for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].C, Ctx{ins[r], outs[r], pl->ranks[r].ws, nullptr}, st));
+    for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].B[k], cx(r), user));
+  for (size_t k = 0; k < K; ++k) ST(exchange_sim(pl, true, k, ins, outs, user));
+  for (size_t r = 0; r < P; ++r) ST(launch(pl->ranks[r].C, cx(r), user));
   return DFFT_SUCCESS;
+}
+
+// ------------------------------------------------------------------------------ watchdog
+// A process-wide thread watches the executes of multi-rank plans.  If the oldest outstanding
+// execute of a plan makes no progress for the timeout (a peer died or never called execute), it
+// reports on stderr, marks the plan failed (later executes return DFFT_ERR_PEER), checks the NCCL
+// communicators for asynchronous errors, and releases the plan's waits by setting every flag word
+// of its windows, so the caller's streams drain instead of hanging; the results are then invalid.
+std::atomic<long long> g_timeout_ms{[] {
+  const char* v = getenv("DFFT_TIMEOUT_MS");
+  return v ? atoll(v) : 120000LL;
+}()};
+
+struct WdEntry {
+  cudaEvent_t ev;
+  std::chrono::steady_clock::time_point t;
+};
+struct Watchdog {
+  std::mutex mu;
+  std::map<dfft_plan_t, std::vector<WdEntry>> pending;  // per plan, oldest first
+  std::map<dfft_plan_t, std::chrono::steady_clock::time_point> progress;
+  std::thread th;
+  bool started = false;
+  void ensure() {
+    if (started) return;
+    started = true;
+    th = std::thread([this] { loop(); });
+    th.detach();
+  }
+  void loop();
+};
+Watchdog& watchdog() {
+  static Watchdog* w = new Watchdog;  // never destroyed: the detached thread outlives static teardown
+  return *w;
+}
+
+void release_flags(dfft_plan_t pl) {
+  if (!(pl->p2p || pl->ce)) return;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return;
+  const size_t words = (size_t)4 * pl->K * pl->P1 * pl->P2;
+  std::vector<unsigned int> ones(words, 1u);
+  for (RankPlan& rp : pl->ranks)
+    if (rp.ws) cudaMemcpyAsync(own_flags(pl, rp), ones.data(), words * 4, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+}
+
+void trigger_failure(dfft_plan_t pl, long long waited_ms) {
+  char buf[512];
+  std::string nccl_state;
+  if (pl->comm->world) {
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(pl->comm->world, &ar) == ncclSuccess && ar != ncclSuccess)
+      nccl_state = std::string("; NCCL async error: ") + ncclGetErrorString(ar);
+  }
+  snprintf(buf, sizeof buf,
+           "execute made no progress for %lld ms (rank %d of %d): a peer did not signal; waits released, "
+           "results invalid%s",
+           waited_ms, pl->comm->rank, pl->comm->nranks, nccl_state.c_str());
+  pl->fail_msg = buf;
+  pl->failed.store(1);
+  fprintf(stderr, "dfft watchdog: plan %p: %s\n", (void*)pl, buf);
+  release_flags(pl);
+  if (!nccl_state.empty()) {  // NCCL kernels of this comm may be stuck too: abort them
+    for (auto& kv : pl->comm->sub) {
+      if (kv.second.first) ncclCommAbort(kv.second.first);
+      if (kv.second.second) ncclCommAbort(kv.second.second);
+      kv.second = {nullptr, nullptr};
+    }
+  }
+}
+
+void Watchdog::loop() {
+  for (;;) {
+    std::this_thread::sleep_for(std::chrono::milliseconds(20));
+    std::lock_guard<std::mutex> lk(mu);
+    const auto now = std::chrono::steady_clock::now();
+    for (auto& kv : pending) {
+      dfft_plan_t pl = kv.first;
+      std::vector<WdEntry>& q = kv.second;
+      if (q.empty()) continue;
+      cudaSetDevice(pl->comm->device);
+      while (!q.empty()) {
+        const cudaError_t e = cudaEventQuery(q.front().ev);
+        if (e == cudaErrorNotReady) break;
+        if (e != cudaSuccess) (void)cudaGetLastError();
+        cudaEventDestroy(q.front().ev);
+        q.erase(q.begin());
+        progress[pl] = now;
+      }
+      if (q.empty() || pl->failed.load()) continue;
+      const auto since = std::max(q.front().t, progress[pl]);
+      const long long ms = std::chrono::duration_cast<std::chrono::milliseconds>(now - since).count();
+      if (ms > g_timeout_ms.load()) trigger_failure(pl, ms);
+    }
+  }
+}
+
+// register an execute (event recorded on the caller's stream after the join); not while the
+// stream is being captured into a graph (the execute happens at replay)
+dfft_status_t wd_track(dfft_plan_t pl, cudaStream_t user) {
+  if ((size_t)pl->P1 * pl->P2 <= 1) return DFFT_SUCCESS;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(user, &cs));
+  if (cs != cudaStreamCaptureStatusNone) return DFFT_SUCCESS;
+  Watchdog& w = watchdog();
+  std::lock_guard<std::mutex> lk(w.mu);
+  std::vector<WdEntry>& q = w.pending[pl];
+  if (q.size() >= 16) return DFFT_SUCCESS;  // the oldest entries already witness progress
+  cudaEvent_t e;
+  CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CU(cudaEventRecord(e, user));
+  q.push_back(WdEntry{e, std::chrono::steady_clock::now()});
+  w.ensure();
+  return DFFT_SUCCESS;
+}
+void wd_forget(dfft_plan_t pl) {
+  Watchdog& w = watchdog();
+  std::lock_guard<std::mutex> lk(w.mu);
+  auto it = w.pending.find(pl);
+  if (it == w.pending.end()) return;
+  for (WdEntry& e : it->second) cudaEventDestroy(e.ev);
+  w.pending.erase(it);
+  w.progress.erase(pl);
+}
+
+// ------------------------------------------------------------------------------ teardown
+void free_host_chain(dfft_plan_t pl) {
+  dfft_plan_s::HostChain* h = pl->host;
+  if (!h) return;
+  if (h->h2d) cudaStreamSynchronize(h->h2d);
+  if (h->d2h) cudaStreamSynchronize(h->d2h);
+  for (int b = 0; b < 2; ++b) {
+    if (h->in_dev[b]) cudaFree(h->in_dev[b]);
+    if (h->out_dev[b]) cudaFree(h->out_dev[b]);
+    for (cudaEvent_t e : {h->in_ready[b], h->in_free[b], h->out_ready[b], h->out_done[b]})
+      if (e) cudaEventDestroy(e);
+  }
+  for (void* m : h->mid)
+    if (m) cudaFree(m);
+  if (h->h2d) cudaStreamDestroy(h->h2d);
+  if (h->d2h) cudaStreamDestroy(h->d2h);
+  delete h;
+  pl->host = nullptr;
 }
 
 void free_stage(Stage& s) {
@@ -1760,19 +1986,47 @@ void free_stage(Stage& s) {
   s.in_tab = s.out_tab = nullptr;
 }
 
-void free_plan(dfft_plan_t pl) {
-  if (!pl) return;
-  if ((pl->p2p || pl->ce) && pl->epoch > 0 && pl->s_comp) {
-    // peers write their final `done` flags into this window after their last stage: wait for
-    // them so no peer store lands in freed memory
-    RankPlan& rp = pl->ranks[0];
-    for (int k = 0; k < (int)rp.A.size(); ++k) {
-      p2p_wait(pl, 1, 0, k, rp.E1[k].peers, pl->epoch, pl->s_comp);
-      p2p_wait(pl, 1, 1, k, rp.E2[k].peers, pl->epoch, pl->s_comp);
+// Peers write their final DONE flags into this window after their last stage: poll them (with the
+// watchdog's timeout) so no peer store lands in freed memory, then drain the plan's streams.
+void wait_peers_done(dfft_plan_t pl) {
+  if (!(pl->p2p || pl->ce) || pl->flag_off == 0) return;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return;
+  const size_t words = (size_t)4 * pl->K * pl->P1 * pl->P2;
+  std::vector<unsigned int> h(words);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (RankPlan& rp : pl->ranks) {
+    if (!rp.ws) continue;
+    for (;;) {
+      if (cudaMemcpyAsync(h.data(), own_flags(pl, rp), words * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+          cudaStreamSynchronize(s) != cudaSuccess)
+        break;
+      bool ok = true;
+      for (int e = 0; e < 2; ++e)
+        for (size_t k = 0; k < rp.A.size(); ++k)
+          for (int r : (e == 0 ? rp.E1[k] : rp.E2[k]).peers) ok = ok && h[flag_index(pl, kDone, e, (int)k, r)] >= 1;
+      if (ok) break;
+      const long long ms =
+          std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+      if (ms > g_timeout_ms.load()) {
+        fprintf(stderr, "dfft: destroy: peers did not finish within %lld ms; releasing\n", ms);
+        release_flags(pl);
+        break;
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
     }
   }
-  if (pl->s_comp) cudaStreamSynchronize(pl->s_comp);
-  if (pl->s_comm) cudaStreamSynchronize(pl->s_comm);
+  cudaStreamDestroy(s);
+}
+
+void free_plan(dfft_plan_t pl) {
+  if (!pl) return;
+  wd_forget(pl);
+  wait_peers_done(pl);
+  for (RankPlan& rp : pl->ranks) {
+    if (rp.sX) cudaStreamSynchronize(rp.sX);
+    if (rp.sY) cudaStreamSynchronize(rp.sY);
+  }
   if (!pl->comm->sim)
     for (size_t r = 0; r < pl->peer_ws.size(); ++r)
       if (pl->peer_ws[r] && (int)r != pl->comm->rank) cudaIpcCloseMemHandle(pl->peer_ws[r]);
@@ -1783,17 +2037,16 @@ void free_plan(dfft_plan_t pl) {
     free_stage(rp.C);
     for (Stage& c : rp.Cc) free_stage(c);
     if (rp.ws) cudaFree(rp.ws);
+    for (cudaEvent_t e : rp.ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : {rp.ev_fork, rp.ev_join[0], rp.ev_join[1]})
+      if (e) cudaEventDestroy(e);
+    if (rp.sX) cudaStreamDestroy(rp.sX);
+    if (rp.sY) cudaStreamDestroy(rp.sY);
   }
-  for (auto* v : {&pl->evA, &pl->evE1, &pl->evB, &pl->evE2})
-    for (cudaEvent_t e : *v) cudaEventDestroy(e);
   for (cudaEvent_t e : pl->prof_ev) cudaEventDestroy(e);
-  for (cudaEvent_t e : {pl->ev_fork, pl->ev_join_comp, pl->ev_join_comm})
-    if (e) cudaEventDestroy(e);
-  if (pl->s_comp) cudaStreamDestroy(pl->s_comp);
-  if (pl->s_comm) cudaStreamDestroy(pl->s_comm);
+  for (cudaEvent_t e : pl->prof_origin) cudaEventDestroy(e);
   if (pl->spec_tab) cudaFree(pl->spec_tab);
-  if (pl->stage_in) cudaFree(pl->stage_in);
-  if (pl->stage_out) cudaFree(pl->stage_out);
+  free_host_chain(pl);
   delete pl;
 }
 
@@ -1806,10 +2059,12 @@ struct PlanGuard {
 
 // Fused-store plans with K > 1 run stage A(k+1) and B(k) concurrently on two streams.  The one
 // of the pair that stores to peers (NVLink-bound) gets at most DFFT_NVL_SMS SMs (default 80) and
-// the HBM-bound one the rest, except in the last chunk, which runs alone.
+// the HBM-bound one the rest, except in the last chunk, which runs alone.  Without overlap every
+// stage runs alone on the whole GPU.
 dfft_status_t apply_sm_caps(dfft_plan_t pl, RankPlan& rp) {
   const size_t K = rp.A.size();
-  if (!pl->p2p || K < 2) return DFFT_SUCCESS;
+  if (!pl->p2p || K < 2 || !pl->overlap) return DFFT_SUCCESS;
+
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->comm->device));
   const char* v = getenv("DFFT_NVL_SMS");
@@ -1853,6 +2108,7 @@ const char* dfft_status_string(dfft_status_t s) {
     case DFFT_ERR_CUDA: return "CUDA error";
     case DFFT_ERR_NCCL: return "NCCL error";
     case DFFT_ERR_INTERNAL: return "internal error";
+    case DFFT_ERR_PEER: return "plan failed (a peer did not signal, or an enqueue failed)";
   }
   return "unknown status";
 }
@@ -1980,16 +2236,18 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   int Kreq = (int)(flags & 0xff);
   bool overlap = !(flags & DFFT_FLAG_NO_OVERLAP);
   long long kmax = direction == DFFT_FORWARD ? nz / p2 : nxc / p1;  // chunk axis extent
-  // exchange transport for P > 1: copy engines into IPC windows (default),
-  // fused epilogue stores into the windows (DFFT_FLAG_FUSED_STORE), or NCCL (DFFT_FLAG_NCCL)
+  // exchange transport for P > 1: fused epilogue stores into the peers' IPC
+  // windows (default; DFFT_FLAG_FUSED_STORE), copy engines into the windows (DFFT_FLAG_CE), CE
+  // with a fused forward x-FFT (DFFT_FLAG_HYBRID), or NCCL send/recv (DFFT_FLAG_NCCL)
   const char* exch_env = getenv("DFFT_EXCHANGE");
   auto env_is = [&](const char* v) { return exch_env && strcmp(exch_env, v) == 0; };
   const bool want_fused = (flags & DFFT_FLAG_FUSED_STORE) || (!comm->sim && env_is("p2p"));
-  // simulated ranks run the NCCL layouts, or (DFFT_FLAG_FUSED_STORE) the fused-store layouts with
-  // every rank's workspace standing in for its IPC window (same kernels, same addresses)
-  const bool nccl_mode = (comm->sim && !want_fused) || P == 1 || (flags & DFFT_FLAG_NCCL) || env_is("nccl");
-  const bool want_ce = !comm->sim && ((flags & DFFT_FLAG_CE) || env_is("ce"));
-  const bool want_hybrid = !comm->sim && ((flags & DFFT_FLAG_HYBRID) || env_is("hybrid"));
+  const bool want_ce = (flags & DFFT_FLAG_CE) || (!comm->sim && env_is("ce"));
+  const bool want_hybrid = (flags & DFFT_FLAG_HYBRID) || (!comm->sim && env_is("hybrid"));
+  // simulated ranks run the NCCL layouts, or (DFFT_FLAG_FUSED_STORE / _CE / _HYBRID) the IPC-window
+  // layouts and schedules with every rank's workspace standing in for its window
+  const bool nccl_mode =
+      (comm->sim && !want_fused && !want_ce && !want_hybrid) || P == 1 || (flags & DFFT_FLAG_NCCL) || env_is("nccl");
   // automatic choice (measured r01, 1024^3 c64): fused epilogue stores into column-blocked
   // windows beat the copy engine on every grid (1x2: 16.1 vs 18.0 ms, 2x2: 9.4 vs 16.9 ms)
   const bool auto_fused = !comm->sim && !want_ce && !want_fused && !want_hybrid;
@@ -2052,25 +2310,11 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
     if (f64 ? lookup_kernel_f64(kStrided, (int)nz, direction, &kz) : lookup_kernel_f32(kStrided, (int)nz, direction, &kz))
       g.wz = kz.tma_fn ? kz.tma_w : kz.per_cta;
   }
-  if (p2p_mode) g.xq = std::max(g.wy, g.wz);
+  // chunk bounds along x at multiples of both column-block widths, so every chunk is a whole
+  // number of blocks of each window layout (R2 by wy, R2' by wz, R1' by wy)
+  if (p2p_mode) g.xq = std::lcm(g.wy, g.wz);
 
-  if (!comm->sim && P > 1) {
-    // collective consistency check: every rank must pass identical arguments
-    unsigned long long h = 1469598103934665603ULL;
-    for (long long v : {(long long)nx, (long long)ny, (long long)nz, (long long)decomp, (long long)p1,
-                        (long long)p2, (long long)type, (long long)direction, (long long)flags}) {
-      h ^= (unsigned long long)v;
-      h *= 1099511628211ULL;
-    }
-    unsigned long long* d = nullptr;
-    CU(cudaMalloc(&d, sizeof(unsigned long long) * (P + 1)));
-    CU(cudaMemcpy(d, &h, sizeof h, cudaMemcpyHostToDevice));
-    NC(ncclAllGather(d, d + 1, 1, ncclUint64, comm->world, 0));
-    std::vector<unsigned long long> all(P);
-    CU(cudaMemcpy(all.data(), d + 1, sizeof(unsigned long long) * P, cudaMemcpyDeviceToHost));
-    cudaFree(d);
-    for (int r = 0; r < P; ++r)
-      if (all[r] != h) return fail(DFFT_ERR_INVALID_VALUE, "plan arguments differ between rank %d and rank %d", comm->rank, r);
+  if (!comm->sim && P > 1) {  // row / column sub-communicators, shared by the comm's plans
     auto key = std::make_pair(p1, p2);
     auto it = comm->sub.find(key);
     if (it == comm->sub.end()) {
@@ -2106,7 +2350,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       memcpy(rp.out_n, d3n, sizeof d3n);
       rp.in_bytes = d1b;
       rp.out_bytes = d3b;
-      ST(P == 1 ? (single_blocked_ok(pl, g) ? build_single_blocked(pl, g, rp) : build_single(pl, g, rp))
+      ST(P == 1 ? build_single(pl, g, rp)
                 : pl->bc ? build_forward_bc(pl, g, rp) : build_forward(pl, g, rp));
     } else {
       memcpy(rp.in_lo, d3lo, sizeof d3lo);
@@ -2115,23 +2359,65 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       memcpy(rp.out_n, d1n, sizeof d1n);
       rp.in_bytes = d3b;
       rp.out_bytes = d1b;
-      ST(P == 1 ? (single_blocked_ok(pl, g) ? build_single_blocked(pl, g, rp) : build_single(pl, g, rp))
+      ST(P == 1 ? build_single(pl, g, rp)
                 : pl->bc ? build_inverse_bc(pl, g, rp) : build_inverse(pl, g, rp));
     }
     ST(apply_sm_caps(pl, rp));
+    build_schedule(pl, rp);
     if (rp.ws_bytes) {
       cudaError_t e = cudaMalloc(&rp.ws, rp.ws_bytes);
       if (e != cudaSuccess) return fail(DFFT_ERR_ALLOC, "workspace of %zu bytes: %s", rp.ws_bytes, cudaGetErrorString(e));
     }
+    if (pl->p2p || pl->ce) {  // flag block: READY = 0, DONE = 1 (before any peer can see the window)
+      const std::vector<unsigned int> fl = initial_flags(pl);
+      CU(cudaMemcpy((char*)rp.ws + pl->flag_off, fl.data(), fl.size() * 4, cudaMemcpyHostToDevice));
+    }
+    if (two_streams(pl)) {
+      CU(cudaStreamCreateWithFlags(&rp.sX, cudaStreamNonBlocking));
+      CU(cudaStreamCreateWithFlags(&rp.sY, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&rp.ev_fork, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&rp.ev_join[0], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&rp.ev_join[1], cudaEventDisableTiming));
+      rp.ev.resize(rp.nev);
+      for (auto& e : rp.ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
   }
-  if (comm->sim && pl->p2p) {
-    // simulated fused stores: rank q's "window" is its workspace on this device
+  {  // hash of the resolved plan state: transport, pipeline, chunking, window layout, schedule
+    unsigned long long h = 1469598103934665603ULL;
+    auto mix = [&](long long v) {
+      h ^= (unsigned long long)v;
+      h *= 1099511628211ULL;
+    };
+    for (long long v : {(long long)nx, (long long)ny, (long long)nz, (long long)decomp, (long long)p1, (long long)p2,
+                        (long long)type, (long long)direction, (long long)flags, (long long)pl->p2p, (long long)pl->ce,
+                        (long long)pl->hybrid, (long long)pl->bc, (long long)pl->overlap, K, g.wy, g.wz, g.xq,
+                        (long long)pl->flag_off, (long long)pl->ranks[0].sched.size()})
+      mix(v);
+    pl->hash = h;
+  }
+  if (!comm->sim && P > 1) {
+    // collective consistency check: every rank must resolve an identical plan (arguments, flags,
+    // and the env-dependent transport / pipeline choices), else peers would address the wrong
+    // window offsets or wait on flags that never come
+    unsigned long long* d = nullptr;
+    CU(cudaMalloc(&d, sizeof(unsigned long long) * (P + 1)));
+    CU(cudaMemcpy(d, &pl->hash, sizeof pl->hash, cudaMemcpyHostToDevice));
+    NC(ncclAllGather(d, d + 1, 1, ncclUint64, comm->world, 0));
+    std::vector<unsigned long long> all(P);
+    CU(cudaMemcpy(all.data(), d + 1, sizeof(unsigned long long) * P, cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    for (int r = 0; r < P; ++r)
+      if (all[r] != pl->hash)
+        return fail(DFFT_ERR_INVALID_VALUE, "plan differs between rank %d and rank %d (arguments, flags or DFFT_* env)",
+                    comm->rank, r);
+  }
+  if (comm->sim && (pl->p2p || pl->ce)) {
+    // simulated windows: rank q's "window" is its workspace on this device
     pl->peer_ws.resize(P);
     for (int q = 0; q < P; ++q) pl->peer_ws[q] = pl->ranks[q].ws;
   } else if (pl->p2p || pl->ce) {
     // every workspace becomes an IPC window; open the windows of the row and column peers
     RankPlan& rp = pl->ranks[0];
-    CU(cudaMemset((char*)rp.ws + pl->flag_off, 0, flag_bytes(g)));
     cudaIpcMemHandle_t h;
     CU(cudaIpcGetMemHandle(&h, rp.ws));
     char* d = nullptr;
@@ -2150,15 +2436,6 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
       if (e != cudaSuccess) return fail(DFFT_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
     }
   }
-  CU(cudaStreamCreateWithFlags(&pl->s_comp, cudaStreamNonBlocking));
-  CU(cudaStreamCreateWithFlags(&pl->s_comm, cudaStreamNonBlocking));
-  for (auto* v : {&pl->evA, &pl->evE1, &pl->evB, &pl->evE2}) {
-    v->resize(K);
-    for (auto& e : *v) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
-  CU(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming));
-  CU(cudaEventCreateWithFlags(&pl->ev_join_comp, cudaEventDisableTiming));
-  CU(cudaEventCreateWithFlags(&pl->ev_join_comm, cudaEventDisableTiming));
   CU(cudaDeviceSynchronize());
   guard.p = nullptr;
   *plan = pl;
@@ -2209,38 +2486,117 @@ static dfft_status_t check_ptrs(dfft_plan_t pl, const RankPlan& rp, const void* 
   return DFFT_SUCCESS;
 }
 
+static dfft_status_t check_usable(dfft_plan_t pl) {
+  if (pl->failed.load()) return fail(DFFT_ERR_PEER, "plan failed earlier: %s", pl->fail_msg.c_str());
+  if (pl->comm->world && !pl->p2p && !pl->ce && pl->comm->nranks > 1) {
+    ncclResult_t ar = ncclSuccess;
+    NC(ncclCommGetAsyncError(pl->comm->world, &ar));
+    if (ar != ncclSuccess) return fail(DFFT_ERR_NCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ar));
+  }
+  return DFFT_SUCCESS;
+}
+
 dfft_status_t dfft_execute(dfft_plan_t pl, const void* in, void* out, void* stream) {
   if (!pl) return fail(DFFT_ERR_INVALID_VALUE, "null plan");
   if (pl->comm->sim) return fail(DFFT_ERR_INVALID_VALUE, "simulated-comm plan: use dfft_execute_sim");
+  ST(check_usable(pl));
   ST(check_ptrs(pl, pl->ranks[0], in, out));
+  CU(cudaSetDevice(pl->comm->device));
   ST(execute_rank(pl, in, out, (cudaStream_t)stream));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(DFFT_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
+  return wd_track(pl, (cudaStream_t)stream);
+}
+
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+dfft_status_t dfft_execute_host_chain(const dfft_plan_t* plans, int nplans, const void* in_host, void* out_host,
+                                      void* stream, int async) {
+  if (!plans || nplans < 1 || !in_host || !out_host) return fail(DFFT_ERR_INVALID_VALUE, "null argument");
+  for (int q = 0; q < nplans; ++q) {
+    if (!plans[q]) return fail(DFFT_ERR_INVALID_VALUE, "null plan %d", q);
+    if (plans[q]->comm->sim) return fail(DFFT_ERR_INVALID_VALUE, "simulated-comm plan");
+    if (plans[q]->comm->device != plans[0]->comm->device) return fail(DFFT_ERR_INVALID_VALUE, "plans on different devices");
+    if (q > 0 && plans[q]->ranks[0].in_bytes != plans[q - 1]->ranks[0].out_bytes)
+      return fail(DFFT_ERR_INVALID_VALUE, "plan %d's input box does not match plan %d's output box", q, q - 1);
+  }
+  if (async && (!host_pinned(in_host) || !host_pinned(out_host)))
+    return fail(DFFT_ERR_INVALID_VALUE, "asynchronous host execution needs page-locked (pinned) host buffers");
+  dfft_plan_t p0 = plans[0];
+  CU(cudaSetDevice(p0->comm->device));
+  const size_t in_b = std::max<size_t>(p0->ranks[0].in_bytes, 16);
+  const size_t out_b = std::max<size_t>(plans[nplans - 1]->ranks[0].out_bytes, 16);
+  dfft_plan_s::HostChain* h = p0->host;
+  if (h && h->plans != std::vector<dfft_plan_s*>(plans, plans + nplans)) {  // another chain: rebuild
+    free_host_chain(p0);
+    h = nullptr;
+  }
+  if (!h) {
+    h = p0->host = new dfft_plan_s::HostChain;
+    h->plans.assign(plans, plans + nplans);
+    for (int b = 0; b < 2; ++b) {
+      CU(cudaMalloc(&h->in_dev[b], in_b));
+      CU(cudaMalloc(&h->out_dev[b], out_b));
+      for (cudaEvent_t* e : {&h->in_ready[b], &h->in_free[b], &h->out_ready[b], &h->out_done[b]})
+        CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    for (int q = 0; q + 1 < nplans; ++q) {
+      void* m = nullptr;
+      CU(cudaMalloc(&m, std::max<size_t>(plans[q]->ranks[0].out_bytes, 16)));
+      h->mid.push_back(m);
+    }
+    CU(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking));
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int b = (int)(h->calls++ & 1);
+  // host -> device on the copy stream, once the call two back has consumed this buffer
+  CU(cudaStreamWaitEvent(h->h2d, h->in_free[b], 0));
+  CU(cudaMemcpyAsync(h->in_dev[b], in_host, p0->ranks[0].in_bytes, cudaMemcpyHostToDevice, h->h2d));
+  CU(cudaEventRecord(h->in_ready[b], h->h2d));
+  CU(cudaStreamWaitEvent(st, h->in_ready[b], 0));
+  for (int q = 0; q < nplans; ++q) {
+    const void* src = q == 0 ? h->in_dev[b] : h->mid[q - 1];
+    void* dst = q + 1 == nplans ? h->out_dev[b] : h->mid[q];
+    ST(dfft_execute(plans[q], src, dst, stream));
+    if (q == 0) CU(cudaEventRecord(h->in_free[b], st));
+  }
+  // device -> host on the other copy stream; the caller's stream completes when it has landed
+  CU(cudaEventRecord(h->out_ready[b], st));
+  CU(cudaStreamWaitEvent(h->d2h, h->out_ready[b], 0));
+  CU(cudaMemcpyAsync(out_host, h->out_dev[b], plans[nplans - 1]->ranks[0].out_bytes, cudaMemcpyDeviceToHost, h->d2h));
+  CU(cudaEventRecord(h->out_done[b], h->d2h));
+  CU(cudaStreamWaitEvent(st, h->out_done[b], 0));
+  if (!async) CU(cudaStreamSynchronize(st));
   return DFFT_SUCCESS;
 }
 
 dfft_status_t dfft_execute_host(dfft_plan_t pl, const void* in_host, void* out_host, void* stream) {
-  if (!pl || !in_host || !out_host) return fail(DFFT_ERR_INVALID_VALUE, "null argument");
-  if (pl->comm->sim) return fail(DFFT_ERR_INVALID_VALUE, "simulated-comm plan");
-  const RankPlan& rp = pl->ranks[0];
-  if (!pl->stage_in) CU(cudaMalloc(&pl->stage_in, std::max<size_t>(rp.in_bytes, 16)));
-  if (!pl->stage_out) CU(cudaMalloc(&pl->stage_out, std::max<size_t>(rp.out_bytes, 16)));
-  cudaStream_t st = (cudaStream_t)stream;
-  CU(cudaMemcpyAsync(pl->stage_in, in_host, rp.in_bytes, cudaMemcpyHostToDevice, st));
-  ST(dfft_execute(pl, pl->stage_in, pl->stage_out, stream));
-  CU(cudaMemcpyAsync(out_host, pl->stage_out, rp.out_bytes, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
-  return DFFT_SUCCESS;
+  if (!pl) return fail(DFFT_ERR_INVALID_VALUE, "null plan");
+  return dfft_execute_host_chain(&pl, 1, in_host, out_host, stream, 0);
 }
 
 dfft_status_t dfft_execute_sim(dfft_plan_t pl, const void* const* ins, void* const* outs, void* stream) {
   if (!pl || !ins || !outs) return fail(DFFT_ERR_INVALID_VALUE, "null argument");
   if (!pl->comm->sim) return fail(DFFT_ERR_INVALID_VALUE, "not a simulated-comm plan");
-  for (size_t r = 0; r < pl->ranks.size(); ++r) ST(check_ptrs(pl, pl->ranks[r], ins[r], outs[r]));
+  ST(check_usable(pl));
+  const bool windows = pl->p2p || pl->ce;
+  for (size_t r = 0; r < pl->ranks.size(); ++r) {
+    if (!ins[r] && windows) continue;  // a failed (non-executing) simulated peer
+    ST(check_ptrs(pl, pl->ranks[r], ins[r], outs[r]));
+  }
+  CU(cudaSetDevice(pl->comm->device));
   ST(execute_sim(pl, ins, outs, (cudaStream_t)stream));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(DFFT_ERR_CUDA, "launch: %s", cudaGetErrorString(e));
-  return DFFT_SUCCESS;
+  return wd_track(pl, (cudaStream_t)stream);
 }
 
 dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double dz) {
@@ -2283,7 +2639,6 @@ dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double
       for (int q = 0; q < 3; ++q)
         s->a.spec[q] = on ? (const void*)((const char*)pl->spec_tab + (size_t)(base[s->gax[q]] + s->glo[q]) * rs)
                           : nullptr;
-      if (on && s->tma_variant == 2) s->tma_grid = 0;  // the two-group kernel has no multiplier
     }
   }
   if (nlast == 0) return fail(DFFT_ERR_INTERNAL, "plan has no last forward stage");
@@ -2298,14 +2653,8 @@ dfft_status_t dfft_plan_set_profiling(dfft_plan_t pl, int on) {
 
 dfft_status_t dfft_plan_phase_times(dfft_plan_t pl, double ms[5], long long launches[5], int reset) {
   if (!pl || !ms) return fail(DFFT_ERR_INVALID_VALUE, "null argument");
-  for (size_t i = 0; i < pl->prof_used; ++i) {
-    CU(cudaEventSynchronize(pl->prof_ev[2 * i + 1]));
-    float t = 0;
-    CU(cudaEventElapsedTime(&t, pl->prof_ev[2 * i], pl->prof_ev[2 * i + 1]));
-    pl->prof_ms[pl->prof_phase[i]] += t;
-    pl->prof_n[pl->prof_phase[i]] += 1;
-  }
-  pl->prof_used = 0;
+  ST(prof_resolve(pl));
+  if (reset) pl->prof_spans.clear();
   for (int q = 0; q < 5; ++q) {
     ms[q] = pl->prof_ms[q];
     if (launches) launches[q] = pl->prof_n[q];
@@ -2315,6 +2664,29 @@ dfft_status_t dfft_plan_phase_times(dfft_plan_t pl, double ms[5], long long laun
     }
   }
   return DFFT_SUCCESS;
+}
+
+dfft_status_t dfft_plan_timeline(dfft_plan_t pl, dfft_span_t* spans, int cap, int* n) {
+  if (!pl || !n || (cap > 0 && !spans)) return fail(DFFT_ERR_INVALID_VALUE, "null argument");
+  ST(prof_resolve(pl));
+  *n = (int)pl->prof_spans.size();
+  if (cap <= 0) return DFFT_SUCCESS;  // size query
+  const int m = std::min(cap, *n);
+  std::copy(pl->prof_spans.begin(), pl->prof_spans.begin() + m, spans);
+  pl->prof_spans.erase(pl->prof_spans.begin(), pl->prof_spans.begin() + m);
+  *n = m;
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t dfft_set_timeout_ms(long long ms) {
+  if (ms <= 0) return fail(DFFT_ERR_INVALID_VALUE, "timeout must be positive");
+  g_timeout_ms.store(ms);
+  return DFFT_SUCCESS;
+}
+
+dfft_status_t dfft_plan_status(dfft_plan_t pl) {
+  if (!pl) return fail(DFFT_ERR_INVALID_VALUE, "null plan");
+  return check_usable(pl);
 }
 
 dfft_status_t dfft_plan_stage_bytes(dfft_plan_t pl, double bytes[5]) {
@@ -2327,17 +2699,26 @@ dfft_status_t dfft_plan_stage_bytes(dfft_plan_t pl, double bytes[5]) {
     double elems = (double)s.a.L0 * (double)s.a.L1 * (double)s.n;  // complex elements of the FFT
     return 2.0 * elems * (double)pl->es;
   };
-  auto xch_b = [&](const Exchange& x) {
-    double b = 0;
-    for (const Xfer& t : x.sends) b += (double)t.bytes;
-    return b;
-  };
+  // off-rank bytes of each exchange from the rank's boxes (identical for every transport; with
+  // fused stores they leave inside stage A's resp. stage B's epilogue)
+  const bool fwd = pl->dir == DFFT_FORWARD;
+  const int64_t* d1 = fwd ? rp.in_n : rp.out_n;  // (nx, Y1n, Zn)
+  const int64_t* d3 = fwd ? rp.out_n : rp.in_n;  // (Xn, Y3n, nz)
+  const double nxc = pl->r2c ? (double)(pl->nx / 2 + 1) : pl->r2r ? (double)(pl->nx / 2) : (double)pl->nx;
+  const double Xn = (double)d3[0] / (pl->r2r ? 2.0 : 1.0), Y3n = (double)d3[1];
+  const double Y1n = (double)d1[1], Zn = (double)d1[2];
+  const double es = (double)pl->es;
   for (int q = 0; q < 5; ++q) bytes[q] = 0;
+  if (fwd) {
+    bytes[1] = Y1n * Zn * (nxc - Xn) * es;
+    bytes[3] = Xn * Zn * ((double)pl->ny - Y3n) * es;
+  } else {
+    bytes[1] = Xn * Y3n * ((double)pl->nz - Zn) * es;
+    bytes[3] = Xn * Zn * ((double)pl->ny - Y1n) * es;
+  }
   for (size_t k = 0; k < rp.A.size(); ++k) {
     bytes[0] += stage_b(rp.A[k]);
-    bytes[1] += xch_b(rp.E1[k]);
     bytes[2] += stage_b(rp.B[k]);
-    bytes[3] += xch_b(rp.E2[k]);
   }
   bytes[4] = stage_b(rp.C);
   for (const Stage& c : rp.Cc) bytes[4] += stage_b(c);

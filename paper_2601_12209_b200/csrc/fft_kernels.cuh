@@ -921,17 +921,13 @@ template <typename Real, int N> struct TmaCfg {
   static constexpr bool OK = S.npass >= 2 && THREADS <= 1024 && SMEM <= 227 * 1024 && 2 * W <= 256;
 };
 
-// OM 3 (TMA stores, stage as output): the last pass writes the tile back into its own stage
-// buffer (drained by pass 0), the TMA store reads it from there, and thread 0 refills the
-// previous tile's stage right after its own pass-0 loads — two CTA barriers per tile instead
-// of four (ncu r01: barrier stalls were the top stall reason at 8 warps/SM).
 // DCT (R2R strided stages on the TMA kernel, OM 1 only): -1 forward (permuted loads from the
 // stage; the (k, N−k) post-processing runs on the output tile before the TMA store), +1 inverse
 // (V from stage rows t and N−t in the loads, permuted rows in the stores).
 template <typename C, int W, int OM, bool SPEC = false, int N_ = 0, int DCT = 0> struct TmaIO : GIO<C, false, SPEC> {
-  static constexpr bool kSyncAfterLoad = OM != 3;
-  static constexpr bool kRefillNoSync = OM == 3;
-  static constexpr bool kLastBar = OM != 3;
+  static constexpr bool kSyncAfterLoad = true;
+  static constexpr bool kRefillNoSync = false;
+  static constexpr bool kLastBar = true;
   const C* stage;  // this tile's stage buffer, dense [t][W]
   C* obuf;         // OM > 0: dense [t][W] output tile, written by a TMA tensor store (1) or bulk copies (2)
   int c;
@@ -968,7 +964,6 @@ template <typename C, int W, int OM, bool SPEC = false, int N_ = 0, int DCT = 0>
   }
   __device__ __forceinline__ void after_load() {
     if (refill && threadIdx.x == 0) {
-      if constexpr (OM == 3) bulk_wait_read0();  // the previous tile's store has read that stage
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(mbar, bytes);
       for (int q = 0; q < nbox; ++q)
@@ -993,7 +988,6 @@ __global__ void __launch_bounds__(TmaCfg<Real, N>::THREADS)
 fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
                        const __grid_constant__ PassArgs a) {
   constexpr bool TST = OM != 0;
-  constexpr bool SOUT = OM == 3;  // stage-as-output flow
   using C = typename CT<Real>::type;
   using Cfg = TmaCfg<Real, N>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1032,19 +1026,18 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     tile_coords(tile, ntile, a.L1, a.g0, tx, l1);
     const long long l0 = tx * Cfg::W + c;
     const bool active = l0 < a.L0;
-    if (TST && !SOUT && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
+    if (TST && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
     TmaIO<C, Cfg::W, OM, SPEC, N, DCT> io;
     io.tw3 = reinterpret_cast<const C*>(a.tw3);
     io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
     io.spectral(a, active ? l0 : 0, l1);
     io.stage = stages + s * Cfg::STAGE_ELEMS;
-    io.obuf = SOUT ? stages + s * Cfg::STAGE_ELEMS : work;
+    io.obuf = work;
     io.c = c;
-    // refill: the drained stage gets the tile NS steps ahead (SOUT: the previous tile's stage,
-    // free once its store has read it, gets the next tile)
-    const int rs = SOUT ? (it + Cfg::NS - 1) % Cfg::NS : s;
-    const long long next = SOUT ? tile + gridDim.x : tile + (long long)Cfg::NS * gridDim.x;
-    io.refill = next < total && (!SOUT || it >= Cfg::NS - 1);
+    // refill: the drained stage gets the tile NS steps ahead
+    const int rs = s;
+    const long long next = tile + (long long)Cfg::NS * gridDim.x;
+    io.refill = next < total;
     io.tmap = &tmap;
     io.mbar = &bars[rs];
     io.stage_ptr = stages + rs * Cfg::STAGE_ELEMS;
@@ -1082,9 +1075,9 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
       __syncthreads();
       if (threadIdx.x == 0) {
-        if constexpr (OM == 1 || OM == 3) {
+        if constexpr (OM == 1) {
           const int c0 = (int)(tx * Cfg::W * 2);
-          const C* src = SOUT ? stages + s * Cfg::STAGE_ELEMS : work;
+          const C* src = work;
           for (int q = 0; q < Cfg::NBOX; ++q)
             tma_store_tile(&omap, a.out.bw, c0, q * Cfg::BOXR, (int)l1, src + q * Cfg::BOXR * Cfg::W);
         } else {
@@ -1100,146 +1093,6 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     }
   }
   if (TST && threadIdx.x == 0) bulk_wait0();
-}
-
-// ------------------------------------------------------------------ strided family, 2 warp groups
-// Two independent warp groups per CTA each run their own tile (named barriers, no CTA-wide sync),
-// so one group's barrier stalls are covered by the other's work (the single-group TMA kernel was
-// barrier-bound at 8-16 warps/SM, ncu r01).  The FFT runs in place in the stage buffer: TMA lands
-// each box of R0 rows at a padded offset, giving the conflict-free layout t·W + c + (t/R0)·PAD
-// directly, so no separate work buffer is needed and three stage buffers fit: two being
-// computed.  Tile it (it-th of this CTA) is processed by group it % 2 in that group's buffer; the
-// group refills its buffer with its next tile as soon as its TMA store has read it, and the other
-// group's compute covers the load latency.
-__device__ __forceinline__ void named_bar(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-template <typename Real, int N> struct Tma2Cfg {
-  static constexpr int ES = (int)sizeof(Real) * 2;
-  static constexpr int MAXR = (ES == 8 && N >= 512 && N % 32 == 0) ? 32 : 16;
-  static constexpr Sched S = make_sched(N, MAXR);
-  static constexpr int W0 = 64 / ES;
-  // 64 B rows, widened (power of 2) only for short lines so a group has >= 128 threads
-  static constexpr int W = S.T * W0 >= 128 ? W0 : (S.T * 2 * W0 >= 128 ? 2 * W0 : S.T * 4 * W0 >= 128 ? 4 * W0 : 8 * W0);
-  static constexpr int GT = S.T * W;  // threads per group
-#ifndef DFFT_TMA2_GROUPS
-#define DFFT_TMA2_GROUPS 2
-#endif
-  static constexpr int NG = DFFT_TMA2_GROUPS;
-  static constexpr int THREADS = NG * GT;
-  // dense [t][W] stage (TMA destinations must be 128 B aligned, which rules out the 64-B-mod-128
-  // padding; the in-place pass-0 scatter then has 2-way bank conflicts on 64 B rows)
-  static constexpr int R0 = largest_divisor_le(N, 256);  // rows per TMA box
-  static constexpr int PAD = 0;
-  static constexpr int NBOX = N / R0;
-  static constexpr int BOX_ELEMS = R0 * W;
-  static constexpr int STAGE_ELEMS = NBOX * BOX_ELEMS;
-  // one stage buffer per group: each group refills its own buffer, so the mbarrier phases of a
-  // buffer advance in step with its single consumer (buffers shared round-robin between groups
-  // let one group run two phases ahead and pass a parity wait spuriously)
-  static constexpr int NSTAGE = NG;
-  static constexpr size_t SMEM = (size_t)NSTAGE * STAGE_ELEMS * ES + NSTAGE * 8 + 16;
-  static constexpr bool OK = S.npass >= 2 && THREADS <= 1024 && SMEM <= 227 * 1024 && 2 * W <= 256 &&
-                             R0 <= 256 && N % R0 == 0 && THREADS <= 512;
-};
-
-template <typename C, int W, int R0, int PAD, bool TST> struct Tma2IO : GIO<C> {
-  static constexpr bool kSyncAfterLoad = true;  // the gather and the in-place writes of pass 0
-  C* buf;
-  int c, gbar, gthreads;
-  __device__ __forceinline__ int sidx(int t) const { return t * W + c; }
-  __device__ __forceinline__ C load(int t) const { return buf[sidx(t)]; }
-  __device__ __forceinline__ void store(int t, C v) const {
-    if constexpr (TST) {
-      if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
-      buf[sidx(t)] = v;
-    } else {
-      GIO<C>::store(t, v);
-    }
-  }
-  __device__ __forceinline__ void bar() const { named_bar(gbar, gthreads); }
-};
-
-template <typename Real, int N, int DIR, bool TST>
-__global__ void __launch_bounds__(Tma2Cfg<Real, N>::THREADS)
-fft_strided_tma2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
-                        const __grid_constant__ PassArgs a) {
-  using C = typename CT<Real>::type;
-  using Cfg = Tma2Cfg<Real, N>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* stages = reinterpret_cast<C*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(stages + Cfg::NSTAGE * Cfg::STAGE_ELEMS);
-  const int g = threadIdx.x / Cfg::GT;        // warp group
-  const int lt = threadIdx.x - g * Cfg::GT;   // thread within the group
-  const int c = lt % Cfg::W;
-  const int j = lt / Cfg::W;
-  const bool leader = lt == 0;
-  const long long ntile = (a.L0 + Cfg::W - 1) / Cfg::W;
-  const long long total = ntile * a.L1;
-  constexpr uint32_t kBytes = (uint32_t)(Cfg::NBOX * Cfg::R0 * Cfg::W * Cfg::ES);
-  auto coords = [&](long long tile, int& c0, int& l1) {
-    long long tx, q;
-    tile_coords(tile, ntile, a.L1, a.g0, tx, q);
-    l1 = (int)q;
-    c0 = (int)(tx * Cfg::W * 2);  // TMA coordinates are in reals
-  };
-  auto issue = [&](long long tile, int b) {
-    int c0, l1;
-    coords(tile, c0, l1);
-    C* dst = stages + b * Cfg::STAGE_ELEMS;
-    mbar_expect_tx(&full[b], kBytes);
-    for (int q = 0; q < Cfg::NBOX; ++q)
-      tma_load_tile(dst + q * Cfg::BOX_ELEMS, &tmap, a.in.bw, c0, q * Cfg::R0, l1, &full[b]);
-  };
-  if (threadIdx.x == 0) {
-    for (int b = 0; b < Cfg::NSTAGE; ++b) mbar_init(&full[b], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int b = 0; b < Cfg::NSTAGE; ++b) {
-      const long long tile = blockIdx.x + (long long)b * gridDim.x;
-      if (tile < total) issue(tile, b);
-    }
-  }
-  __syncthreads();
-  for (int it = g;; it += Cfg::NG) {
-    const long long tile = blockIdx.x + (long long)it * gridDim.x;
-    if (tile >= total) break;
-    const int b = it % Cfg::NSTAGE;
-    const uint32_t parity = (uint32_t)((it / Cfg::NSTAGE) & 1);
-    int c0, l1i;
-    coords(tile, c0, l1i);
-    const long long l0 = (long long)(c0 / 2) + c;
-    const bool active = l0 < a.L0;
-    Tma2IO<C, Cfg::W, Cfg::R0, Cfg::PAD, TST> io;
-    io.init(a.in, a.out, active ? l0 : 0, l1i, a.scale);
-    io.buf = stages + b * Cfg::STAGE_ELEMS;
-    io.c = c;
-    io.gbar = 1 + g;
-    io.gthreads = Cfg::GT;
-    mbar_wait(&full[b], parity);
-    StridedSM<Cfg::W, 1, 0> sm{c};
-    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, io.buf, reinterpret_cast<const C*>(a.tw), j, active);
-    if constexpr (TST) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    named_bar(1 + g, Cfg::GT);  // the tile is complete (in the buffer, or stored from registers)
-    if (leader) {
-      if constexpr (TST) {
-        for (int q = 0; q < Cfg::NBOX; ++q)
-          tma_store_3d(&omap, c0, q * Cfg::R0, l1i, io.buf + q * Cfg::BOX_ELEMS);
-        bulk_commit();
-      }
-      const long long next = tile + (long long)Cfg::NSTAGE * gridDim.x;
-      if (next < total) {
-#ifdef DFFT_TMA2_WAIT_FULL
-        if constexpr (TST) bulk_wait0();
-#else
-        if constexpr (TST) bulk_wait_read0();  // the store has read the buffer
-#endif
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(next, b);
-      }
-    }
-  }
-  if (TST && threadIdx.x % Cfg::GT == 0) bulk_wait0();
 }
 
 }  // namespace dfft

@@ -28,7 +28,7 @@ KernelInfo make_strided_dct() {
   k.twlen = sched_twlen(Cfg::S);
   using TC = TmaCfg<Real, N>;
   if constexpr (TC::OK) {  // TMA-staged variant, TMA stores only (unsegmented outputs)
-    k.tma_fn = k.tma_st_fn = k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, false, DIR>;
+    k.tma_fn = k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, false, DIR>;
     k.tma_st_only = true;
     k.tma_threads = TC::THREADS;
     k.tma_w = TC::W;
@@ -51,8 +51,7 @@ KernelInfo make_strided() {
   using TC = TmaCfg<Real, N>;
   if constexpr (TC::OK) {
     k.tma_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 0>;
-    k.tma_st_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 3>;   // stage-as-output flow
-    k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1>;  // work-buffer flow (A/B)
+    k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1>;  // TMA stores
     k.tma_bk_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 2>;
     if constexpr (DIR < 0) k.tma_st_spec_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, true>;
     k.tma_threads = TC::THREADS;
@@ -60,17 +59,6 @@ KernelInfo make_strided() {
     k.tma_boxr = TC::BOXR;
     k.tma_maxr = TC::MAXR;
     k.tma_smem = TC::SMEM;
-  }
-  using T2 = Tma2Cfg<Real, N>;
-  if constexpr (T2::OK) {
-    k.tma2_fn = (const void*)&fft_strided_tma2_kernel<Real, N, DIR, false>;
-    k.tma2_st_fn = (const void*)&fft_strided_tma2_kernel<Real, N, DIR, true>;
-    k.tma2_threads = T2::THREADS;
-    k.tma2_w = T2::W;
-    k.tma2_r0 = T2::R0;
-    k.tma2_box = T2::BOX_ELEMS;
-    k.tma2_maxr = T2::MAXR;
-    k.tma2_smem = T2::SMEM;
   }
   return k;
 }

@@ -20,16 +20,10 @@ struct KernelInfo {
   int twlen = 0;         // twiddle table length (complex elements)
   // strided family only: persistent TMA-staged variant (null if not instantiable for n)
   const void* tma_fn = nullptr;
-  const void* tma_st_fn = nullptr;  // same, with TMA stores (unsegmented output side)
-  const void* tma_st1_fn = nullptr;  // same, the work-buffer flow (default; tma_st_fn = OM 3, opt-in)
+  const void* tma_st1_fn = nullptr;  // same, with TMA stores (unsegmented output side)
   const void* tma_bk_fn = nullptr;  // same, with bulk-copy stores (column-blocked segmented output)
   const void* tma_st_spec_fn = nullptr;  // TMA stores + Poisson multiplier (forward only)
   bool tma_st_only = false;              // the TMA variant exists only with TMA stores (R2R)
-  // two-warp-group variant (preferred when it fits): in-place padded stage buffers
-  const void* tma2_fn = nullptr;
-  const void* tma2_st_fn = nullptr;
-  int tma2_threads = 0, tma2_w = 0, tma2_r0 = 0, tma2_box = 0, tma2_maxr = 16;
-  size_t tma2_smem = 0;
   int tma_threads = 0, tma_w = 0, tma_boxr = 0, tma_maxr = 16;  // tma_maxr: its radix schedule
   size_t tma_smem = 0;
 };
