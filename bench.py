@@ -29,7 +29,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "3D FFT ms and GFLOP/s (5N·log2N) at 1/2/4/8 B200; % of HBM/NVLink roofline"
-NVLINK_GBS = 900.0  # per direction per GPU, nominal (north star); measured peer copy ~770 (B200_PROFILING.md)
+NVLINK_GBS = 900.0  # per direction per GPU, nominal (north star)
+NVLINK_MEASURED_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md): the NVLink roofline peak
 GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
 
 
@@ -55,6 +56,7 @@ def parse():
                         "packed blocks into the windows; hybrid: p2p for the x-FFT, ce elsewhere; nccl: grouped "
                         "send/recv; auto: p2p")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=260112209 + 4)
     return p.parse_args()
@@ -189,6 +191,45 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ GPU arm
+def _union(iv):
+    """Total length of a union of intervals [(t0, t1), ...]."""
+    tot, end = 0.0, -1e30
+    for t0, t1 in sorted(iv):
+        if t1 <= end:
+            continue
+        tot += t1 - max(t0, end)
+        end = t1
+    return tot
+
+
+def _intersect_len(a, b):
+    """Length of (union of a) ∩ (union of b)."""
+    return _union(a) + _union(b) - _union(a + b)
+
+
+def breakdown_from_timeline(spans, remote_phases):
+    """Fig. 9 analog per execute: wall, FFT busy (any stage kernel running), the part of
+    the NVLink-bound (fused-exchange) stages that ran with no local stage beside it (exposed
+    exchange, Eq. 2's non-overlapped part), the part overlapped with a local stage, and
+    idle (no kernel of ours running: flag waits, pipeline fill/drain, launch gaps)."""
+    by_exec = {}
+    for sp in spans:
+        by_exec.setdefault(sp["exec"], []).append(sp)
+    rows = []
+    for ex, ss in by_exec.items():
+        allv = [(s["t0_ms"], s["t1_ms"]) for s in ss]
+        nvl = [(s["t0_ms"], s["t1_ms"]) for s in ss if s["phase"] in remote_phases]
+        loc = [(s["t0_ms"], s["t1_ms"]) for s in ss if s["phase"] not in remote_phases]
+        wall = max(t1 for _, t1 in allv)
+        busy = _union(allv)
+        ov = _intersect_len(nvl, loc) if nvl and loc else 0.0
+        rows.append({"wall": wall, "busy": busy, "idle": wall - busy, "exchange_exposed": _union(nvl) - ov,
+                     "exchange_overlapped": ov, "local_fft": _union(loc)})
+    if not rows:
+        return None
+    return {k: statistics.mean(r[k] for r in rows) for k in rows[0]}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -237,80 +278,145 @@ def main():
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(vals):
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def timed(fn, iters):
+        """back-to-back: `iters` calls between one pair of events, barrier + sync on both sides."""
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return e0.elapsed_time(e1)
+
+    def per_iteration(fn, iters):
+        """§8(d) ("average execution time over multiple iterations"): every iteration
+        barrier-separated and timed alone; per-iteration max over ranks."""
+        out = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(iters):
+            barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return max_over_ranks(out)
+
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
-    # --- timed region: K fwd+inv steps, barrier + sync on both sides, events on the stream
+    clocks = ClockSampler(local)
+    clocks.start()
+    # --- headline timed region: K back-to-back fwd+inv steps (no profiling events inside)
+    n_launch0 = dfft.kernel_launches()
+    ms_local = timed(step, args.steps)
+    n_launch = dfft.kernel_launches() - n_launch0
+    ms_total = max_over_ranks([ms_local])[0]
+    ms_step = ms_total / max(args.steps, 1)
+    gflops = flops_fwd_inv(shape, args.kind) / (ms_step * 1e-3) / 1e9
+    # --- §8(d) timing procedure: per-iteration statistics, forward only, CUDA graph
+    it_ms = per_iteration(step, max(args.steps, 3))
+    fwd_ms = per_iteration(lambda: fwd.execute(x, y), max(args.steps, 3))
+    step()  # y is the forward of x again (the inverse reads it)
+    graph_ms = None
+    if not args.no_graph:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            fwd.execute(x, y, stream=gs)
+            inv.execute(y, z, stream=gs)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        graph_ms = max_over_ranks([timed(g.replay, args.steps)])[0] / max(args.steps, 1)
+        del g
+    timing = {
+        "procedure": "P:558 / SURVEY §8(d): back-to-back mean (headline, the contract's timed region); "
+                     "per-iteration barrier-separated fwd+inv and forward-only, max over ranks per iteration",
+        "back_to_back_ms": ms_step,
+        "per_iteration_ms": {"median": statistics.median(it_ms), "min": min(it_ms), "mean": statistics.mean(it_ms),
+                             "sd": statistics.pstdev(it_ms), "n": len(it_ms)},
+        "forward_only_ms": {"median": statistics.median(fwd_ms), "min": min(fwd_ms), "mean": statistics.mean(fwd_ms),
+                            "sd": statistics.pstdev(fwd_ms), "n": len(fwd_ms)},
+        "cuda_graph_ms": graph_ms,
+    }
+    # --- profiled pass (separate from the headline): per-phase times, timeline, roofline
+    R = max(3, min(args.steps, 10))
     fwd.set_profiling(True)
     inv.set_profiling(True)
     fwd.phase_times(reset=True)
     inv.phase_times(reset=True)
-    clocks = ClockSampler(local)
-    clocks.start()
-    barrier()
-    torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_launch0 = dfft.kernel_launches()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(stream)
-    n_launch = dfft.kernel_launches() - n_launch0
-    torch.cuda.synchronize()
-    barrier()
-    clk = clocks.stop()
-    ms_local = ev0.elapsed_time(ev1)
-    pf, pi = fwd.phase_times(), inv.phase_times()
+    prof_ms = timed(step, R) / R
+    pf, pi = fwd.phase_times(reset=False), inv.phase_times(reset=False)
+    tf, ti = fwd.timeline(), inv.timeline()
     fwd.set_profiling(False)
     inv.set_profiling(False)
-    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = t.item()
-    ms_step = ms_total / max(args.steps, 1)
-    gflops = flops_fwd_inv(shape, args.kind) / (ms_step * 1e-3) / 1e9
+    clk = clocks.stop()
+    timing["profiled_pass_ms"] = max_over_ranks([prof_ms])[0]
 
-    # --- roofline of the dominant kernel (largest total time among the FFT stages)
+    # --- roofline: every FFT stage against its binding resource; the dominant one is `roofline`
     hbm_peak, peak_kind = load_peaks()
     bf, bi = fwd.stage_bytes(), inv.stage_bytes()
-    kernels = []
+    P = grid[0] * grid[1]
+    fused = world > 1 and args.exchange in ("auto", "p2p")
+    # with fused stores stage A carries exchange 1 and stage B exchange 2 inside their epilogues
+    carries = {"stage_A": "exchange_1", "stage_B": "exchange_2"}
+    traffic_tab = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic_tab = json.load(f).get(f"{shape[0]}x{shape[1]}x{shape[2]}_{args.precision}_{grid[0]}x{grid[1]}", {})
+    except Exception:
+        pass
+    if P == 1:  # single GPU: forward x, z, y; inverse y, z, x (DESIGN.md §5)
+        stage_names = {"fwd": {"stage_A": "x-FFT (contig)", "stage_B": "z-FFT (strided TMA, reads [y][z][x])",
+                               "stage_C": "y-FFT (strided TMA)"},
+                       "inv": {"stage_A": "y-IFFT (strided TMA)", "stage_B": "z-IFFT (strided TMA, writes [y][z][x])",
+                               "stage_C": "x-IFFT (contig, 1/N)"}}
+    else:
+        stage_names = {"fwd": {"stage_A": "x-FFT (contig, fused T1 pack/store)",
+                               "stage_B": "y-FFT (strided, fused T2 pack/store)", "stage_C": "z-FFT (strided)"},
+                       "inv": {"stage_A": "z-IFFT (strided, fused T2 pack/store)",
+                               "stage_B": "y-IFFT (strided, fused T1 pack/store)",
+                               "stage_C": "x-IFFT (contig, fused unpack, 1/N)"}}
+    stages = []
     for tag, pt, bt in (("fwd", pf, bf), ("inv", pi, bi)):
         for ph in ("stage_A", "stage_B", "stage_C"):
             ms, cnt = pt[ph]
-            if cnt:
-                per_launch_bytes = bt[ph] / (cnt / args.steps)
-                kernels.append((ms, tag, ph, cnt, per_launch_bytes))
-    kernels.sort(reverse=True)
-    ms_k, tag_k, ph_k, cnt_k, bytes_k = kernels[0]
-    avg_ms = ms_k / cnt_k
-    achieved = bytes_k / (avg_ms * 1e-3) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f)
-        traffic = tr.get(f"{shape[0]}x{shape[1]}x{shape[2]}_{args.precision}_{grid[0]}x{grid[1]}", {}).get(
-            f"{tag_k}_{ph_k}")
-        if traffic is not None:
-            traffic = traffic / (cnt_k / args.steps)  # per launch
-    except Exception:
-        pass
-    if grid[0] * grid[1] == 1:  # single GPU: forward x, z, y; inverse y, z, x
-        stage_names = {"fwd": {"stage_A": "x-FFT (contig)", "stage_B": "z-FFT (strided TMA, writes [y][z][x])",
-                               "stage_C": "y-FFT (strided TMA)"},
-                       "inv": {"stage_A": "y-IFFT (strided TMA)", "stage_B": "z-IFFT (strided TMA)",
-                               "stage_C": "x-IFFT (contig, 1/N)"}}
-    else:
-        stage_names = {"fwd": {"stage_A": "x-FFT (contig, fused T1 pack)", "stage_B": "y-FFT (strided, fused T2 pack)",
-                               "stage_C": "z-FFT (strided)"},
-                       "inv": {"stage_A": "z-IFFT (strided, fused T2 pack)", "stage_B": "y-IFFT (strided, fused pack)",
-                               "stage_C": "x-IFFT (contig, fused unpack, 1/N)"}}
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic,
-                "kernel": f"{tag_k} {stage_names[tag_k][ph_k]}", "peak_kind": peak_kind,
-                "bytes_per_launch": bytes_k, "avg_launch_ms": avg_ms}
+            if not cnt:
+                continue
+            launches = cnt / R
+            avg = ms / cnt
+            xb = bt.get(carries.get(ph, ""), 0.0) if fused else 0.0
+            if xb > 0:  # NVLink-bound: off-rank bytes of the exchange this stage stores
+                ach = xb / launches / (avg * 1e-3) / 1e9
+                ent = {"bound": "nvlink", "achieved": ach, "peak": NVLINK_MEASURED_GBS, "unit": "GB/s",
+                       "frac": ach / NVLINK_MEASURED_GBS, "frac_of_nominal_900": ach / NVLINK_GBS,
+                       "bytes_per_launch": xb / launches, "peak_kind": "measured peer copy (B200_PROFILING.md)"}
+            else:
+                ach = bt[ph] / launches / (avg * 1e-3) / 1e9
+                ent = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                       "bytes_per_launch": bt[ph] / launches, "peak_kind": peak_kind}
+            tr = traffic_tab.get(f"{tag}_{ph}")
+            ent.update({"kernel": f"{tag} {stage_names[tag][ph]}", "avg_launch_ms": avg, "ms_per_step": ms / R,
+                        "traffic": tr / launches if tr is not None and ent["bound"] == "hbm" else None})
+            stages.append(ent)
+    dom = max(stages, key=lambda e: e["ms_per_step"])
+    roofline = {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel", "peak_kind",
+                                    "bytes_per_launch", "avg_launch_ms")}
+    roofline["stages"] = stages
 
     # --- north-star roofline: T_roof = max(T_HBM, T_NVL) per GPU for fwd+inv (SURVEY §8(d))
-    P = grid[0] * grid[1]
     Nloc = shape[0] * shape[1] * shape[2] / P
     # complex elements per rank after stage 1 (R2C: nx/2+1 bins along x) and stage-1 bytes
     Ncl = Nloc * ((shape[0] // 2 + 1) / shape[0] if args.kind == "r2c" else 0.5 if args.kind == "r2r" else 1.0)
@@ -320,41 +426,42 @@ def main():
     nvl_bytes = Ncl * es * ((p1 - 1) / p1 + (p2 - 1) / p2)
     t_nvl = 2 * nvl_bytes / (NVLINK_GBS * 1e9)
     t_roof = max(t_hbm, t_nvl)
-    breakdown = {f"fwd_{k}": v[0] / args.steps for k, v in pf.items() if v[1]}
-    breakdown.update({f"inv_{k}": v[0] / args.steps for k, v in pi.items() if v[1]})
-    launches_per_step = sum(v[1] for v in pf.values() if v[1]) + sum(v[1] for v in pi.values() if v[1])
-    exch = sum(pf[k][1] + pi[k][1] for k in ("exchange_1", "exchange_2"))
-    gpu_launches = n_launch  # our kernels (FFT stages + flag signals) in the timed region, counted by libdfft
+    breakdown = {f"fwd_{k}": v[0] / R for k, v in pf.items() if v[1]}
+    breakdown.update({f"inv_{k}": v[0] / R for k, v in pi.items() if v[1]})
+    # Fig. 9 analog: FFT / exchange (exposed vs overlapped) / idle per direction, and each
+    # exchange's NVLink rate (off-rank bytes over the time of the stage that carries them)
+    fig9 = None
+    if world > 1:
+        remote = {"stage_A", "stage_B"} if fused else {"exchange_1", "exchange_2"}
+        fig9 = {"fwd": breakdown_from_timeline(tf, {p for p in remote if bf.get(carries.get(p, p), 1) > 0}),
+                "inv": breakdown_from_timeline(ti, {p for p in remote if bi.get(carries.get(p, p), 1) > 0}),
+                "exchange_gbs": {}}
+        for tag, pt, bt in (("fwd", pf, bf), ("inv", pi, bi)):
+            for ex, carrier in (("exchange_1", "stage_A"), ("exchange_2", "stage_B")):
+                ph = carrier if fused else ex
+                if bt[ex] > 0 and pt[ph][1]:
+                    gbs = bt[ex] * R / (pt[ph][0] * 1e-3) / 1e9
+                    fig9["exchange_gbs"][f"{tag}_{ex}"] = {"gbs": gbs, "frac_of_770": gbs / NVLINK_MEASURED_GBS,
+                                                           "frac_of_900": gbs / NVLINK_GBS, "timed_on": ph}
+    gpu_launches = n_launch  # our kernels (FFT stages + flag kernels) in the headline region, counted by libdfft
 
-    # --- e2e: host pinned input -> device -> fwd+inv -> host, through the public API
+    # --- e2e: pinned host input -> device -> fwd -> inv -> pinned host, through the C ABI
+    # (dfft_execute_host_chain: double-buffered staging, H2D / D2H on their own streams)
     e2e = None
     if not args.no_e2e:
         xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
         xh.copy_(x)
         zh = torch.empty(z.shape, dtype=z.dtype, pin_memory=True)
         ke = max(2, min(args.steps, 5))
-        for it in range(ke + 1):
-            if it == 1:
-                barrier()
-                torch.cuda.synchronize()
-                e0 = time.perf_counter()
-                s0 = torch.cuda.Event(enable_timing=True)
-                s1 = torch.cuda.Event(enable_timing=True)
-                s0.record(stream)
-            x.copy_(xh, non_blocking=True)
-            step()
-            zh.copy_(z, non_blocking=True)
-        s1.record(stream)
+        chain = lambda: dfft.execute_host_chain([fwd, inv], xh, zh, async_=True)  # noqa: E731
+        chain()
         torch.cuda.synchronize()
-        el = s0.elapsed_time(s1) / ke
-        te = torch.tensor([el], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        el = te.item()
+        el = max_over_ranks([timed(chain, ke) / ke])[0]
         e2e = {"value": flops_fwd_inv(shape, args.kind) / (el * 1e-3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(x.numel() * x.element_size()),
                "d2h_bytes_per_step": int(z.numel() * z.element_size()), "ms_per_step": el,
-               "path": "pinned host -> Plan.execute(fwd) -> Plan.execute(inv) -> pinned host"}
+               "path": "dfft_execute_host_chain([fwd, inv]): pinned host -> device -> fwd -> inv -> pinned host, "
+                       "asynchronous, H2D/D2H on their own copy streams (double-buffered staging)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -382,7 +489,9 @@ def main():
             "north_star_roofline": {"t_roof_ms": t_roof * 1e3, "t_hbm_ms": t_hbm * 1e3, "t_nvl_ms": t_nvl * 1e3,
                                     "frac": t_roof / (ms_step * 1e-3), "hbm_peak_gbs": hbm_peak,
                                     "nvlink_gbs": NVLINK_GBS},
+            "timing": timing,
             "phase_ms_per_step": breakdown,
+            "fig9_breakdown_ms": fig9,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": int(gpu_launches),

@@ -1907,6 +1907,10 @@ void trigger_failure(dfft_plan_t pl, long long waited_ms) {
 }
 
 void Watchdog::loop() {
+  // relaxed capture interaction: this thread's event queries must neither fail nor invalidate a
+  // CUDA-graph capture the application runs on another thread
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
   for (;;) {
     std::this_thread::sleep_for(std::chrono::milliseconds(20));
     std::lock_guard<std::mutex> lk(mu);

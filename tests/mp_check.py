@@ -144,7 +144,8 @@ def main():
         results = []
         for chunks, overlap, exch in ((0, True, "auto"), (3, True, "hybrid"), (0, True, "ce"), (1, True, "ce"),
                                       (3, True, "ce"), (0, True, "p2p"),
-                                      (3, True, "p2p"), (0, True, "nccl"), (3, True, "nccl"), (2, False, "nccl")):
+                                      (3, True, "p2p"), (0, True, "nccl"), (3, True, "nccl"), (2, False, "nccl"),
+                                      (2, False, "p2p"), (2, False, "ce")):
             log(decomp, grid, shape, prec, chunks, overlap, exch)
             fwd = dfft.Plan(comm, shape, decomp, grid, "c2c_" + prec, dfft.FORWARD, chunks=chunks, overlap=overlap,
                             exchange=exch)
@@ -176,6 +177,50 @@ def main():
                 for (_, _, a0), (_, _, a1) in zip(results[0][0], ys):
                     assert np.array_equal(a0, a1), ("schedule changed bits", decomp, grid, shape, prec)
             n_ok += 1
+        dist.barrier()
+    # CUDA-graph capture of the fused-store schedule on real ranks: each rank captures fwd+inv once
+    # and replays it on fresh inputs (the flag protocol waits for constant values)
+    for decomp, grid in grids[:2]:
+        shape = (64, 48, 32)
+        log("graph capture", decomp, grid)
+        fwd = dfft.Plan(comm, shape, decomp, grid, "c2c_f64", dfft.FORWARD, chunks=2)
+        inv = dfft.Plan(comm, shape, decomp, grid, "c2c_f64", dfft.INVERSE, chunks=2)
+        lo, n = fwd.box(0)
+        x = fwd.alloc_in()
+        y, z = fwd.alloc_out(), inv.alloc_out()
+        inputs.fill_box_cuda(x, 3, shape, lo, n, True)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fwd.execute(x, y, stream=s)
+            inv.execute(y, z, stream=s)
+        s.synchronize()
+        dist.barrier()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            fwd.execute(x, y, stream=s)
+            inv.execute(y, z, stream=s)
+        for seed in (21, 22):
+            inputs.fill_box_cuda(x, seed, shape, lo, n, True)
+            torch.cuda.synchronize()
+            dist.barrier()
+            g.replay()
+            torch.cuda.synchronize()
+            ys, zs = gather(y, fwd, 1), gather(z, inv, 1)
+            if rank == 0:
+                a = oracle.gen_complex(seed, shape)
+                A = oracle.fft3d(a, -1)
+                Y, Z = np.zeros_like(A), np.zeros_like(a)
+                for lo_, n_, arr in ys:
+                    box_slice(Y, lo_, n_)[...] = arr
+                for lo_, n_, arr in zs:
+                    box_slice(Z, lo_, n_)[...] = arr
+                ef, er = oracle.rel_l2(Y, A), oracle.rel_l2(Z, a)
+                assert ef <= 1e-12 and er <= 1e-12, ("graph replay", decomp, grid, ef, er)
+                n_ok += 1
+        del g
+        fwd.destroy()
+        inv.destroy()
         dist.barrier()
     # the bench's launch configuration at full size (BASELINE configs[3], default transport and
     # chunking): sampled bins vs the oracle's direct sums, round trip, Parseval
