@@ -55,6 +55,10 @@ def _load():
         lib.or_poisson3d.argtypes = [_dp, _i64, _i64, _i64, _d, _d, _d, _dp]
         lib.or_laplacian7.argtypes = [_dp, _i64, _i64, _i64, _d, _d, _d, _dp]
         lib.or_dct3d.argtypes = [_dp, _i64, _i64, _i64, _int]
+        lib.or_axis_transform.argtypes = [_dp, _i64, _i64, _i64, _int, _int, _int]
+        lib.or_rfft_x.argtypes = [_dp, _i64, _i64, _i64, _dp]
+        lib.or_irfft_x.argtypes = [_dp, _i64, _i64, _i64, _dp]
+        lib.or_poisson_eigen_kind.argtypes = [_i64, ctypes.c_double, _int, _dp]
         lib.or_set_threads.argtypes = [_int]
         lib.or_dft3d_bin_seeded.argtypes = [_u64, _i64, _i64, _i64, _int, _int, _i64, _i64, _i64, _dp]
         lib.or_err_sums.argtypes = [_dp, _dp, _i64, _dp]
@@ -163,6 +167,85 @@ def dct3d(a: np.ndarray, inverse: bool = False) -> np.ndarray:
     nz, ny, nx = out.shape
     _load().or_dct3d(_p(out), nx, ny, nz, int(bool(inverse)))
     return out
+
+
+KINDS = {"dft": 0, "dct": 1, "dst": 2}
+
+
+def axis_transform(a: np.ndarray, axis: int, kind: str, inverse: bool = False) -> np.ndarray:
+    """One axis (0 x, 1 y, 2 z) of a complex (nz,ny,nx) array: DFT (inverse ×1/n), DCT-II /
+    DCT-III/(2n), DST-II / DST-III/(2n) of the real and imaginary parts (reading R22)."""
+    out = np.array(a, dtype=np.complex128, order="C", copy=True)
+    nz, ny, nx = out.shape
+    _load().or_axis_transform(_p(out.view(np.float64)), nx, ny, nz, int(axis), KINDS[kind], int(bool(inverse)))
+    return out
+
+
+def rfft_x(f: np.ndarray) -> np.ndarray:
+    """R2C along x only: (nz,ny,nx) real -> (nz,ny,nx/2+1) complex."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    nz, ny, nx = f.shape
+    out = np.empty((nz, ny, nx // 2 + 1), dtype=np.complex128)
+    _load().or_rfft_x(_p(f), nx, ny, nz, _p(out.view(np.float64)))
+    return out
+
+
+def irfft_x(h: np.ndarray, nx: int) -> np.ndarray:
+    """C2R along x only (Hermitian extension per line, reading R8)."""
+    h = np.ascontiguousarray(h, dtype=np.complex128)
+    nz, ny, _ = h.shape
+    out = np.empty((nz, ny, nx), dtype=np.float64)
+    _load().or_irfft_x(_p(h.view(np.float64)), nx, ny, nz, _p(out))
+    return out
+
+
+def transform_kinds(a: np.ndarray, kinds, inverse: bool = False, real_x: bool = False, nx: int = 0) -> np.ndarray:
+    """The 3D transform with per-axis kinds (x, y, z), in the paper's axis order: forward x, y, z;
+    inverse z, y, x.  real_x: x is the R2C axis (forward: real input, half
+    spectrum out; inverse: half spectrum in, real output of length nx).  R2R plans: real data
+    with DCT/DST on every axis (the complex view is only the carrier)."""
+    kinds = list(kinds)
+    if not inverse:
+        if real_x:
+            out = rfft_x(a)
+        elif kinds[0] == "dft":
+            out = axis_transform(a, 0, "dft")
+        else:
+            out = axis_transform(a, 0, kinds[0])
+        for ax in (1, 2):
+            out = axis_transform(out, ax, kinds[ax])
+        return out
+    out = np.asarray(a, dtype=np.complex128)
+    for ax in (2, 1):
+        out = axis_transform(out, ax, kinds[ax], inverse=True)
+    if real_x:
+        return irfft_x(out, nx)
+    return axis_transform(out, 0, kinds[0], inverse=True)
+
+
+def poisson_eigen_kind(n: int, h: float, kind: str) -> np.ndarray:
+    """λ_k of the 3-point second difference on the basis of the axis's transform kind (R22)."""
+    out = np.empty(n)
+    _load().or_poisson_eigen_kind(n, float(h), KINDS[kind], _p(out))
+    return out
+
+
+def poisson_kinds(f: np.ndarray, kinds, spacing=(1.0, 1.0, 1.0)) -> np.ndarray:
+    """∇²φ = f with per-axis boundary kinds (periodic DFT, Neumann DCT, Dirichlet DST), step by step
+    as the solver does it: forward transform (R2C along x if x is periodic), Φ = F/λ(k) with
+    λ = Σ_d λ_d(k_d) and Φ = 0 where λ = 0 (the zero-mean solution when no axis is Dirichlet),
+    inverse transform (readings R20, R22)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    nz, ny, nx = f.shape
+    real_x = kinds[0] == "dft"
+    F = transform_kinds(f if real_x else f.astype(np.complex128), kinds, real_x=real_x)
+    lam = (poisson_eigen_kind(nx, spacing[0], kinds[0])[: F.shape[2]][None, None, :]
+           + poisson_eigen_kind(ny, spacing[1], kinds[1])[None, :, None]
+           + poisson_eigen_kind(nz, spacing[2], kinds[2])[:, None, None])
+    with np.errstate(divide="ignore", invalid="ignore"):
+        Phi = np.where(lam != 0, F / np.where(lam != 0, lam, 1.0), 0)
+    out = transform_kinds(Phi, kinds, inverse=True, real_x=real_x, nx=nx)
+    return np.real(out).copy() if not real_x else out
 
 
 def poisson_eigen(n: int, h: float = 1.0) -> np.ndarray:

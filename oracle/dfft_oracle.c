@@ -581,3 +581,152 @@ void or_set_threads(int n) {
     (void)n;
 #endif
 }
+
+/* ------------------------------------------------------------------ per-axis transform kinds (f4) */
+
+/*
+ * Bounded directions ("C2C, R2C and R2R"; "DCT and DST"; P:620 the (Periodic,
+ * Periodic, Bounded) topology): each axis carries its own 1D transform, kind
+ *   0 = DFT   (Periodic):                     X_k = Σ_n x_n e^{∓2πi kn/N}
+ *   1 = DCT-II (Bounded, Neumann; REDFT10):   X_k = 2 Σ_n x_n cos(π k (2n+1) / (2N))
+ *   2 = DST-II (Bounded, Dirichlet; RODFT10): X_k = 2 Σ_n x_n sin(π (k+1) (2n+1) / (2N))
+ * with inverses DFT⁺/N, DCT-III/(2N) and DST-III/(2N) (RODFT01):
+ *   x_n = ((-1)^n X_{N-1} + 2 Σ_{k<N-1} X_k sin(π (k+1) (2n+1) / (2N))) / (2N)
+ * (reading R22).  The 3D transform applies the axes in the paper's order (x, y, z
+ * forward; z, y, x inverse).  A real-coefficient transform (DCT / DST) of
+ * complex data transforms the real and imaginary parts alike (it is linear), which is how a
+ * bounded direction follows an R2C (periodic) x axis.  Sums written out, sines in long double.
+ */
+static void or_dst_line(const double* x, int64_t n, int inverse, double* y, const double* s /* sin(π m/(2n)), m < 4n */) {
+    for (int64_t a = 0; a < n; ++a) {
+        long double acc = 0.0L;
+        if (!inverse) {
+            for (int64_t b = 0; b < n; ++b) acc += (long double)x[b] * s[((a + 1) * (2 * b + 1)) % (4 * n)];
+            y[a] = (double)(2.0L * acc);
+        } else {
+            acc = (a % 2 ? -1.0L : 1.0L) * (long double)x[n - 1];
+            for (int64_t b = 0; b + 1 < n; ++b) acc += 2.0L * (long double)x[b] * s[((b + 1) * (2 * a + 1)) % (4 * n)];
+            y[a] = (double)(acc / (long double)(2 * n));
+        }
+    }
+}
+
+/* One axis of a complex (nx, ny, nz) array (interleaved re, im): kind 0 = the DFT (sign -1 forward;
+ * inverse sign +1 and ×1/n), kinds 1 / 2 = DCT / DST of the real and the imaginary parts. */
+void or_axis_transform(double* a, int64_t nx, int64_t ny, int64_t nz, int axis, int kind, int inverse) {
+    const int64_t n = axis == 0 ? nx : axis == 1 ? ny : nz;
+    const int64_t stride = axis == 0 ? 1 : axis == 1 ? nx : nx * ny;
+    const int64_t lines = nx * ny * nz / n;
+    double* tab = (double*)malloc(sizeof(double) * 4 * (size_t)n);
+    for (int64_t m = 0; m < 4 * n; ++m) {
+        const long double ang = OR_PI_L * (long double)m / (long double)(2 * n);
+        tab[m] = (double)(kind == 2 ? sinl(ang) : cosl(ang));
+    }
+#pragma omp parallel
+    {
+        double* line = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+        double* in = (double*)malloc(sizeof(double) * (size_t)n);
+        double* out = (double*)malloc(sizeof(double) * (size_t)n);
+        or_line_plan lp;
+        if (kind == 0) or_line_init(&lp, n, inverse ? +1 : -1);
+#pragma omp for schedule(static)
+        for (int64_t l = 0; l < lines; ++l) {
+            int64_t base;
+            if (axis == 0) base = l * nx;
+            else if (axis == 1) base = (l % nx) + (l / nx) * nx * ny;
+            else base = l;
+            if (kind == 0) {
+                for (int64_t t = 0; t < n; ++t) {
+                    line[2 * t] = a[2 * (base + t * stride)];
+                    line[2 * t + 1] = a[2 * (base + t * stride) + 1];
+                }
+                or_line_exec(&lp, line);
+                const double sc = inverse ? 1.0 / (double)n : 1.0;
+                for (int64_t t = 0; t < n; ++t) {
+                    a[2 * (base + t * stride)] = line[2 * t] * sc;
+                    a[2 * (base + t * stride) + 1] = line[2 * t + 1] * sc;
+                }
+            } else {
+                for (int part = 0; part < 2; ++part) {
+                    for (int64_t t = 0; t < n; ++t) in[t] = a[2 * (base + t * stride) + part];
+                    if (kind == 1) or_dct_line(in, 1, n, inverse, out, 1, tab);
+                    else or_dst_line(in, n, inverse, out, tab);
+                    for (int64_t t = 0; t < n; ++t) a[2 * (base + t * stride) + part] = out[t];
+                }
+            }
+        }
+        if (kind == 0) or_line_free(&lp);
+        free(line);
+        free(in);
+        free(out);
+    }
+    free(tab);
+}
+
+/* R2C along x only: each real x-line → c2c DFT of (x + 0i), bins 0..nx/2 (reading R8, per line). */
+void or_rfft_x(const double* real, int64_t nx, int64_t ny, int64_t nz, double* out) {
+    const int64_t nxc = nx / 2 + 1;
+#pragma omp parallel
+    {
+        double* line = (double*)malloc(sizeof(double) * 2 * (size_t)nx);
+        or_line_plan lp;
+        or_line_init(&lp, nx, -1);
+#pragma omp for schedule(static)
+        for (int64_t l = 0; l < ny * nz; ++l) {
+            for (int64_t t = 0; t < nx; ++t) {
+                line[2 * t] = real[l * nx + t];
+                line[2 * t + 1] = 0.0;
+            }
+            or_line_exec(&lp, line);
+            memcpy(out + 2 * l * nxc, line, sizeof(double) * 2 * (size_t)nxc);
+        }
+        or_line_free(&lp);
+        free(line);
+    }
+}
+
+/* C2R along x only: Hermitian-extend each half line (X[nx-k] = conj X[k], 1 <= k < nx/2; the
+ * imaginary parts of bins 0 and nx/2 dropped), inverse DFT ×1/nx, real part (reading R8). */
+void or_irfft_x(const double* half, int64_t nx, int64_t ny, int64_t nz, double* real_out) {
+    const int64_t nxc = nx / 2 + 1;
+#pragma omp parallel
+    {
+        double* line = (double*)malloc(sizeof(double) * 2 * (size_t)nx);
+        or_line_plan lp;
+        or_line_init(&lp, nx, +1);
+#pragma omp for schedule(static)
+        for (int64_t l = 0; l < ny * nz; ++l) {
+            const double* h = half + 2 * l * nxc;
+            for (int64_t t = 0; t < nx; ++t) {
+                if (t < nxc) {
+                    line[2 * t] = h[2 * t];
+                    line[2 * t + 1] = (t == 0 || 2 * t == nx) ? 0.0 : h[2 * t + 1];
+                } else {
+                    line[2 * t] = h[2 * (nx - t)];
+                    line[2 * t + 1] = -h[2 * (nx - t) + 1];
+                }
+            }
+            or_line_exec(&lp, line);
+            for (int64_t t = 0; t < nx; ++t) real_out[l * nx + t] = line[2 * t] / (double)nx;
+        }
+        or_line_free(&lp);
+        free(line);
+    }
+}
+
+/*
+ * Eigenvalues of the second-order 3-point difference along one axis of n cells, spacing h, on
+ * the basis of its transform kind (reading R22):
+ *   DFT (periodic):                       λ_k = -(2 sin(π k / n) / h)²
+ *   DCT-II (Neumann, cell-centred mirror): λ_k = -(2 sin(π k / (2n)) / h)²
+ *   DST-II (Dirichlet, cell-centred antimirror): λ_k = -(2 sin(π (k+1) / (2n)) / h)²
+ */
+void or_poisson_eigen_kind(int64_t n, double h, int kind, double* lam) {
+    for (int64_t k = 0; k < n; ++k) {
+        const long double ang = kind == 0 ? OR_PI_L * (long double)k / (long double)n
+                              : kind == 1 ? OR_PI_L * (long double)k / (long double)(2 * n)
+                                          : OR_PI_L * (long double)(k + 1) / (long double)(2 * n);
+        const long double s = 2.0L * sinl(ang) / (long double)h;
+        lam[k] = (double)(-(s * s));
+    }
+}

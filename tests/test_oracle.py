@@ -9,6 +9,7 @@ twiddle index, missing 1/N) fails at least one of them.
 import os
 
 import numpy as np
+import scipy.fft as sf
 import pytest
 
 import inputs
@@ -290,3 +291,107 @@ def test_dct3d_closed_forms(oracle_mod):
     ref = np.zeros_like(C)
     ref[0, 0, 0] = 8 * nx * ny * nz * 0.5
     assert np.abs(C - ref).max() < 1e-11
+
+
+# ------------------------------------------------------------------ per-axis kinds: DST, mixed topologies (f4)
+@pytest.mark.parametrize("kind,fwd,inv", [
+    ("dct", lambda a, ax: sf.dct(a, 2, axis=ax), lambda a, ax: sf.idct(a, 2, axis=ax)),
+    ("dst", lambda a, ax: sf.dst(a, 2, axis=ax), lambda a, ax: sf.idst(a, 2, axis=ax)),
+    ("dft", lambda a, ax: sf.fft(a, axis=ax), lambda a, ax: sf.ifft(a, axis=ax)),
+])
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_axis_transform_vs_scipy(oracle_mod, kind, fwd, inv, axis):
+    # P:409 "DCT and DST" (reading R22: FFTW REDFT10/RODFT10 forward, REDFT01/RODFT01 ÷ 2N inverse)
+    # = scipy.fft dct/dst type 2 with norm=None and their idct/idst (pocketfft, independent code);
+    # on complex data the real and imaginary parts are transformed alike
+    rng = np.random.default_rng(axis)
+    a = rng.standard_normal((6, 10, 8)) + 1j * rng.standard_normal((6, 10, 8))
+    ax = 2 - axis  # numpy axis of x / y / z in a (nz, ny, nx) array
+    Y = oracle_mod.axis_transform(a, axis, kind)
+    ref = fwd(a, ax) if kind == "dft" else fwd(a.real, ax) + 1j * fwd(a.imag, ax)
+    assert np.abs(Y - ref).max() <= 1e-13 * np.abs(ref).max()
+    back = oracle_mod.axis_transform(Y, axis, kind, inverse=True)
+    ref_b = inv(Y, ax) if kind == "dft" else inv(Y.real, ax) + 1j * inv(Y.imag, ax)
+    assert np.abs(back - ref_b).max() <= 1e-13 and np.abs(back - a).max() <= 1e-13
+
+
+def test_dst_closed_forms(oracle_mod):
+    # textbook: the DST-II basis vector sin(π(m+1)(2n+1)/(2N)) maps to N at k = m only (orthogonality;
+    # 2N for m = N-1, whose vector is (-1)^n), and RODFT01 of a spike 2N at k = N-1 is (-1)^n
+    N = 12
+    n = np.arange(N)
+    for m in (0, 3, N - 1):
+        v = np.sin(np.pi * (m + 1) * (2 * n + 1) / (2 * N)).reshape(1, 1, N)
+        Y = oracle_mod.axis_transform(v, 0, "dst").real.ravel()
+        e = np.zeros(N)
+        e[m] = N if m < N - 1 else 2 * N
+        assert np.abs(Y - e).max() < 1e-12
+    s = np.zeros((1, 1, N))
+    s[0, 0, N - 1] = 2 * N
+    assert np.abs(oracle_mod.axis_transform(s, 0, "dst", inverse=True).real.ravel() - (-1.0) ** n).max() < 1e-13
+
+
+def test_rfft_irfft_x_vs_numpy(oracle_mod):
+    rng = np.random.default_rng(5)
+    f = rng.standard_normal((4, 6, 10))
+    H = oracle_mod.rfft_x(f)
+    assert np.abs(H - np.fft.rfft(f, axis=2)).max() < 1e-13
+    G = rng.standard_normal(H.shape) + 1j * rng.standard_normal(H.shape)  # arbitrary (non-Hermitian)
+    assert np.abs(oracle_mod.irfft_x(G, 10) - np.fft.irfft(G, 10, axis=2)).max() < 1e-13
+
+
+@pytest.mark.parametrize("kinds", [("dft", "dft", "dct"), ("dft", "dst", "dft"), ("dft", "dct", "dst"),
+                                   ("dct", "dst", "dct"), ("dst", "dst", "dst")])
+def test_mixed_kinds_vs_scipy_axis_by_axis(oracle_mod, kinds):
+    # P:620's (Periodic, Periodic, Bounded) topology and its relatives: the separable transform is
+    # each axis's 1D transform in turn, composed here with scipy along each axis
+    nx, ny, nz = 12, 8, 6
+    f = oracle_mod.gen_real(7, (nx, ny, nz))
+    real_x = kinds[0] == "dft"
+    ref = np.fft.rfft(f, axis=2) if real_x else (sf.dct if kinds[0] == "dct" else sf.dst)(f, 2, axis=2) + 0j
+    for k, ax in ((kinds[1], 1), (kinds[2], 0)):
+        if k == "dft":
+            ref = np.fft.fft(ref, axis=ax)
+        else:
+            t = sf.dct if k == "dct" else sf.dst
+            ref = t(ref.real, 2, axis=ax) + 1j * t(ref.imag, 2, axis=ax)
+    X = oracle_mod.transform_kinds(f if real_x else f + 0j, kinds, real_x=real_x)
+    assert np.abs(X - ref).max() <= 1e-12 * np.abs(ref).max()
+    back = oracle_mod.transform_kinds(X, kinds, inverse=True, real_x=real_x, nx=nx)
+    assert np.abs(np.real(back) - f).max() <= 1e-13
+
+
+def _lap_bc(phi, h, kinds):
+    """3-point second differences per axis with the boundary each kind encodes (numpy, independent
+    of the oracle): periodic wrap (DFT), cell-centred mirror ghost φ_{-1} = φ_0 (Neumann, DCT-II),
+    antimirror ghost φ_{-1} = -φ_0 (Dirichlet, DST-II)."""
+    out = np.zeros_like(phi)
+    for d, (k, hd) in enumerate(zip(kinds, h)):
+        ax = 2 - d
+        if k == "dft":
+            lo, hi = np.roll(phi, 1, ax), np.roll(phi, -1, ax)
+        else:
+            s = 1.0 if k == "dct" else -1.0
+            first = np.take(phi, [0], axis=ax)
+            last = np.take(phi, [phi.shape[ax] - 1], axis=ax)
+            lo = np.concatenate([s * first, np.take(phi, range(phi.shape[ax] - 1), axis=ax)], axis=ax)
+            hi = np.concatenate([np.take(phi, range(1, phi.shape[ax]), axis=ax), s * last], axis=ax)
+        out += (lo - 2 * phi + hi) / hd**2
+    return out
+
+
+@pytest.mark.parametrize("kinds,h", [(("dft", "dft", "dct"), (1.0, 0.5, 2.0)), (("dft", "dft", "dst"), (1.0, 1.0, 1.0)),
+                                     (("dct", "dct", "dct"), (1.0, 2.0, 0.5)), (("dst", "dct", "dst"), (0.5, 1.0, 1.0)),
+                                     (("dft", "dst", "dct"), (2.0, 1.0, 0.25))])
+def test_poisson_kinds_inverts_the_bounded_laplacian(oracle_mod, kinds, h):
+    # P:606-620 with P:620's bounded directions (readings R20, R22): applying the 7-point operator
+    # with each axis's boundary (numpy) to φ gives back f, minus its mean when no axis is Dirichlet
+    # (the operator is then singular on constants and the solver returns the zero-mean solution)
+    shape = (12, 8, 10)
+    f = oracle_mod.gen_real(13, shape)
+    phi = oracle_mod.poisson_kinds(f, kinds, h)
+    target = f - f.mean() if "dst" not in kinds else f
+    r = _lap_bc(phi, h, kinds) - target
+    assert np.abs(r).max() <= 1e-11 * np.abs(f).max() * max(1.0, max(1 / v**2 for v in h))
+    if kinds == ("dft", "dft", "dft"):
+        assert np.abs(phi - oracle_mod.poisson3d(f, h)).max() < 1e-12
