@@ -61,14 +61,23 @@ typedef enum {
 typedef enum { DFFT_SLAB = 1, DFFT_PENCIL = 2 } dfft_decomp_t;
 
 /* Transform type and precision.  R2C with direction INVERSE is the C2R transform.
- * R2R (reading R21 in DESIGN.md): FORWARD = the DCT-II along every axis (FFTW REDFT10,
- * X_k = 2 Σ x_n cos(πk(2n+1)/(2N))), INVERSE = the DCT-III along every axis divided by 2N per
- * axis, so INVERSE(FORWARD(x)) = x.  Both boxes are real (float/double), x-fastest; every extent
- * must be even and nx/2, ny, nz supported lengths; the x split of the D2/D3 layouts is in pairs
- * of reals.  dfft_plan_set_poisson does not apply (UNSUPPORTED). */
+ * R2R (reading R21 in DESIGN.md): by default FORWARD = the DCT-II along every axis (FFTW
+ * REDFT10, X_k = 2 Σ x_n cos(πk(2n+1)/(2N))), INVERSE = the DCT-III along every axis divided by 2N
+ * per axis, so INVERSE(FORWARD(x)) = x; dfft_plan_create_kinds picks DCT or DST per axis.  Both
+ * boxes are real (float/double), x-fastest; every extent must be even and nx/2, ny, nz supported
+ * lengths; the x split of the D2/D3 layouts is in pairs of reals. */
 typedef enum {
   DFFT_C2C_F32 = 1, DFFT_C2C_F64 = 2, DFFT_R2C_F32 = 3, DFFT_R2C_F64 = 4, DFFT_R2R_F32 = 5, DFFT_R2R_F64 = 6
 } dfft_type_t;
+
+/* Per-axis transform kinds (dfft_plan_create_kinds; "C2C, R2C and R2R", "DCT and DST",
+ * P:620 the (Periodic, Periodic, Bounded) topology; reading R22).  Forward / inverse:
+ *   DFFT_KIND_DFT  (Periodic):            the DFT / the conjugate DFT ÷ n
+ *   DFFT_KIND_DCT2 (Bounded, Neumann):    DCT-II  X_k = 2 Σ x_n cos(πk(2n+1)/(2n_))  / DCT-III ÷ 2n_
+ *   DFFT_KIND_DST2 (Bounded, Dirichlet):  DST-II  X_k = 2 Σ x_n sin(π(k+1)(2n+1)/(2n_)) / DST-III ÷ 2n_
+ * (FFTW REDFT10 / RODFT10 and their inverses REDFT01 / RODFT01 ÷ 2n_.)  A DCT / DST along y or z of
+ * complex data transforms the real and imaginary parts alike. */
+enum { DFFT_KIND_DFT = 0, DFFT_KIND_DCT2 = 1, DFFT_KIND_DST2 = 2 };
 
 /* Sign of the exponent: FORWARD = -1, INVERSE = +1 with the 1/N scale. */
 typedef enum { DFFT_FORWARD = -1, DFFT_INVERSE = 1 } dfft_direction_t;
@@ -150,6 +159,20 @@ dfft_status_t dfft_comm_destroy(dfft_comm_t comm);
 dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, int64_t ny, int64_t nz,
                                dfft_decomp_t decomp, int p1, int p2, dfft_type_t type,
                                dfft_direction_t direction, uint64_t flags);
+/*
+ * Same, with a transform kind per axis (x, y, z): kinds[d] ∈ DFFT_KIND_*.  dfft_plan_create is this
+ * with all-DFT kinds for C2C / R2C types and all-DCT2 for R2R.  Allowed combinations:
+ *   C2C and R2C: kinds[0] = DFT (x periodic; R2C halves it), kinds[1], kinds[2] any — e.g. the
+ *                paper's (Periodic, Periodic, Bounded) box is R2C with {DFT, DFT, DCT2} (Neumann)
+ *                or {DFT, DFT, DST2} (Dirichlet);
+ *   R2R:         DCT2 or DST2 on every axis (real boxes both ways, x split in pairs of reals).
+ * Every DCT / DST axis needs an even extent.  Boxes, layouts, transports and the other arguments
+ * are as for dfft_plan_create; errors: INVALID_VALUE for a bad kind, UNSUPPORTED for a combination
+ * outside the list.
+ */
+dfft_status_t dfft_plan_create_kinds(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, int64_t ny, int64_t nz,
+                                     dfft_decomp_t decomp, int p1, int p2, dfft_type_t type, const int kinds[3],
+                                     dfft_direction_t direction, uint64_t flags);
 
 /* This rank's input (which = 0) or output (which = 1) box, x,y,z order.  For a simulated
  * comm use dfft_plan_box_rank. */
@@ -219,15 +242,18 @@ dfft_status_t dfft_execute_host_chain(const dfft_plan_t* plans, int nplans, cons
 dfft_status_t dfft_execute_sim(dfft_plan_t plan, const void* const* ins, void* const* outs, void* stream);
 
 /*
- * Periodic Poisson solve, fused (the paper's application, §VI-B:
- * the Oceananigans pressure Poisson solver on a (Periodic, Periodic, Periodic) box).
- * Turns a FORWARD plan into  F(k) -> F(k) / λ(k),  λ(k) = -Σ_d (2 sin(π k_d / n_d) / h_d)²
- * (the eigenvalues of the 7-point discrete Laplacian with spacings h = (dx, dy, dz); DESIGN.md
- * reading R20), with F(0) -> 0 (the zero-mean solution).  The multiply is fused into the
- * epilogue of the plan's last stage (no extra pass over HBM).  Executing the forward plan and
- * then the matching INVERSE plan (C2R for R2C plans) solves ∇²φ = f for zero-mean φ.
- * dx = dy = dz = 0 switches the multiplier off again.  Synchronises the device (plan setup,
- * not for the hot path).  Errors: INVALID_VALUE for an inverse plan or non-positive spacings.
+ * Poisson solve, fused (the paper's application, §VI-B: the
+ * Oceananigans pressure Poisson solver on a (Periodic, Periodic, Periodic) box, and P:620's
+ * (Periodic, Periodic, Bounded) box).  Turns a FORWARD plan into  F(k) -> F(k) / λ(k),
+ * λ(k) = Σ_d λ_d(k_d) with λ_d(k) = -(2 sin(θ_k) / h_d)² and θ_k = πk/n_d on a DFT axis
+ * (periodic), πk/(2n_d) on a DCT2 axis (Neumann: cell-centred mirror boundary), π(k+1)/(2n_d) on
+ * a DST2 axis (Dirichlet: antimirror boundary) — the eigenvalues of the 7-point discrete Laplacian
+ * with spacings h = (dx, dy, dz) and those boundaries (readings R20, R22) — and F(k) -> 0
+ * where λ(k) = 0 (the zero-mean solution; only k = 0 without a Dirichlet axis).  The multiply is
+ * fused into the epilogue of the plan's last stage (no extra pass over HBM).  Executing the
+ * forward plan and then the matching INVERSE plan solves ∇²φ = f.  dx = dy = dz = 0 switches the
+ * multiplier off again.  Synchronises the device (plan setup, not for the hot path).  Errors:
+ * INVALID_VALUE for an inverse plan or non-positive spacings.
  */
 dfft_status_t dfft_plan_set_poisson(dfft_plan_t plan, double dx, double dy, double dz);
 

@@ -35,8 +35,9 @@ EXPORTS = [
     "dfft_plan_bytes", "dfft_decomp_box", "dfft_plan_chunks", "dfft_execute", "dfft_execute_host", "dfft_execute_sim",
     "dfft_destroy", "dfft_fft1d", "dfft_plan_set_profiling", "dfft_plan_phase_times", "dfft_plan_stage_bytes",
     "dfft_plan_set_poisson", "dfft_kernel_launches", "dfft_plan_timeline", "dfft_set_timeout_ms", "dfft_plan_status",
-    "dfft_execute_host_chain",
+    "dfft_execute_host_chain", "dfft_plan_create_kinds",
 ]
+KINDS = {"dft": 0, "dct": 1, "dst": 2}  # DFFT_KIND_*: periodic, Neumann (DCT-II), Dirichlet (DST-II)
 PHASES = ["stage_A", "exchange_1", "stage_B", "exchange_2", "stage_C"]
 
 _lib = None
@@ -81,6 +82,8 @@ def lib():
         L.dfft_comm_destroy.argtypes = [_vp]
         L.dfft_plan_create.argtypes = [ctypes.POINTER(_vp), _vp, _i64, _i64, _i64, _int, _int, _int, _int, _int,
                                        ctypes.c_uint64]
+        L.dfft_plan_create_kinds.argtypes = [ctypes.POINTER(_vp), _vp, _i64, _i64, _i64, _int, _int, _int, _int,
+                                             ctypes.POINTER(_int), _int, ctypes.c_uint64]
         L.dfft_plan_box.argtypes = [_vp, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
         L.dfft_plan_box_rank.argtypes = [_vp, _int, _int, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
         L.dfft_plan_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t),
@@ -184,18 +187,26 @@ class Comm:
 # ---------------------------------------------------------------------------------- plan
 class Plan:
     """A distributed 3D FFT plan (dfft_plan_create).  dtype: c2c_f32 | c2c_f64 | r2c_f32 | r2c_f64 |
-    r2r_f32 | r2r_f64 (DCT-II forward / DCT-III/(2N) inverse per axis, real boxes)."""
+    r2r_f32 | r2r_f64 (DCT-II forward / DCT-III/(2N) inverse per axis, real boxes).  kinds: per-axis
+    transform kinds ("dft" | "dct" | "dst" for x, y, z; dfft_plan_create_kinds), e.g. the paper's
+    (Periodic, Periodic, Bounded) box = r2c with ("dft", "dft", "dct")."""
 
     def __init__(self, comm: Comm, shape: Sequence[int], decomp: str = "pencil", grid: Sequence[int] = (1, 1),
                  dtype: str = "c2c_f32", direction: int = FORWARD, chunks: int = 0, overlap: bool = True,
-                 exchange: str = "auto"):
+                 exchange: str = "auto", kinds=None):
         self.comm, self.shape, self.dtype, self.direction = comm, tuple(int(s) for s in shape), dtype, direction
         self.decomp = decomp
         flags = flag_chunks(chunks) | (0 if overlap else FLAG_NO_OVERLAP) | {"nccl": FLAG_NCCL, "p2p": FLAG_FUSED_STORE, "ce": FLAG_CE, "hybrid": FLAG_HYBRID, "auto": 0}[exchange]
         h = _vp()
         d = SLAB if decomp == "slab" else PENCIL
-        _check(lib().dfft_plan_create(ctypes.byref(h), comm.h, *self.shape, d, int(grid[0]), int(grid[1]),
-                                      TYPES[dtype], direction, flags), "dfft_plan_create")
+        self.kinds = tuple(kinds) if kinds is not None else None
+        if kinds is None:
+            _check(lib().dfft_plan_create(ctypes.byref(h), comm.h, *self.shape, d, int(grid[0]), int(grid[1]),
+                                          TYPES[dtype], direction, flags), "dfft_plan_create")
+        else:
+            ks = (_int * 3)(*[KINDS[k] for k in kinds])
+            _check(lib().dfft_plan_create_kinds(ctypes.byref(h), comm.h, *self.shape, d, int(grid[0]), int(grid[1]),
+                                                TYPES[dtype], ks, direction, flags), "dfft_plan_create_kinds")
         self.h = h
 
     # boxes ------------------------------------------------------------------------

@@ -180,7 +180,7 @@ dfft_status_t get_split_twiddles(int N, bool f64, int dir, int dev, const void**
   return DFFT_SUCCESS;
 }
 
-inline bool is_contig(int family) { return family != kStrided && family != kStridedDct; }
+inline bool is_contig(int family) { return family != kStrided && family != kStridedDct && family != kStridedDst; }
 
 // R2R (DCT) post/pre twiddles: c_k = exp(dir·iπk/(2L)), k ∈ [0, L), long double once each.
 dfft_status_t get_dct_twiddles(int L, bool f64, int dir, int dev, const void** out) {
@@ -353,7 +353,8 @@ struct dfft_plan_s {
   int64_t nx = 0, ny = 0, nz = 0;
   int P1 = 1, P2 = 1, K = 1, dir = -1;
   bool f64 = false, r2c = false, overlap = true;
-  bool r2r = false;  // DCT-II forward / DCT-III inverse along every axis (reading R21)
+  bool r2r = false;  // real x axis transformed by a DCT / DST (reading R21, R22)
+  int kind[3] = {0, 0, 0};  // per-axis transform kind (DFFT_KIND_*): DFT, DCT-II, DST-II
   size_t es = 8;  // complex element bytes
   std::vector<RankPlan> ranks;
   ncclComm_t row = nullptr, col = nullptr;
@@ -411,9 +412,15 @@ namespace {
 
 // x lines are real (R2C/C2R, R2R): nx reals per line = nx/2 complex elements on the kernel side
 inline bool xreal(const dfft_plan_s* pl) { return pl->r2c || pl->r2r; }
-inline int fam_x_fwd(const dfft_plan_s* pl) { return pl->r2c ? kContigR2C : pl->r2r ? kContigDct : kContig; }
-inline int fam_x_inv(const dfft_plan_s* pl) { return pl->r2c ? kContigC2R : pl->r2r ? kContigDct : kContig; }
-inline int fam_s(const dfft_plan_s* pl) { return pl->r2r ? kStridedDct : kStrided; }
+inline int fam_x_r2r(const dfft_plan_s* pl) { return pl->kind[0] == DFFT_KIND_DST2 ? kContigDst : kContigDct; }
+inline int fam_x_fwd(const dfft_plan_s* pl) { return pl->r2c ? kContigR2C : pl->r2r ? fam_x_r2r(pl) : kContig; }
+inline int fam_x_inv(const dfft_plan_s* pl) { return pl->r2c ? kContigC2R : pl->r2r ? fam_x_r2r(pl) : kContig; }
+// strided stage along y (axis 1) or z (axis 2): the axis's kind picks the kernel family
+inline int fam_axis(const dfft_plan_s* pl, int axis) {
+  return pl->kind[axis] == DFFT_KIND_DCT2 ? kStridedDct : pl->kind[axis] == DFFT_KIND_DST2 ? kStridedDst : kStrided;
+}
+inline int fam_y(const dfft_plan_s* pl) { return fam_axis(pl, 1); }
+inline int fam_z(const dfft_plan_s* pl) { return fam_axis(pl, 2); }
 
 // ------------------------------------------------------------------------------ stage builders
 dfft_status_t upload_table(const std::vector<longlong2>& h, void** d) {
@@ -526,10 +533,11 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   }
   ST(get_kernel(family, n, pl->f64, pl->dir, &s.k));
   ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw));
-  if (family == kContigR2C || family == kContigC2R || family == kContigDct)
+  const bool contig_r2r = family == kContigDct || family == kContigDst;
+  if (family == kContigR2C || family == kContigC2R || contig_r2r)
     ST(get_split_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw2));
-  if (family == kContigDct || family == kStridedDct)  // c_k over the real line length L
-    ST(get_dct_twiddles(family == kContigDct ? 2 * n : n, pl->f64, pl->dir, pl->comm->device, &s.a.tw3));
+  if (contig_r2r || family == kStridedDct || family == kStridedDst)  // c_k over the real line length L
+    ST(get_dct_twiddles(contig_r2r ? 2 * n : n, pl->f64, pl->dir, pl->comm->device, &s.a.tw3));
   if (in_tab) ST(upload_table(*in_tab, &s.in_tab));
   if (out_tab) ST(upload_table(*out_tab, &s.out_tab));
   s.a.in.ttab = (const SegEnt*)s.in_tab;
@@ -551,10 +559,14 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
       }
     }
   }
+  // contig: walk lines so that consecutive CTAs write adjacent lines (unsegmented outputs)
+  if (is_contig(family) && !out_tab && !getenv("DFFT_LORDER0") && s.a.out.bw == 0 && L1 > 1 &&
+      std::llabs(s.a.out.s1) < std::llabs(s.a.out.s0))
+    s.a.lorder = 1;
   if (is_contig(family)) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
   else s.grid = ((L0 + s.k.per_cta - 1) / s.k.per_cta) * L1;
   if (s.grid >= (1LL << 31)) return fail(DFFT_ERR_UNSUPPORTED, "grid too large (%lld CTAs)", s.grid);
-  if ((family == kStrided || family == kStridedDct) && s.k.tma_fn && g_use_tma && !in_tab &&
+  if ((family == kStrided || family == kStridedDct || family == kStridedDst) && s.k.tma_fn && g_use_tma && !in_tab &&
       tensor_map_encoder()) {
     const long long es = (long long)pl->es;
     bool ok = s.a.in.s0 == 1 && (s.a.in.tstride * es) % 16 == 0 && (L1 == 1 || (s.a.in.s1 * es) % 16 == 0) &&
@@ -572,8 +584,9 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
         s.tma_variant = 1;
         s.tma_grid = std::min<long long>(tiles, (long long)sms * occ);
         s.tma_occ = occ;
-        ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, s.k.tma_maxr));
       }
+      if (s.tma_variant == 1)  // the TMA variant's own radix schedule
+        ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, s.k.tma_maxr));
       if (getenv("DFFT_DEBUG"))
         fprintf(stderr, "dfft: strided n=%d L0=%lld L1=%lld tma grid %lld (occ %d)\n", n, L0, L1, s.tma_grid, occ);
     }
@@ -792,7 +805,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       B.a.out.mT = g.nz;
     }
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, fam_s(pl), (int)g.ny, Xn, zc, nullptr, &bseg));
+    ST(finish_stage(pl, B, fam_y(pl), (int)g.ny, Xn, zc, nullptr, &bseg));
     // ---- exchange 2 (column group)
     Exchange& E2 = rp.E2[k];
     E2.comm = 1;
@@ -839,7 +852,7 @@ dfft_status_t build_forward(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   C.last_fwd = true;  // t = z, l0 = x, l1 = y
   C.gax[0] = 2, C.gax[1] = 0, C.gax[2] = 1;
   C.glo[1] = g.Xlo(i), C.glo[2] = g.Y3lo(j);
-  ST(finish_stage(pl, C, fam_s(pl), (int)g.nz, Xn, Y3n, nullptr, nullptr));
+  ST(finish_stage(pl, C, fam_z(pl), (int)g.nz, Xn, Y3n, nullptr, nullptr));
   return DFFT_SUCCESS;
 }
 
@@ -897,7 +910,7 @@ dfft_status_t build_forward_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     B.a.out.bw = (int)g.wy;
     B.a.out.mT = g.nz;
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, fam_s(pl), (int)g.ny, xc, Zn, nullptr, &bseg));
+    ST(finish_stage(pl, B, fam_y(pl), (int)g.ny, xc, Zn, nullptr, &bseg));
     Exchange& E2 = rp.E2[k];
     E2.comm = 1;
     E2.fused = true;
@@ -916,7 +929,7 @@ dfft_status_t build_forward_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.last_fwd = true;  // t = z, l0 = x - x0, l1 = y
     C.gax[0] = 2, C.gax[1] = 0, C.gax[2] = 1;
     C.glo[1] = g.Xlo(i) + x0, C.glo[2] = g.Y3lo(j);
-    ST(finish_stage(pl, C, fam_s(pl), (int)g.nz, xc, Y3n, nullptr, nullptr));
+    ST(finish_stage(pl, C, fam_z(pl), (int)g.nz, xc, Y3n, nullptr, nullptr));
   }
   return DFFT_SUCCESS;
 }
@@ -951,7 +964,7 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   A.a.out.bw = (int)g.wz;
   A.a.out.mT = g.ny;
   A.a.scale = 1.0;
-  ST(finish_stage(pl, A, fam_s(pl), (int)g.nz, Xn, Y3n, nullptr, &aseg));
+  ST(finish_stage(pl, A, fam_z(pl), (int)g.nz, Xn, Y3n, nullptr, &aseg));
   for (long long k = 1; k < K; ++k) rp.A[k].empty = true;
   rp.E1[0].comm = 1;
   rp.E1[0].fused = true;
@@ -980,7 +993,7 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     B.a.out.bw = (int)g.wy;
     B.a.out.mT = Zn;
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, fam_s(pl), (int)g.ny, Xn, zc, nullptr, &bseg));
+    ST(finish_stage(pl, B, fam_y(pl), (int)g.ny, Xn, zc, nullptr, &bseg));
     Exchange& E2 = rp.E2[k];
     E2.comm = 0;
     E2.fused = true;
@@ -1032,7 +1045,7 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     Z.out = {kWs, c2r ? W * es : 0};
     set_side(Z.a.out, nxc, 1, nz * nxc);
     Z.a.scale = 1.0;
-    return finish_stage(pl, Z, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr);
+    return finish_stage(pl, Z, fam_z(pl), (int)nz, nxc, ny, nullptr, nullptr);
   };
   if (pl->dir == DFFT_FORWARD) {
     // forward with one large-pitch side in total (r01 session 2): the x-pass writes [y][z][x],
@@ -1049,7 +1062,7 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     B.out = {kWs, 0};
     set_side(B.a.out, ny * nxc, 1, nxc);
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, fam_s(pl), (int)nz, nxc, ny, nullptr, nullptr));
+    ST(finish_stage(pl, B, fam_z(pl), (int)nz, nxc, ny, nullptr, nullptr));
     C.in = {kWs, 0};  // y-pass: columns (l0 = x, l1 = z), natural -> natural
     set_side(C.a.in, nxc, 1, ny * nxc);
     C.out = {kUserOut, 0};
@@ -1057,14 +1070,14 @@ dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     C.a.scale = 1.0;
     C.last_fwd = true;  // t = y, l0 = x, l1 = z
     C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
-    ST(finish_stage(pl, C, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
+    ST(finish_stage(pl, C, fam_y(pl), (int)ny, nxc, nz, nullptr, nullptr));
   } else {
     A.in = {kUserIn, 0};  // columns (l0 = x, l1 = z)
     set_side(A.a.in, nxc, 1, ny * nxc);
     A.out = c2r ? Ref{kWs, 0} : Ref{kUserOut, 0};
     set_side(A.a.out, nxc, 1, ny * nxc);
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, fam_s(pl), (int)ny, nxc, nz, nullptr, nullptr));
+    ST(finish_stage(pl, A, fam_y(pl), (int)ny, nxc, nz, nullptr, nullptr));
     ST(zpass(B));
     C.in = {kWs, c2r ? W * es : 0};  // lines (l0 = y, l1 = z) of ws [y][z][x]
     set_side(C.a.in, 1, nz * nxc, nxc);
@@ -1132,7 +1145,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       A.a.out.mT = g.ny;
     }
     A.a.scale = 1.0;
-    ST(finish_stage(pl, A, fam_s(pl), (int)g.nz, xc, Y3n, nullptr, &aseg));
+    ST(finish_stage(pl, A, fam_z(pl), (int)g.nz, xc, Y3n, nullptr, &aseg));
     // first exchange of the inverse = T2⁻¹ on the column group
     Exchange& E1 = rp.E1[k];
     E1.comm = 1;
@@ -1185,7 +1198,7 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       B.a.out.mT = Zn;
     }
     B.a.scale = 1.0;
-    ST(finish_stage(pl, B, fam_s(pl), (int)g.ny, xc, Zn, nullptr, &bseg));
+    ST(finish_stage(pl, B, fam_y(pl), (int)g.ny, xc, Zn, nullptr, &bseg));
     // second exchange of the inverse = T1⁻¹ on the row group
     Exchange& E2 = rp.E2[k];
     E2.comm = 0;
@@ -1249,7 +1262,21 @@ void* resolve(const Ref& r, const Ctx& c) {
   }
 }
 
+dfft_status_t launch_impl(const Stage& s, const Ctx& c, cudaStream_t st);
+// DFFT_DEBUG_SYNC=1: synchronise after every stage launch and name the stage that failed
 dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
+  static const bool dbg = getenv("DFFT_DEBUG_SYNC") != nullptr;
+  const dfft_status_t r = launch_impl(s, c, st);
+  if (dbg && r == DFFT_SUCCESS) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess)
+      return fail(DFFT_ERR_CUDA, "stage (family %d, n %d, L0 %lld, L1 %lld, tma %d) failed: %s", s.family, s.n, s.a.L0,
+                  s.a.L1, s.tma_variant, cudaGetErrorString(e));
+  }
+  return r;
+}
+
+dfft_status_t launch_impl(const Stage& s, const Ctx& c, cudaStream_t st) {
   if (s.empty) return DFFT_SUCCESS;
   g_launches.fetch_add(1, std::memory_order_relaxed);  // exactly one kernel per stage launch
   PassArgs a = s.a;
@@ -1298,9 +1325,10 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
       a.tw = s.tw_tma;
       void* targs[] = {&tin, &tout, &a};
       const long long grid = s.sm_cap > 0 ? std::min<long long>(s.tma_grid, (long long)s.sm_cap * s.tma_occ) : s.tma_grid;
-      if (spec && !(use_st && s.tma_variant == 1 && s.k.tma_st_spec_fn)) goto plain;  // multiplier: TST or plain
       if (s.k.tma_st_only && !use_st) goto plain;  // R2R: the TMA variant needs TMA stores
-      if (spec)
+      // multiplier: the c2c TMA-store variant with SPEC, or the R2R kernel (runtime multiplier)
+      if (spec && !s.k.tma_st_only && !(use_st && s.tma_variant == 1 && s.k.tma_st_spec_fn)) goto plain;
+      if (spec && !s.k.tma_st_only)
         CU(cudaLaunchKernel(s.k.tma_st_spec_fn, dim3((unsigned)grid), dim3(s.k.tma_threads), targs, s.k.tma_smem, st));
       else
         CU(cudaLaunchKernel(a.out.nbulk > 0 ? s.k.tma_bk_fn
@@ -2171,9 +2199,9 @@ dfft_status_t dfft_comm_destroy(dfft_comm_t c) {
   return DFFT_SUCCESS;
 }
 
-// argument validation shared by dfft_plan_create and dfft_decomp_box; maps slab to pencil 1×P
+// argument validation shared by dfft_plan_create(_kinds) and dfft_decomp_box; maps slab to pencil 1×P
 static dfft_status_t validate(int P, int64_t nx, int64_t ny, int64_t nz, dfft_decomp_t decomp, int* p1p, int* p2p,
-                              dfft_type_t type, dfft_direction_t direction) {
+                              dfft_type_t type, dfft_direction_t direction, const int* kinds = nullptr) {
   int p1 = *p1p, p2 = *p2p;
   if (nx <= 0 || ny <= 0 || nz <= 0) return fail(DFFT_ERR_INVALID_VALUE, "grid extents must be positive");
   if (direction != DFFT_FORWARD && direction != DFFT_INVERSE) return fail(DFFT_ERR_INVALID_VALUE, "bad direction");
@@ -2189,14 +2217,25 @@ static dfft_status_t validate(int P, int64_t nx, int64_t ny, int64_t nz, dfft_de
     return fail(DFFT_ERR_INVALID_VALUE, "proc grid %d x %d != nranks %d", p1, p2, P);
   bool r2c = type == DFFT_R2C_F32 || type == DFFT_R2C_F64;
   bool r2r = type == DFFT_R2R_F32 || type == DFFT_R2R_F64;
+  if (kinds) {  // per-axis kinds (reading R22): x DFT for C2C / R2C, DCT or DST for R2R; y, z any (R2R: not DFT)
+    for (int d = 0; d < 3; ++d)
+      if (kinds[d] < DFFT_KIND_DFT || kinds[d] > DFFT_KIND_DST2) return fail(DFFT_ERR_INVALID_VALUE, "bad kind on axis %d", d);
+    if (!r2r && kinds[0] != DFFT_KIND_DFT)
+      return fail(DFFT_ERR_UNSUPPORTED, "C2C / R2C plans take the DFT along x (bounded x needs an R2R plan)");
+    if (r2r && (kinds[0] == DFFT_KIND_DFT || kinds[1] == DFFT_KIND_DFT || kinds[2] == DFFT_KIND_DFT))
+      return fail(DFFT_ERR_UNSUPPORTED, "R2R plans take a DCT or DST on every axis (periodic x with bounded y/z: R2C)");
+  }
   if (r2c && nx % 2) return fail(DFFT_ERR_UNSUPPORTED, "R2C needs even nx");
   if (r2r && (nx % 2 || ny % 2 || nz % 2))
-    return fail(DFFT_ERR_UNSUPPORTED, "R2R (DCT via Makhoul's permutation) needs even extents");
+    return fail(DFFT_ERR_UNSUPPORTED, "R2R (DCT/DST via Makhoul's permutation) needs even extents");
+  for (int d = 1; d < 3; ++d)
+    if (kinds && kinds[d] != DFFT_KIND_DFT && (d == 1 ? ny : nz) % 2)
+      return fail(DFFT_ERR_UNSUPPORTED, "a DCT / DST axis needs an even extent");
   long long nxc = r2c ? nx / 2 + 1 : r2r ? nx / 2 : nx;
   long long nfft_x = (r2c || r2r) ? nx / 2 : nx;
   if (!length_ok(nfft_x) || !length_ok(ny) || !length_ok(nz))
-    return fail(DFFT_ERR_UNSUPPORTED, "axis lengths (%lld,%lld,%lld): need 2^a 3^b 5^c 7^d from the instantiated set",
-                (long long)nfft_x, (long long)ny, (long long)nz);
+    return fail(DFFT_ERR_UNSUPPORTED, "axis FFT lengths (%lld,%lld,%lld): each must be one of the supported lengths "
+                "(include/dfft.h)", (long long)nfft_x, (long long)ny, (long long)nz);
   if (p1 > ny || p1 > nxc || p2 > nz || p2 > ny)
     return fail(DFFT_ERR_INFEASIBLE_DECOMP, "grid %d x %d leaves an empty block for (%lld,%lld,%lld)", p1, p2,
                 (long long)nx, (long long)ny, (long long)nz);
@@ -2229,10 +2268,19 @@ dfft_status_t dfft_decomp_box(int64_t nx, int64_t ny, int64_t nz, dfft_decomp_t 
 dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, int64_t ny, int64_t nz,
                                dfft_decomp_t decomp, int p1, int p2, dfft_type_t type, dfft_direction_t direction,
                                uint64_t flags) {
-  if (!plan || !comm) return fail(DFFT_ERR_INVALID_VALUE, "null plan/comm");
+  const bool r2r = type == DFFT_R2R_F32 || type == DFFT_R2R_F64;
+  const int kinds[3] = {r2r ? DFFT_KIND_DCT2 : DFFT_KIND_DFT, r2r ? DFFT_KIND_DCT2 : DFFT_KIND_DFT,
+                        r2r ? DFFT_KIND_DCT2 : DFFT_KIND_DFT};
+  return dfft_plan_create_kinds(plan, comm, nx, ny, nz, decomp, p1, p2, type, kinds, direction, flags);
+}
+
+dfft_status_t dfft_plan_create_kinds(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, int64_t ny, int64_t nz,
+                                     dfft_decomp_t decomp, int p1, int p2, dfft_type_t type, const int kinds[3],
+                                     dfft_direction_t direction, uint64_t flags) {
+  if (!plan || !comm || !kinds) return fail(DFFT_ERR_INVALID_VALUE, "null plan/comm/kinds");
   *plan = nullptr;
   int P = comm->nranks;
-  ST(validate(P, nx, ny, nz, decomp, &p1, &p2, type, direction));
+  ST(validate(P, nx, ny, nz, decomp, &p1, &p2, type, direction, kinds));
   bool r2c = type == DFFT_R2C_F32 || type == DFFT_R2C_F64;
   bool r2r = type == DFFT_R2R_F32 || type == DFFT_R2R_F64;
   bool f64 = type == DFFT_C2C_F64 || type == DFFT_R2C_F64 || type == DFFT_R2R_F64;
@@ -2297,6 +2345,7 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
   pl->f64 = f64;
   pl->r2c = r2c;
   pl->r2r = r2r;
+  for (int d = 0; d < 3; ++d) pl->kind[d] = kinds[d];
   pl->overlap = overlap;
   pl->es = f64 ? 16 : 8;
   // exchange over NVLink peer memory unless asked for NCCL (flag or DFFT_EXCHANGE=nccl)
@@ -2395,7 +2444,8 @@ dfft_status_t dfft_plan_create(dfft_plan_t* plan, dfft_comm_t comm, int64_t nx, 
     for (long long v : {(long long)nx, (long long)ny, (long long)nz, (long long)decomp, (long long)p1, (long long)p2,
                         (long long)type, (long long)direction, (long long)flags, (long long)pl->p2p, (long long)pl->ce,
                         (long long)pl->hybrid, (long long)pl->bc, (long long)pl->overlap, K, g.wy, g.wz, g.xq,
-                        (long long)pl->flag_off, (long long)pl->ranks[0].sched.size()})
+                        (long long)pl->flag_off, (long long)pl->ranks[0].sched.size(), (long long)pl->kind[0],
+                        (long long)pl->kind[1], (long long)pl->kind[2]})
       mix(v);
     pl->hash = h;
   }
@@ -2606,7 +2656,6 @@ dfft_status_t dfft_execute_sim(dfft_plan_t pl, const void* const* ins, void* con
 dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double dz) {
   if (!pl) return fail(DFFT_ERR_INVALID_VALUE, "null plan");
   if (pl->dir != DFFT_FORWARD) return fail(DFFT_ERR_INVALID_VALUE, "the Poisson multiplier belongs to a forward plan");
-  if (pl->r2r) return fail(DFFT_ERR_UNSUPPORTED, "the periodic Poisson multiplier applies to C2C/R2C plans");
   const bool on = dx > 0 && dy > 0 && dz > 0;
   if (!on && (dx != 0 || dy != 0 || dz != 0))
     return fail(DFFT_ERR_INVALID_VALUE, "grid spacings must all be > 0 (or all 0 to switch the multiplier off)");
@@ -2618,13 +2667,18 @@ dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double
   const double h[3] = {dx, dy, dz};
   const size_t rs = pl->es / 2;
   if (on) {
-    // λ_d(k) = -(2 sin(πk/n_d)/h_d)², long double, rounded once to the plan's precision (reading R20)
+    // λ_d(k) = -(2 sin(θ_k)/h_d)² with θ_k = πk/n_d (periodic, DFT), πk/(2n_d) (Neumann, DCT-II) or
+    // π(k+1)/(2n_d) (Dirichlet, DST-II); long double, rounded once to the plan's precision (R20, R22),
+    // one entry per output bin of the axis (for R2R x: per real bin; see PassArgs::spec_pairs)
     std::vector<unsigned char> host((size_t)(n[0] + n[1] + n[2]) * rs);
     long long o = 0;
     for (int d = 0; d < 3; ++d)
       for (long long k = 0; k < n[d]; ++k, ++o) {
-        const long double sv = 2.0L * sinl(3.14159265358979323846264338327950288L * (long double)k / (long double)n[d]) /
-                               (long double)h[d];
+        const long double PI = 3.14159265358979323846264338327950288L;
+        const long double ang = pl->kind[d] == DFFT_KIND_DFT    ? PI * (long double)k / (long double)n[d]
+                                : pl->kind[d] == DFFT_KIND_DCT2 ? PI * (long double)k / (long double)(2 * n[d])
+                                                                : PI * (long double)(k + 1) / (long double)(2 * n[d]);
+        const long double sv = 2.0L * sinl(ang) / (long double)h[d];
         const long double lam = -(sv * sv);
         if (pl->f64) reinterpret_cast<double*>(host.data())[o] = (double)lam;
         else reinterpret_cast<float*>(host.data())[o] = (float)lam;
@@ -2640,9 +2694,13 @@ dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double
     for (Stage* s : st) {
       if (!s->last_fwd) continue;
       ++nlast;
-      for (int q = 0; q < 3; ++q)
-        s->a.spec[q] = on ? (const void*)((const char*)pl->spec_tab + (size_t)(base[s->gax[q]] + s->glo[q]) * rs)
-                          : nullptr;
+      // R2R: the stage's x index counts pairs of reals, the x table real bins (offset ×2)
+      const bool pairs = pl->r2r;
+      s->a.spec_pairs = pairs ? 1 : 0;
+      for (int q = 0; q < 3; ++q) {
+        const long long off = (pairs && s->gax[q] == 0 ? 2 : 1) * s->glo[q];
+        s->a.spec[q] = on ? (const void*)((const char*)pl->spec_tab + (size_t)(base[s->gax[q]] + off) * rs) : nullptr;
+      }
     }
   }
   if (nlast == 0) return fail(DFFT_ERR_INTERNAL, "plan has no last forward stage");

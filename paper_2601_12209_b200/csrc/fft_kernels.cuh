@@ -367,6 +367,13 @@ struct PassArgs {
   // already offset to the rank's global bins); each output is multiplied by 1/(λt+λ0+λ1), 0 at
   // k = 0.  spec[0] == nullptr: off.
   const void* spec[3];
+  // R2R plans: a complex column l0 carries two real x columns (bins 2·l0 and 2·l0+1), so the x table
+  // (spec[1]) holds one eigenvalue per real bin and re / im take their own factor
+  int spec_pairs;
+  // contig family: line order of consecutive CTAs — 0: l0 fastest, 1: l1 fastest (the host picks the
+  // order whose consecutive lines are adjacent on the output side: scattered 8 KB writes cost more
+  // than scattered 8 KB reads)
+  int lorder;
 };
 
 // tile -> (column tile tx, line l1) under the grouped order above
@@ -577,14 +584,20 @@ __host__ __device__ constexpr int dct_perm(int n, int L) { return n < L / 2 ? 2 
 // complex element q of the line holds (x_{2q}, x_{2q+1}) = (v_q, v_{L-1-q}).
 // (the forward reads its permuted reals straight from global memory: staging its line the same
 // way measured slower, 1.58 vs 2.36 ms at 768x768x384 f64; the inverse gains, 2.07 -> 1.98 ms)
-template <typename C, int N> struct DctXFwdIO : GIO<C, true> {
+// DST (reading R22) by the identities  DST-II(x)_k = DCT-II(x')_{L-1-k},  x'_n = (-1)^n x_n,  and
+// DST-III(X)_n = (-1)^n DCT-III(X')_n,  X'_k = X_{L-1-k}:  sign-flipped loads and a reversed
+// output (forward), reversed loads and sign-flipped outputs (inverse).
+template <bool DST, typename R> __device__ __forceinline__ R alt_sign(int n, R v) { return (DST && (n & 1)) ? -v : v; }
+
+template <typename C, int N, bool DST = false> struct DctXFwdIO : GIO<C, true> {
   C* zb;  // the last pass's outputs
   __device__ __forceinline__ C load(int t) const {
-    return {this->load_real(dct_perm(2 * t, 2 * N)), this->load_real(dct_perm(2 * t + 1, 2 * N))};
+    const int p0 = dct_perm(2 * t, 2 * N), p1 = dct_perm(2 * t + 1, 2 * N);
+    return {alt_sign<DST>(p0, this->load_real(p0)), alt_sign<DST>(p1, this->load_real(p1))};
   }
   __device__ __forceinline__ void store(int t, C v) const { zb[t] = v; }
 };
-template <typename C, int N> struct DctXInvIO : GIO<C, true> {
+template <typename C, int N, bool DST = false> struct DctXInvIO : GIO<C, true> {
   using R = decltype(C{}.x);
   static constexpr bool kSyncAfterLoad = true;
   const C* tw2;  // exp(+2πi t / 2N)
@@ -592,7 +605,9 @@ template <typename C, int N> struct DctXInvIO : GIO<C, true> {
   const R* xr;   // the staged input line (2N reals)
   C* zb;         // the last pass's outputs z_t = (v_{2t}, v_{2t+1}) (times N)
   __device__ __forceinline__ C vk(int k) const {  // V_k = ½·conj(c_k)·(X_k − i·X_{L−k}), k ≤ N
-    const R xk = xr[k], xl = k == 0 ? R(0) : xr[2 * N - k];
+    // (DST: X'_k = X_{L-1-k})
+    const R xk = DST ? (k == 2 * N ? R(0) : xr[2 * N - 1 - k]) : xr[k];
+    const R xl = k == 0 ? R(0) : DST ? xr[k - 1] : xr[2 * N - k];
     const C c = __ldg(tw3 + k);
     const C d = {xk * R(0.5), -xl * R(0.5)};
     return cmul(c, d);
@@ -608,6 +623,7 @@ template <typename C, int N> struct DctXInvIO : GIO<C, true> {
   __device__ __forceinline__ void store(int t, C v) const { zb[t] = v; }
 };
 
+// MODE 0 c2c, 1 R2C, 2 C2R, 3 / 4 DCT-II / DCT-III of real x-lines, 5 / 6 DST-II / DST-III
 template <typename Real, int N, int DIR, int MODE, bool TB = false>
 __global__ void __launch_bounds__(ContigCfg<N>::THREADS)
 fft_contig_kernel(const __grid_constant__ PassArgs a) {
@@ -619,8 +635,16 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
   const int j = threadIdx.x % Cfg::S.T;
   const long long line = (long long)blockIdx.x * Cfg::LPC + li;
   const bool active = line < a.L0 * a.L1;
-  const long long l1 = active ? line / a.L0 : 0;
-  const long long l0 = active ? line - l1 * a.L0 : 0;
+  long long l0 = 0, l1 = 0;
+  if (active) {
+    if (a.lorder) {
+      l0 = line / a.L1;
+      l1 = line - l0 * a.L1;
+    } else {
+      l1 = line / a.L0;
+      l0 = line - l1 * a.L0;
+    }
+  }
   ContigSM sm{li * Cfg::LS};
   const C* tw = reinterpret_cast<const C*>(a.tw);
   if constexpr (MODE == 0) {
@@ -651,9 +675,10 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
     io.init(a.in, a.out, l0, l1, a.scale);
     io.tw2 = reinterpret_cast<const C*>(a.tw2);
     stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
-  } else if constexpr (MODE == 3) {  // forward DCT-II of real x-lines of length 2N
+  } else if constexpr (MODE == 3 || MODE == 5) {  // forward DCT-II / DST-II of real x-lines of length 2N
     using R = Real;
-    DctXFwdIO<C, N> io;
+    constexpr bool DST = MODE == 5;
+    DctXFwdIO<C, N, DST> io;
     io.init(a.in, a.out, l0, l1, a.scale);
     C* zb = smem + li * Cfg::LS;
     io.zb = zb;
@@ -669,16 +694,18 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
         const C w = k == N ? C{-1, 0} : __ldg(tw2 + k);
         const C v = cadd(e, cmul(w, o));  // V_k of the real permuted line, k <= N
         const C ck = __ldg(tw3 + k);
-        io.store_real(k, R(2) * (ck.x * v.x - ck.y * v.y));  // X_k = 2 Re(c_k V_k)
-        if (k > 0 && k < N) {  // X_{2N-k} = 2 Re(c_{2N-k} conj V_k)
+        // X_k = 2 Re(c_k V_k)  (DST: stored at 2N-1-k)
+        io.store_real(DST ? 2 * N - 1 - k : k, R(2) * (ck.x * v.x - ck.y * v.y));
+        if (k > 0 && k < N) {  // X_{2N-k} = 2 Re(c_{2N-k} conj V_k)  (DST: at k-1)
           const C cl = __ldg(tw3 + 2 * N - k);
-          io.store_real(2 * N - k, R(2) * (cl.x * v.x + cl.y * v.y));
+          io.store_real(DST ? k - 1 : 2 * N - k, R(2) * (cl.x * v.x + cl.y * v.y));
         }
       }
     }
-  } else {  // MODE 4: inverse DCT-III of real x-lines of length 2N (scale folded by the host)
+  } else {  // MODE 4 / 6: inverse DCT-III / DST-III of real x-lines of length 2N (scale by the host)
     using R = Real;
-    DctXInvIO<C, N> io;
+    constexpr bool DST = MODE == 6;
+    DctXInvIO<C, N, DST> io;
     io.init(a.in, a.out, l0, l1, a.scale);
     io.tw2 = reinterpret_cast<const C*>(a.tw2);
     io.tw3 = reinterpret_cast<const C*>(a.tw3);
@@ -692,7 +719,8 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
     __syncthreads();
     if (active) {  // output element q = (x_{2q}, x_{2q+1}) = (v_q, v_{2N-1-q}); coalesced stores
       const R* vr = reinterpret_cast<const R*>(zb);
-      for (int q = j; q < N; q += Cfg::S.T) io.GIO<C, true>::store(q, C{vr[q], vr[2 * N - 1 - q]});
+      for (int q = j; q < N; q += Cfg::S.T)
+        io.GIO<C, true>::store(q, C{vr[q], DST ? -vr[2 * N - 1 - q] : vr[2 * N - 1 - q]});
     }
   }
 }
@@ -750,17 +778,19 @@ fft_strided_kernel(const __grid_constant__ PassArgs a) {
 //   X_k = (2 Re(c_k Va_k), 2 Re(c_k Vb_k))  — the last pass goes to shared memory and each thread
 // finishes the pairs (k, N−k).  Inverse: Z_t = Va_t + i·Vb_t with V from rows t and N−t, z =
 // IDFT_N(Z) (unnormalised; the host folds 1/N), row perm(t) = z_t.
-template <typename C, int N, int DIR> struct DctStridedIO : GIO<C> {
+template <typename C, int N, int DIR, bool DST = false> struct DctStridedIO : GIO<C> {
   using R = decltype(C{}.x);
   const C* tw3;  // c_k = exp(DIR·iπk/(2N)), k < N
   C* tile;       // forward: the last pass's outputs, dense [t][W] at column c
   int W, c;
   __device__ __forceinline__ C load(int t) const {
     if constexpr (DIR < 0) {
-      return GIO<C>::load(dct_perm(t, N));
+      const int p = dct_perm(t, N);
+      const C v = GIO<C>::load(p);
+      return (DST && (p & 1)) ? C{-v.x, -v.y} : v;
     } else {
-      const C xt = GIO<C>::load(t);
-      const C xl = t == 0 ? C{0, 0} : GIO<C>::load(N - t);
+      const C xt = GIO<C>::load(DST ? N - 1 - t : t);
+      const C xl = t == 0 ? C{0, 0} : GIO<C>::load(DST ? t - 1 : N - t);
       const C cc = __ldg(tw3 + t);  // conj(c_t) for the inverse table
       const C da = {xt.x * R(0.5), -xl.x * R(0.5)}, db = {xt.y * R(0.5), -xl.y * R(0.5)};
       const C va = cmul(cc, da), vb = cmul(cc, db);
@@ -768,12 +798,27 @@ template <typename C, int N, int DIR> struct DctStridedIO : GIO<C> {
     }
   }
   __device__ __forceinline__ void store(int t, C v) const {
-    if constexpr (DIR < 0) tile[t * W + c] = v;
-    else GIO<C>::store(dct_perm(t, N), v);
+    if constexpr (DIR < 0) {
+      tile[t * W + c] = v;
+    } else {
+      const int p = dct_perm(t, N);
+      GIO<C>::store(p, (DST && (p & 1)) ? C{-v.x, -v.y} : v);
+    }
   }
 };
 
-template <typename Real, int N, int DIR>
+// multiplier 1/λ of the Poisson solve on a DCT / DST output row (runtime: those stages only)
+template <typename C> __device__ __forceinline__ C dct_spec(const PassArgs& a, int row, long long l0, long long l1, C v) {
+  using R = decltype(C{}.x);
+  if (a.spec[0] == nullptr) return v;
+  const R* lx = reinterpret_cast<const R*>(a.spec[1]);
+  const R base = __ldg(reinterpret_cast<const R*>(a.spec[0]) + row) + __ldg(reinterpret_cast<const R*>(a.spec[2]) + l1);
+  const R lre = base + __ldg(lx + (a.spec_pairs ? 2 * l0 : l0));
+  const R lim = base + __ldg(lx + (a.spec_pairs ? 2 * l0 + 1 : l0));
+  return {lre != R(0) ? v.x / lre : R(0), lim != R(0) ? v.y / lim : R(0)};
+}
+
+template <typename Real, int N, int DIR, bool DST = false>
 __global__ void __launch_bounds__(StridedCfg<Real, N>::THREADS)
 fft_strided_dct_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
@@ -788,7 +833,7 @@ fft_strided_dct_kernel(const __grid_constant__ PassArgs a) {
   const long long l1 = blockIdx.x / ntile;
   const long long l0 = (blockIdx.x - l1 * ntile) * Cfg::W + c;
   const bool active = l0 < a.L0;
-  DctStridedIO<C, N, DIR> io;
+  DctStridedIO<C, N, DIR, DST> io;
   io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
   io.tw3 = reinterpret_cast<const C*>(a.tw3);
   io.tile = tile;
@@ -805,12 +850,14 @@ fft_strided_dct_kernel(const __grid_constant__ PassArgs a) {
         // s = Z_k + conj Z_{N-k} (= 2 Va_k),  d = Z_k − conj Z_{N-k} (= 2i Vb_k)
         const C sk = {zk.x + zn.x, zk.y - zn.y}, dk = {zk.x - zn.x, zk.y + zn.y};
         const C ck = __ldg(tw3 + k);
-        // X^a_k = Re(c_k s), X^b_k = Re(c_k d / i) = Im(c_k d)
-        io.GIO<C>::store(k, C{ck.x * sk.x - ck.y * sk.y, ck.x * dk.y + ck.y * dk.x});
-        if (k > 0 && 2 * k != N) {  // the partner row N−k: s' = conj s, d' = −conj d
+        // X^a_k = Re(c_k s), X^b_k = Re(c_k d / i) = Im(c_k d)   (DST: row N-1-k)
+        const int rk = DST ? N - 1 - k : k;
+        io.GIO<C>::store(rk, dct_spec(a, rk, l0, l1, C{ck.x * sk.x - ck.y * sk.y, ck.x * dk.y + ck.y * dk.x}));
+        if (k > 0 && 2 * k != N) {  // the partner row N−k: s' = conj s, d' = −conj d   (DST: row k-1)
           const C cl = __ldg(tw3 + N - k);
           const C sl = {sk.x, -sk.y}, dl = {-dk.x, dk.y};
-          io.GIO<C>::store(N - k, C{cl.x * sl.x - cl.y * sl.y, cl.x * dl.y + cl.y * dl.x});
+          const int rl = DST ? k - 1 : N - k;
+          io.GIO<C>::store(rl, dct_spec(a, rl, l0, l1, C{cl.x * sl.x - cl.y * sl.y, cl.x * dl.y + cl.y * dl.x}));
         }
       }
     }
@@ -924,7 +971,9 @@ template <typename Real, int N> struct TmaCfg {
 // DCT (R2R strided stages on the TMA kernel, OM 1 only): -1 forward (permuted loads from the
 // stage; the (k, N−k) post-processing runs on the output tile before the TMA store), +1 inverse
 // (V from stage rows t and N−t in the loads, permuted rows in the stores).
+// DCT (R2R strided stages, OM 1 only): 0 = c2c; -1 / +1 = DCT-II / DCT-III; -2 / +2 = DST-II / DST-III
 template <typename C, int W, int OM, bool SPEC = false, int N_ = 0, int DCT = 0> struct TmaIO : GIO<C, false, SPEC> {
+  static constexpr bool DSTV = DCT == 2 || DCT == -2;
   static constexpr bool kSyncAfterLoad = true;
   static constexpr bool kRefillNoSync = false;
   static constexpr bool kLastBar = true;
@@ -941,11 +990,13 @@ template <typename C, int W, int OM, bool SPEC = false, int N_ = 0, int DCT = 0>
   const C* tw3 = nullptr;  // DCT: c_k = exp(DCT·iπk/(2N))
   __device__ __forceinline__ C load(int t) const {
     if constexpr (DCT < 0) {
-      return stage[dct_perm(t, N_) * W + c];
+      const int p = dct_perm(t, N_);
+      const C v = stage[p * W + c];
+      return (DSTV && (p & 1)) ? C{-v.x, -v.y} : v;
     } else if constexpr (DCT > 0) {
       using R = decltype(C{}.x);
-      const C xt = stage[t * W + c];
-      const C xl = t == 0 ? C{0, 0} : stage[(N_ - t) * W + c];
+      const C xt = stage[(DSTV ? N_ - 1 - t : t) * W + c];
+      const C xl = t == 0 ? C{0, 0} : stage[(DSTV ? t - 1 : N_ - t) * W + c];
       const C cc = __ldg(tw3 + t);
       const C da = {xt.x * R(0.5), -xl.x * R(0.5)}, db = {xt.y * R(0.5), -xl.y * R(0.5)};
       const C va = cmul(cc, da), vb = cmul(cc, db);
@@ -957,7 +1008,12 @@ template <typename C, int W, int OM, bool SPEC = false, int N_ = 0, int DCT = 0>
   __device__ __forceinline__ void store(int t, C v) const {
     if constexpr (OM != 0) {
       if (this->scale != 1) { v.x *= this->scale; v.y *= this->scale; }
-      obuf[(DCT > 0 ? dct_perm(t, N_) : t) * W + c] = this->apply_spec(t, v);
+      if constexpr (DCT > 0) {
+        const int p = dct_perm(t, N_);
+        obuf[p * W + c] = (DSTV && (p & 1)) ? C{-v.x, -v.y} : v;
+        return;
+      }
+      obuf[t * W + c] = this->apply_spec(t, v);
     } else {
       GIO<C, false, SPEC>::store(t, v);
     }
@@ -990,7 +1046,9 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
   constexpr bool TST = OM != 0;
   using C = typename CT<Real>::type;
   using Cfg = TmaCfg<Real, N>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 1024-byte aligned: TMA destinations need 128 B alignment, and a cluster launch does not
+  // otherwise guarantee it for the dynamic shared-memory base
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* stages = reinterpret_cast<C*>(smem_raw);
   C* work = stages + Cfg::NS * Cfg::STAGE_ELEMS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(work + Cfg::WORK_ELEMS);
@@ -1055,18 +1113,35 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
     stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, work, reinterpret_cast<const C*>(a.tw), j, active);
     if constexpr (DCT < 0) {  // forward R2R: finish the row pairs (k, N−k) of the output tile
+      constexpr bool DST = DCT == -2;
+      constexpr int NP = (N / 2 + Cfg::S.T) / Cfg::S.T;  // pairs per thread (upper bound)
       __syncthreads();
-      if (active) {
-        const C* tw3 = reinterpret_cast<const C*>(a.tw3);
-        for (int k = j; k <= N / 2; k += Cfg::S.T) {
+      const C* tw3 = reinterpret_cast<const C*>(a.tw3);
+      // all pairs are read before any is written: the DST's reversed rows cross pairs
+      C ok[NP], ol[NP];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const int k = j + q * Cfg::S.T;
+        if (active && k <= N / 2) {
           const C zk = work[k * Cfg::W + c], zn = work[(k == 0 ? 0 : N - k) * Cfg::W + c];
           const C sk = {zk.x + zn.x, zk.y - zn.y}, dk = {zk.x - zn.x, zk.y + zn.y};
           const C ck = __ldg(tw3 + k);
-          work[k * Cfg::W + c] = C{ck.x * sk.x - ck.y * sk.y, ck.x * dk.y + ck.y * dk.x};
+          ok[q] = C{ck.x * sk.x - ck.y * sk.y, ck.x * dk.y + ck.y * dk.x};
+          const C cl = __ldg(tw3 + (k == 0 ? 0 : N - k));
+          const C sl = {sk.x, -sk.y}, dl = {-dk.x, dk.y};
+          ol[q] = C{cl.x * sl.x - cl.y * sl.y, cl.x * dl.y + cl.y * dl.x};
+        }
+      }
+      if constexpr (DST) __syncthreads();
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        const int k = j + q * Cfg::S.T;
+        if (active && k <= N / 2) {
+          const int rk = DST ? N - 1 - k : k;
+          work[rk * Cfg::W + c] = dct_spec(a, rk, l0, l1, ok[q]);
           if (k > 0 && 2 * k != N) {
-            const C cl = __ldg(tw3 + N - k);
-            const C sl = {sk.x, -sk.y}, dl = {-dk.x, dk.y};
-            work[(N - k) * Cfg::W + c] = C{cl.x * sl.x - cl.y * sl.y, cl.x * dl.y + cl.y * dl.x};
+            const int rl = DST ? k - 1 : N - k;
+            work[rl * Cfg::W + c] = dct_spec(a, rl, l0, l1, ol[q]);
           }
         }
       }

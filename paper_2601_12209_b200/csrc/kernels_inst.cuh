@@ -17,18 +17,19 @@ KernelInfo make_contig() {
   k.twlen = sched_twlen(Cfg::S);
   return k;
 }
-template <typename Real, int N, int DIR>
+template <typename Real, int N, int DIR, bool DST = false>
 KernelInfo make_strided_dct() {
   using Cfg = StridedCfg<Real, N>;
   KernelInfo k;
-  k.fn = (const void*)&fft_strided_dct_kernel<Real, N, DIR>;
+  k.fn = (const void*)&fft_strided_dct_kernel<Real, N, DIR, DST>;
+  k.spec_fn = k.fn;  // the DCT / DST kernels apply the Poisson multiplier at run time (dct_spec)
   k.threads = Cfg::THREADS;
   k.per_cta = Cfg::W;
   k.smem = (size_t)Cfg::SMEM_ELEMS * sizeof(Real) * 2;
   k.twlen = sched_twlen(Cfg::S);
   using TC = TmaCfg<Real, N>;
   if constexpr (TC::OK) {  // TMA-staged variant, TMA stores only (unsegmented outputs)
-    k.tma_fn = k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, false, DIR>;
+    k.tma_fn = k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, false, DST ? 2 * DIR : DIR>;
     k.tma_st_only = true;
     k.tma_threads = TC::THREADS;
     k.tma_w = TC::W;
@@ -72,6 +73,8 @@ bool DFFT_LOOKUP(int family, int n, int dir, KernelInfo* out) {
     else if (family == kContigC2R) *out = make_contig<DFFT_REAL, N, 1, 2>();                   \
     else if (family == kContigDct) *out = dir < 0 ? make_contig<DFFT_REAL, N, -1, 3>() : make_contig<DFFT_REAL, N, 1, 4>(); \
     else if (family == kStridedDct) *out = dir < 0 ? make_strided_dct<DFFT_REAL, N, -1>() : make_strided_dct<DFFT_REAL, N, 1>(); \
+    else if (family == kContigDst) *out = dir < 0 ? make_contig<DFFT_REAL, N, -1, 5>() : make_contig<DFFT_REAL, N, 1, 6>(); \
+    else if (family == kStridedDst) *out = dir < 0 ? make_strided_dct<DFFT_REAL, N, -1, true>() : make_strided_dct<DFFT_REAL, N, 1, true>(); \
     else *out = dir < 0 ? make_strided<DFFT_REAL, N, -1>() : make_strided<DFFT_REAL, N, 1>();    \
     return true;
   switch (n) {

@@ -8,7 +8,9 @@
 
 namespace dfft {
 
-enum Family { kContig = 0, kStrided = 1, kContigR2C = 2, kContigC2R = 3, kContigDct = 4, kStridedDct = 5 };
+enum Family {
+  kContig = 0, kStrided = 1, kContigR2C = 2, kContigC2R = 3, kContigDct = 4, kStridedDct = 5, kContigDst = 6, kStridedDst = 7
+};
 
 struct KernelInfo {
   const void* fn = nullptr;
