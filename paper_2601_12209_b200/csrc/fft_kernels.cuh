@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(ContigCfg<N>::THREADS)
 fft_contig_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
   using Cfg = ContigCfg<N>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int li = threadIdx.x / Cfg::S.T;
   const int j = threadIdx.x % Cfg::S.T;
@@ -756,7 +756,7 @@ __global__ void __launch_bounds__(StridedCfg<Real, N>::THREADS)
 fft_strided_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
   using Cfg = StridedCfg<Real, N>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int c = threadIdx.x % Cfg::W;
   const int j = threadIdx.x / Cfg::W;
@@ -824,7 +824,7 @@ fft_strided_dct_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
   using R = Real;
   using Cfg = StridedCfg<Real, N>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   C* tile = smem;  // dense [t][W] (forward): aliases the pass buffer (the last pass reads it first)
   const int c = threadIdx.x % Cfg::W;

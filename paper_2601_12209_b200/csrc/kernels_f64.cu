@@ -1,3 +1,4 @@
 #define DFFT_REAL double
 #define DFFT_LOOKUP lookup_kernel_f64
+#define DFFT_LOOKUP_FUSED lookup_fused_xy_f64
 #include "kernels_inst.cuh"
