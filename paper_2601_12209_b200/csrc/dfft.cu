@@ -269,12 +269,6 @@ struct Stage {
   int sm_cap = 0;          // > 0: run the persistent variant on at most this many SMs (leaves the
                            // rest to a concurrently running HBM-bound stage)
   int tma_variant = 0;     // 1 = the persistent TMA kernel is used
-  // fused x+y pass (fused_xy.cuh; single-GPU c2c, nx == ny): `in` = the z-pass output [y][z][x],
-  // `out` = natural; scratch planes and counters in the workspace
-  bool xy = false;
-  FusedInfo xyk;
-  long long xy_nz = 0, xy_scratch = 0, xy_ctr = 0;  // planes; byte offsets in the workspace
-  int xy_slots = 0, xy_grid = 0, xy_nx = 0;
   const void* tw_tma = nullptr;  // twiddles of the TMA variant's radix schedule
   bool empty = false;
   // last forward stage: which global axis (0 x, 1 y, 2 z) its t / l0 / l1 run along and the
@@ -361,7 +355,6 @@ struct dfft_plan_s {
   bool f64 = false, r2c = false, overlap = true;
   bool r2r = false;  // real x axis transformed by a DCT / DST (reading R21, R22)
   int kind[3] = {0, 0, 0};  // per-axis transform kind (DFFT_KIND_*): DFT, DCT-II, DST-II
-  bool no_fused = false;    // set_poisson on a 1-GPU c2c cube: rebuilt without the fused XY pass
   size_t es = 8;  // complex element bytes
   std::vector<RankPlan> ranks;
   ncclComm_t row = nullptr, col = nullptr;
@@ -1034,69 +1027,7 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
 //            y (ws -> out, natural -> natural)
 //   inverse: y (in -> out, natural), z (natural -> ws as [y][z][x]: the large-pitch read),
 //            x (ws -> out, natural, ×1/N)
-// Single GPU, c2c, nx == ny with a fused XY kernel: two passes over HBM instead of three
-// (DESIGN.md §5): A = z-pass (natural -> ws [y][z][x], the large-pitch side on its loads),
-// B = fused x+y pass (ws -> natural `out`, planes through an L2-resident scratch ring; ×1/N on
-// the inverse).  Both directions have the same shape (the 3D DFT is separable).
-bool fused_ok(dfft_plan_t pl, const Geo& g, FusedInfo* fk) {
-  if (pl->r2c || pl->r2r || g.nx != g.ny || !getenv("DFFT_FUSED_XY") || !g_use_tma || !tensor_map_encoder() ||
-      pl->no_fused)
-    return false;
-  const bool ok = pl->f64 ? lookup_fused_xy_f64((int)g.nx, pl->dir, fk) : lookup_fused_xy_f32((int)g.nx, pl->dir, fk);
-  return ok && fk->fn && g.nz >= 2;
-}
-
-dfft_status_t build_single_fused(dfft_plan_t pl, const Geo& g, RankPlan& rp, const FusedInfo& fk) {
-  const long long n = g.nx, nz = g.nz, es = (long long)pl->es;
-  const long long Wel = n * n * nz;  // elements of the [y][z][x] intermediate
-  rp.A.resize(1);
-  rp.B.resize(1);
-  rp.E1.resize(1);
-  rp.E2.resize(1);
-  Stage &A = rp.A[0], &B = rp.B[0];
-  rp.C = Stage{};
-  rp.C.empty = true;  // two passes
-  // A: z-pass, columns (l0 = x, l1 = y): natural `in` -> ws [y][z][x]
-  A.in = {kUserIn, 0};
-  set_side(A.a.in, n * n, 1, n);
-  A.out = {kWs, 0};
-  set_side(A.a.out, n, 1, nz * n);
-  A.a.scale = 1.0;
-  ST(finish_stage(pl, A, fam_z(pl), (int)nz, n, n, nullptr, nullptr));
-  // B: fused x+y over the nz planes of ws -> `out` (natural); 4 scratch planes + counters
-  B.xy = true;
-  B.xyk = fk;
-  B.n = (int)n;
-  B.es = (int)es;
-  B.family = kStrided;
-  B.in = {kWs, 0};
-  B.out = {kUserOut, 0};
-  B.a.L0 = n;  // stage_bytes: read + write of n * n * nz elements
-  B.a.L1 = nz;
-  B.a.scale = pl->dir == DFFT_INVERSE ? 1.0 / ((double)n * (double)n * (double)nz) : 1.0;
-  B.xy_nz = nz;
-  B.xy_slots = (int)std::min<long long>(nz, getenv("DFFT_XY_SLOTS") ? atoi(getenv("DFFT_XY_SLOTS")) : 4);
-  B.xy_scratch = ((Wel * es + 1023) / 1024) * 1024;
-  B.xy_ctr = B.xy_scratch + (long long)B.xy_slots * n * n * es;
-  ST(get_twiddles((int)n, pl->f64, pl->dir, pl->comm->device, &B.tw_tma, fk.maxr));
-  CU(cudaFuncSetAttribute(fk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fk.smem));
-  int occ = 0, sms = 0;
-  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fk.fn, fk.threads, fk.smem));
-  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, pl->comm->device));
-  if (occ < 1) return fail(DFFT_ERR_INTERNAL, "fused XY kernel does not fit on an SM");
-  B.xy_grid = sms * occ;
-  const char* xf = getenv("DFFT_XY_XPCT");  // percent of the CTAs running x items (default 50)
-  B.xy_nx = std::max(1, std::min(B.xy_grid - 1, B.xy_grid * (xf ? atoi(xf) : 50) / 100));
-  B.last_fwd = false;
-  rp.ws_bytes = (size_t)(B.xy_ctr + 2 * nz * 4 + 16);
-  return DFFT_SUCCESS;
-}
-
 dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
-  {
-    FusedInfo fk;
-    if (fused_ok(pl, g, &fk)) return build_single_fused(pl, g, rp, fk);
-  }
   const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
   const long long nxl = xreal(pl) ? nx / 2 : nx;
   const long long W = nxc * ny * nz;
@@ -1345,60 +1276,8 @@ dfft_status_t launch(const Stage& s, const Ctx& c, cudaStream_t st) {
   return r;
 }
 
-dfft_status_t launch_xy(const Stage& s, const Ctx& c, cudaStream_t st) {
-  char* ws = (char*)c.ws;
-  void* in = resolve(s.in, c);
-  void* out = resolve(s.out, c);
-  void* scratch = ws + s.xy_scratch;
-  unsigned int* ctr = reinterpret_cast<unsigned int*>(ws + s.xy_ctr);
-  const long long n = s.n, nz = s.xy_nz;
-  CU(cudaMemsetAsync(ctr, 0, (size_t)(2 * nz * 4 + 16), st));
-  const bool f64 = s.es == 16;
-  const cuuint64_t esz = f64 ? 8 : 4, ces = 2 * esz, CH = 256 / esz;  // reals per 256 B chunk
-  const CUtensorMapDataType dt = f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  auto enc = [&](CUtensorMap* tm, void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-                 const cuuint32_t* box) {
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    return tensor_map_encoder()(tm, dt, rank, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                CU_TENSOR_MAP_SWIZZLE_NONE, g_tma_promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-  };
-  CUtensorMap xin, xsc, ysc, yout;
-  const cuuint64_t nch = 2 * (cuuint64_t)n / CH;
-  // X loads: [y][z][x] lines as (reals in a 256 B chunk, chunks, y (pitch nz·n), z (pitch n))
-  const cuuint64_t d_xin[4] = {CH, nch, (cuuint64_t)n, (cuuint64_t)nz};
-  const cuuint64_t s_xin[3] = {256, (cuuint64_t)(nz * n) * ces, (cuuint64_t)n * ces};
-  const cuuint32_t b_x[4] = {(cuuint32_t)CH, (cuuint32_t)nch, (cuuint32_t)s.xyk.w, 1};
-  // X stores / Y loads: scratch planes [slot][y][x]
-  const cuuint64_t d_xsc[4] = {CH, nch, (cuuint64_t)n, (cuuint64_t)s.xy_slots};
-  const cuuint64_t s_xsc[3] = {256, (cuuint64_t)n * ces, (cuuint64_t)(n * n) * ces};
-  const cuuint64_t d_ysc[3] = {2 * (cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)s.xy_slots};
-  const cuuint64_t s_ysc[2] = {(cuuint64_t)n * ces, (cuuint64_t)(n * n) * ces};
-  const cuuint32_t b_y[3] = {(cuuint32_t)(2 * s.xyk.w), (cuuint32_t)s.xyk.boxr, 1};
-  // Y stores: natural `out` [z][y][x]
-  const cuuint64_t d_yout[3] = {2 * (cuuint64_t)n, (cuuint64_t)n, (cuuint64_t)nz};
-  if (!enc(&xin, in, 4, d_xin, s_xin, b_x) || !enc(&xsc, scratch, 4, d_xsc, s_xsc, b_x) ||
-      !enc(&ysc, scratch, 3, d_ysc, s_ysc, b_y) || !enc(&yout, out, 3, d_yout, s_ysc, b_y))
-    return fail(DFFT_ERR_INTERNAL, "fused XY: tensor map encoding failed");
-  XYArgs a{};
-  a.tw = s.tw_tma;
-  a.nplanes = nz;
-  a.tpp = (int)(n / s.xyk.w);
-  a.nslots = s.xy_slots;
-  a.nx_ctas = s.xy_nx;
-  a.done_x = ctr;
-  a.done_y = ctr + nz;
-  a.tickets = reinterpret_cast<unsigned long long*>(ws + s.xy_ctr + ((2 * nz * 4 + 7) / 8) * 8);
-  a.scale = s.a.scale;
-  a.nodep = getenv("DFFT_XY_NODEP") ? 1 : 0;
-  void* args[] = {&xin, &xsc, &ysc, &yout, &a};
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  CU(cudaLaunchCooperativeKernel(s.xyk.fn, dim3((unsigned)s.xy_grid), dim3(s.xyk.threads), args, s.xyk.smem, st));
-  return DFFT_SUCCESS;
-}
-
 dfft_status_t launch_impl(const Stage& s, const Ctx& c, cudaStream_t st) {
   if (s.empty) return DFFT_SUCCESS;
-  if (s.xy) return launch_xy(s, c, st);
   g_launches.fetch_add(1, std::memory_order_relaxed);  // exactly one kernel per stage launch
   PassArgs a = s.a;
   a.in.base = resolve(s.in, c);
@@ -2782,28 +2661,6 @@ dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double
     return fail(DFFT_ERR_INVALID_VALUE, "grid spacings must all be > 0 (or all 0 to switch the multiplier off)");
   CU(cudaSetDevice(pl->comm->device));
   CU(cudaDeviceSynchronize());  // no execute of this plan may be reading the old tables
-  if (on && !pl->no_fused) {
-    // the fused XY pass has no spectral epilogue: rebuild a single-GPU cube plan as three passes
-    bool fused = false;
-    for (RankPlan& rp : pl->ranks)
-      for (Stage& b : rp.B) fused = fused || b.xy;
-    if (fused) {
-      pl->no_fused = true;
-      RankPlan& rp = pl->ranks[0];
-      for (Stage& st : rp.A) free_stage(st);
-      for (Stage& st : rp.B) free_stage(st);
-      free_stage(rp.C);
-      rp.A.clear();
-      rp.B.clear();
-      rp.C = Stage{};
-      if (rp.ws) cudaFree(rp.ws);
-      rp.ws = nullptr;
-      Geo g{pl->nx, pl->ny, pl->nz, pl->nx, 1, 1, 1};
-      ST(build_single(pl, g, rp));
-      build_schedule(pl, rp);
-      if (rp.ws_bytes) CU(cudaMalloc(&rp.ws, rp.ws_bytes));
-    }
-  }
   if (pl->spec_tab) cudaFree(pl->spec_tab);
   pl->spec_tab = nullptr;
   const long long n[3] = {pl->nx, pl->ny, pl->nz};

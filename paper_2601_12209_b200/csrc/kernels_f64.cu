@@ -1,4 +1,3 @@
 #define DFFT_REAL double
 #define DFFT_LOOKUP lookup_kernel_f64
-#define DFFT_LOOKUP_FUSED lookup_fused_xy_f64
 #include "kernels_inst.cuh"

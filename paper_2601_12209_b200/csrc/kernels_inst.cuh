@@ -1,6 +1,5 @@
 // kernels_inst.cuh — instantiation + registration of the FFT kernels for one precision.
 // Included by kernels_f32.cu / kernels_f64.cu with DFFT_REAL and DFFT_LOOKUP defined.
-#include "fused_xy.cuh"
 #include "registry.h"
 
 namespace dfft {
@@ -64,35 +63,7 @@ KernelInfo make_strided() {
   }
   return k;
 }
-template <typename Real, int N, int DIR>
-FusedInfo make_fused() {
-  FusedInfo f;
-  if constexpr (XYCfg<Real, N>::OK) {
-    using TC = TmaCfg<Real, N>;
-    f.fn = (const void*)&fft_xy_fused_kernel<Real, N, DIR>;
-    f.threads = TC::THREADS;
-    f.w = TC::W;  // (one in-place tile buffer per CTA: XYCfg::SMEM)
-    f.boxr = TC::BOXR;
-    f.nbox = TC::NBOX;
-    f.maxr = TC::MAXR;
-    f.smem = XYCfg<Real, N>::SMEM;
-  }
-  return f;
-}
 }  // namespace
-
-bool DFFT_LOOKUP_FUSED(int n, int dir, FusedInfo* out) {
-  switch (n) {
-#define DFFT_FCASE(N)                                                                   \
-  case N:                                                                               \
-    *out = dir < 0 ? make_fused<DFFT_REAL, N, -1>() : make_fused<DFFT_REAL, N, 1>();   \
-    return out->fn != nullptr;
-    DFFT_FCASE(256) DFFT_FCASE(512) DFFT_FCASE(1024)
-#undef DFFT_FCASE
-    default:
-      return false;
-  }
-}
 
 bool DFFT_LOOKUP(int family, int n, int dir, KernelInfo* out) {
 #define DFFT_CASE(N)                                                                             \

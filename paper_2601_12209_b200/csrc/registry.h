@@ -5,7 +5,6 @@
 #include <stddef.h>
 
 #include "fft_kernels.cuh"
-#include "fused_xy.cuh"
 
 namespace dfft {
 
@@ -38,16 +37,7 @@ struct KernelInfo {
   X(3) X(6) X(12) X(24) X(48) X(96) X(192) X(384) X(768) X(1536) X(3072) \
   X(5) X(7) X(480) X(720) X(840)
 
-// fused x+y pass of the single-GPU c2c plan (fused_xy.cuh), for nx == ny == n
-struct FusedInfo {
-  const void* fn = nullptr;
-  int threads = 0, w = 0, boxr = 0, nbox = 0, maxr = 16;
-  size_t smem = 0;
-};
-
 bool lookup_kernel_f32(int family, int n, int dir, KernelInfo* out);
-bool lookup_fused_xy_f32(int n, int dir, FusedInfo* out);
-bool lookup_fused_xy_f64(int n, int dir, FusedInfo* out);
 bool lookup_kernel_f64(int family, int n, int dir, KernelInfo* out);
 bool length_supported(long long n);
 // radix schedule of length n (for twiddle generation): returns npass, fills rad[]

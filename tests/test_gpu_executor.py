@@ -272,34 +272,3 @@ def test_execute_host_and_chain(oracle_mod):
         assert oracle_mod.rel_l2(z.numpy(), x.numpy()) <= GATE["f64"]
     with pytest.raises(dfft.DfftError):  # asynchronous calls need pinned host memory
         dfft.execute_host_chain([fwd, inv], np.ascontiguousarray(a), np.empty_like(a), async_=True)
-
-
-# ------------------------------------------------------------------------------ fused XY (1 GPU, c2c, nx == ny)
-@pytest.mark.parametrize("shape,prec", [((256, 256, 64), "f32"), ((256, 256, 256), "f64"), ((512, 512, 32), "f32"),
-                                        ((1024, 1024, 16), "f32"), ((1024, 1024, 8), "f64"), ((256, 256, 2), "f32")])
-def test_fused_xy_plan_elementwise(oracle_mod, shape, prec, monkeypatch):
-    monkeypatch.setenv("DFFT_FUSED_XY", "1")
-    """The single-GPU c2c plan with nx == ny runs a z-pass and one fused x+y pass whose plane
-    intermediate cycles through an L2 scratch ring (csrc/fused_xy.cuh): forward and inverse alone
-    element-wise vs the oracle (P:90-96), in the launch configuration the 1024^3 bench uses."""
-    ef, ei = _single(oracle_mod, shape, prec, seed=37)
-    assert ef <= GATE[prec] and ei <= GATE[prec], (ef, ei)
-    assert ef <= QUALITY[prec] and ei <= QUALITY[prec], (ef, ei)
-
-
-def test_fused_xy_poisson_rebuilds(oracle_mod, monkeypatch):
-    monkeypatch.setenv("DFFT_FUSED_XY", "1")
-    # the fused pass has no spectral epilogue: set_poisson rebuilds the plan as three passes
-    shape = (256, 256, 32)
-    comm = dfft.Comm.create(nranks=1, rank=0, device=0)
-    fwd = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_f64", dfft.FORWARD).set_poisson((1.0, 0.5, 2.0))
-    inv = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_f64", dfft.INVERSE)
-    x = fwd.alloc_in()
-    inputs.fill_box_cuda(x, 5, shape, (0, 0, 0), shape, True)
-    y, z = fwd.alloc_out(), inv.alloc_out()
-    fwd.execute(x, y)
-    inv.execute(y, z)
-    torch.cuda.synchronize()
-    a = oracle_mod.gen_complex(5, shape)
-    ref = oracle_mod.poisson3d(a.real.copy(), (1.0, 0.5, 2.0)) + 1j * oracle_mod.poisson3d(a.imag.copy(), (1.0, 0.5, 2.0))
-    assert oracle_mod.rel_l2(z.cpu().numpy(), ref) <= 1e-12
