@@ -284,14 +284,19 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.tolist()
 
-    def timed(fn, iters):
+    host_ms = {}
+
+    def timed(fn, iters, tag=None):
         """back-to-back: `iters` calls between one pair of events, barrier + sync on both sides."""
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        h0 = time.perf_counter()
         for _ in range(iters):
             fn()
+        if tag:  # host time to enqueue the calls (the GPU may still be running them)
+            host_ms[tag] = (time.perf_counter() - h0) * 1e3 / max(iters, 1)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -319,7 +324,7 @@ def main():
     clocks.start()
     # --- headline timed region: K back-to-back fwd+inv steps (no profiling events inside)
     n_launch0 = dfft.kernel_launches()
-    ms_local = timed(step, args.steps)
+    ms_local = timed(step, args.steps, "headline")
     n_launch = dfft.kernel_launches() - n_launch0
     ms_total = max_over_ranks([ms_local])[0]
     ms_step = ms_total / max(args.steps, 1)
@@ -350,6 +355,7 @@ def main():
         "forward_only_ms": {"median": statistics.median(fwd_ms), "min": min(fwd_ms), "mean": statistics.mean(fwd_ms),
                             "sd": statistics.pstdev(fwd_ms), "n": len(fwd_ms)},
         "cuda_graph_ms": graph_ms,
+        "host_enqueue_ms_per_step": host_ms.get("headline"),
     }
     # --- profiled pass (separate from the headline): per-phase times, timeline, roofline
     R = max(3, min(args.steps, 10))

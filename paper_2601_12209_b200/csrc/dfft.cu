@@ -373,6 +373,15 @@ struct dfft_plan_s {
     unsigned long long calls = 0;
   };
   HostChain* host = nullptr;
+  // executes replay a CUDA graph of the schedule, captured once per (in, out) pair on a private
+  // stream (DFFT_NO_GRAPH=1: issue the schedule directly every time); invalidated by set_poisson
+  struct GraphEntry {
+    const void* in;
+    void* out;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t cap_stream = nullptr;
   // P2P exchange (default for P > 1): every rank's workspace is an IPC window; the FFT epilogues
   // store straight into the peers' receive regions over NVLink; flags in the windows order it
   bool p2p = false;
@@ -1783,7 +1792,7 @@ dfft_status_t join_rank(dfft_plan_t pl, RankPlan& rp, cudaStream_t user) {
   return DFFT_SUCCESS;
 }
 
-dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream_t user) {
+dfft_status_t issue_rank(dfft_plan_t pl, const void* in, void* out, cudaStream_t user) {
   RankPlan& rp = pl->ranks[0];
   RunCtx rc{Ctx{in, out, rp.ws, pl->peer_ws.empty() ? nullptr : pl->peer_ws.data()}, {user, user}, 0};
   ST(prof_origin(pl, user, &rc.exec));
@@ -1792,6 +1801,53 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
   for (size_t pos = 0; pos < rp.sched.size(); ++pos) run.step(rp, pos, rc);
   ST(join_rank(pl, rp, user));
   return run.finish();
+}
+
+void drop_graphs(dfft_plan_t pl) {
+  for (auto& g : pl->graphs) cudaGraphExecDestroy(g.exec);
+  pl->graphs.clear();
+}
+
+// Replay the schedule as a CUDA graph: one launch instead of every kernel, flag wait and
+// cross-stream event of the execute (N=4 1024^3: 8.5 -> 7.9 ms fwd+inv).  Captured on the plan's
+// private stream the first time a (in, out) pair is executed; not while profiling (the phase
+// events must be live) or while the caller's stream is itself being captured (the schedule then
+// goes into the caller's graph).
+dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream_t user) {
+  static const bool no_graph = getenv("DFFT_NO_GRAPH") != nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CU(cudaStreamIsCapturing(user, &cs));
+  if (no_graph || pl->prof || cs != cudaStreamCaptureStatusNone) return issue_rank(pl, in, out, user);
+  for (size_t q = 0; q < pl->graphs.size(); ++q)
+    if (pl->graphs[q].in == in && pl->graphs[q].out == out) {
+      CU(cudaGraphLaunch(pl->graphs[q].exec, user));
+      return DFFT_SUCCESS;
+    }
+  if (!pl->cap_stream) CU(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
+  CU(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const dfft_status_t st = issue_rank(pl, in, out, pl->cap_stream);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(pl->cap_stream, &graph);
+  if (st != DFFT_SUCCESS || ec != cudaSuccess || !graph) {  // capture failed: issue directly
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    if (st != DFFT_SUCCESS) return st;
+    return issue_rank(pl, in, out, user);
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {
+    (void)cudaGetLastError();
+    return issue_rank(pl, in, out, user);
+  }
+  if (pl->graphs.size() >= 4) {  // a few (in, out) pairs: the host chain alternates two
+    cudaGraphExecDestroy(pl->graphs.front().exec);
+    pl->graphs.erase(pl->graphs.begin());
+  }
+  pl->graphs.push_back({in, out, exec});
+  CU(cudaGraphLaunch(exec, user));
+  return DFFT_SUCCESS;
 }
 
 // simulated ranks, NCCL layouts: rank r's send to peer q is matched with q's receive from r
@@ -1967,7 +2023,8 @@ void Watchdog::loop() {
 // register an execute (event recorded on the caller's stream after the join); not while the
 // stream is being captured into a graph (the execute happens at replay)
 dfft_status_t wd_track(dfft_plan_t pl, cudaStream_t user) {
-  if ((size_t)pl->P1 * pl->P2 <= 1) return DFFT_SUCCESS;
+  static const bool off = getenv("DFFT_NO_WATCHDOG") != nullptr;  // A/B switch
+  if ((size_t)pl->P1 * pl->P2 <= 1 || off) return DFFT_SUCCESS;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   CU(cudaStreamIsCapturing(user, &cs));
   if (cs != cudaStreamCaptureStatusNone) return DFFT_SUCCESS;
@@ -2055,6 +2112,9 @@ void free_plan(dfft_plan_t pl) {
   if (!pl) return;
   wd_forget(pl);
   wait_peers_done(pl);
+  if (pl->cap_stream) cudaStreamSynchronize(pl->cap_stream);
+  drop_graphs(pl);
+  if (pl->cap_stream) cudaStreamDestroy(pl->cap_stream);
   for (RankPlan& rp : pl->ranks) {
     if (rp.sX) cudaStreamSynchronize(rp.sX);
     if (rp.sY) cudaStreamSynchronize(rp.sY);
@@ -2661,6 +2721,7 @@ dfft_status_t dfft_plan_set_poisson(dfft_plan_t pl, double dx, double dy, double
     return fail(DFFT_ERR_INVALID_VALUE, "grid spacings must all be > 0 (or all 0 to switch the multiplier off)");
   CU(cudaSetDevice(pl->comm->device));
   CU(cudaDeviceSynchronize());  // no execute of this plan may be reading the old tables
+  drop_graphs(pl);  // the captured kernels carry the old multiplier tables
   if (pl->spec_tab) cudaFree(pl->spec_tab);
   pl->spec_tab = nullptr;
   const long long n[3] = {pl->nx, pl->ny, pl->nz};
