@@ -416,6 +416,13 @@ def main():
             tr = traffic_tab.get(f"{tag}_{ph}")
             ent.update({"kernel": f"{tag} {stage_names[tag][ph]}", "avg_launch_ms": avg, "ms_per_step": ms / R,
                         "traffic": tr / launches if tr is not None and ent["bound"] == "hbm" else None})
+            # pipelined plans run a stage beside another (on an SM cap): the share of its time it
+            # shared the GPU, from the timeline of the profiled pass
+            spans = tf if tag == "fwd" else ti
+            mine = [(x["t0_ms"] + 1e3 * x["exec"], x["t1_ms"] + 1e3 * x["exec"]) for x in spans if x["phase"] == ph]
+            other = [(x["t0_ms"] + 1e3 * x["exec"], x["t1_ms"] + 1e3 * x["exec"]) for x in spans if x["phase"] != ph]
+            if mine and other:
+                ent["concurrent_frac"] = _intersect_len(mine, other) / max(_union(mine), 1e-12)
             stages.append(ent)
     dom = max(stages, key=lambda e: e["ms_per_step"])
     roofline = {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel", "peak_kind",
