@@ -146,9 +146,11 @@ dfft_status_t dfft_comm_init_sim(dfft_comm_t* comm, int nranks, int cuda_device)
 dfft_status_t dfft_comm_destroy(dfft_comm_t comm);
 
 /* ------------------------------------------------------------------ plans
- * Supported FFT axis lengths (each of nx — nx/2 for R2C / R2R — ny, nz): 2^a for 2 ≤ 2^a ≤ 4096,
- * 3·2^a for 3 ≤ 3·2^a ≤ 3072, 5, 7, and the paper's GPU shapes 480, 720, 840; any other
- * length returns DFFT_ERR_UNSUPPORTED.
+ * Supported FFT axis lengths: every n = 2^a 3^b 5^c 7^d <= 4096.  Specialised kernels (persistent
+ * TMA strided kernel, fused pack epilogues, R2C / C2R / DCT / DST variants) exist for 2^a (2..4096),
+ * 3·2^a (3..3072), 5, 7 and the paper's GPU shapes 480, 720, 840; other lengths run a
+ * generic kernel with the radix schedule at run time (c2c axes only: an R2C / R2R x axis — nx/2 —
+ * and DCT / DST axes need a specialised length).  Anything else returns DFFT_ERR_UNSUPPORTED.
  * Collective over comm (every rank calls it with the same arguments).  Builds the stage
  * geometry, twiddle tables, per-stage address tables, work buffers, sub-communicators
  * (row = ranks with the same j, column = same i), streams and events once; execution

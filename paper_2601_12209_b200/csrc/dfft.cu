@@ -520,7 +520,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   if (s.in_bases.size() > (size_t)kMaxBases || s.out_bases.size() > (size_t)kMaxBases)
     return fail(DFFT_ERR_UNSUPPORTED, "more than %d segment bases", kMaxBases);
   if (in_segs && linearize(*in_segs, n, s.in, s.in_bases, s.a.in, (long long)pl->es)) in_segs = nullptr;
-  if (in_segs && family == kContig && !getenv("DFFT_NO_TBLOCK") &&
+  if (in_segs && family == kContig && !getenv("DFFT_NO_TBLOCK") && length_specialised(n) &&
       linearize_tblocked(*in_segs, s.in, s.in_bases, s.a.in, (long long)pl->es))
     in_segs = nullptr;
   if (out_segs && linearize(*out_segs, n, s.out, s.out_bases, s.a.out, (long long)pl->es)) out_segs = nullptr;
@@ -542,6 +542,10 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
   }
   ST(get_kernel(family, n, pl->f64, pl->dir, &s.k));
   ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw));
+  if (s.k.generic) {  // the radix schedule at run time
+    s.a.gen = make_sched(n);
+    s.a.gen_per = s.k.per_cta;
+  }
   const bool contig_r2r = family == kContigDct || family == kContigDst;
   if (family == kContigR2C || family == kContigC2R || contig_r2r)
     ST(get_split_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw2));
@@ -2294,8 +2298,15 @@ static dfft_status_t validate(int P, int64_t nx, int64_t ny, int64_t nz, dfft_de
   long long nxc = r2c ? nx / 2 + 1 : r2r ? nx / 2 : nx;
   long long nfft_x = (r2c || r2r) ? nx / 2 : nx;
   if (!length_ok(nfft_x) || !length_ok(ny) || !length_ok(nz))
-    return fail(DFFT_ERR_UNSUPPORTED, "axis FFT lengths (%lld,%lld,%lld): each must be one of the supported lengths "
-                "(include/dfft.h)", (long long)nfft_x, (long long)ny, (long long)nz);
+    return fail(DFFT_ERR_UNSUPPORTED, "axis FFT lengths (%lld,%lld,%lld): each must be 2^a 3^b 5^c 7^d <= 4096",
+                (long long)nfft_x, (long long)ny, (long long)nz);
+  {  // R2C / R2R x axes and DCT / DST y, z axes run specialised kernels only
+    const bool xs_need = r2c || r2r;
+    const bool y_need = r2r || (kinds && kinds[1] != DFFT_KIND_DFT), z_need = r2r || (kinds && kinds[2] != DFFT_KIND_DFT);
+    if ((xs_need && !length_specialised(nfft_x)) || (y_need && !length_specialised(ny)) ||
+        (z_need && !length_specialised(nz)))
+      return fail(DFFT_ERR_UNSUPPORTED, "R2C / R2R / DCT / DST axes need one of the specialised lengths (include/dfft.h)");
+  }
   if (p1 > ny || p1 > nxc || p2 > nz || p2 > ny)
     return fail(DFFT_ERR_INFEASIBLE_DECOMP, "grid %d x %d leaves an empty block for (%lld,%lld,%lld)", p1, p2,
                 (long long)nx, (long long)ny, (long long)nz);
@@ -2862,6 +2873,10 @@ dfft_status_t dfft_fft1d(const void* in, void* out, int64_t n, int64_t howmany, 
   Stage s;
   ST(get_kernel(kContig, (int)n, f64 != 0, sign, &s.k));
   ST(get_twiddles((int)n, f64 != 0, sign, dev, &s.a.tw));
+  if (s.k.generic) {
+    s.a.gen = make_sched((int)n);
+    s.a.gen_per = s.k.per_cta;
+  }
   s.a.in.base = const_cast<void*>(in);
   s.a.out.base = out;
   set_side(s.a.in, 1, n, 0);
@@ -2879,9 +2894,22 @@ dfft_status_t dfft_fft1d(const void* in, void* out, int64_t n, int64_t howmany, 
 
 // ------------------------------------------------------------------------------ registry helpers
 namespace dfft {
+bool length_specialised(long long n) {
+  switch (n) {
+#define DFFT_LCASE(N) case N:
+    DFFT_LENGTHS(DFFT_LCASE)
+#undef DFFT_LCASE
+    return true;
+    default:
+      return false;
+  }
+}
 bool length_supported(long long n) {
-  KernelInfo k;
-  return n > 0 && n <= 4096 && lookup_kernel_f32(kContig, (int)n, -1, &k);
+  if (n <= 0 || n > 4096) return false;
+  long long m = n;
+  for (long long p : {2, 3, 5, 7})
+    while (m % p == 0) m /= p;
+  return m == 1;
 }
 int length_schedule(int n, int rad[kMaxPass], int maxr) {
   Sched s = make_sched(n, maxr);

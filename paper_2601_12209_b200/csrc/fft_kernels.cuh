@@ -374,6 +374,10 @@ struct PassArgs {
   // order whose consecutive lines are adjacent on the output side: scattered 8 KB writes cost more
   // than scattered 8 KB reads)
   int lorder;
+  // generic kernels (lengths without a specialised instantiation): the radix schedule at run time
+  // and the lines (contig) / columns (strided) per CTA
+  Sched gen;
+  int gen_per;
 };
 
 // tile -> (column tile tx, line l1) under the grouped order above
@@ -1168,6 +1172,124 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     }
   }
   if (TST && threadIdx.x == 0) bulk_wait0();
+}
+
+// ------------------------------------------------------------------ generic lengths
+// Any 2^a 3^b 5^c 7^d length without a specialised instantiation: the same Stockham passes with the
+// radix schedule read at run time (PassArgs::gen, make_sched), each pass dispatched to its
+// compile-time butterfly, ping-pong through shared memory (one barrier per pass).  CONTIG: gen_per
+// lines per CTA (t unit stride on the global side); strided: gen_per columns per CTA.
+template <typename C, int DIR, int R, bool FIRST, bool LAST, class IO, class IDX>
+__device__ __forceinline__ void gen_pass(IO& io, const IDX& idx, const C* src, C* dst, const C* tw, int n, int Ns,
+                                         int j, int TP, bool active) {
+  const int NR = n / R;
+  for (int b = j; b < NR; b += TP) {
+    C v[R];
+    const int m = b % Ns;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if constexpr (FIRST) v[r] = active ? io.load(b + r * NR) : C{0, 0};
+      else v[r] = src[idx(b + r * NR)];
+    }
+    if constexpr (!FIRST) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + (r - 1) * Ns + m));
+    }
+    dft<DIR, R>(v);
+    const int d = (b / Ns) * Ns * R + m;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if constexpr (LAST) {
+        if (active) io.store(d + r * Ns, v[r]);
+      } else {
+        dst[idx(d + r * Ns)] = v[r];
+      }
+    }
+  }
+}
+template <typename C, int DIR, bool FIRST, bool LAST, class IO, class IDX>
+__device__ __forceinline__ void gen_pass_any(int R, IO& io, const IDX& idx, const C* src, C* dst, const C* tw, int n,
+                                             int Ns, int j, int TP, bool active) {
+  switch (R) {
+    case 2: gen_pass<C, DIR, 2, FIRST, LAST>(io, idx, src, dst, tw, n, Ns, j, TP, active); break;
+    case 3: gen_pass<C, DIR, 3, FIRST, LAST>(io, idx, src, dst, tw, n, Ns, j, TP, active); break;
+    case 4: gen_pass<C, DIR, 4, FIRST, LAST>(io, idx, src, dst, tw, n, Ns, j, TP, active); break;
+    case 5: gen_pass<C, DIR, 5, FIRST, LAST>(io, idx, src, dst, tw, n, Ns, j, TP, active); break;
+    case 7: gen_pass<C, DIR, 7, FIRST, LAST>(io, idx, src, dst, tw, n, Ns, j, TP, active); break;
+    case 8: gen_pass<C, DIR, 8, FIRST, LAST>(io, idx, src, dst, tw, n, Ns, j, TP, active); break;
+    default: gen_pass<C, DIR, 16, FIRST, LAST>(io, idx, src, dst, tw, n, Ns, j, TP, active); break;
+  }
+}
+struct GenLineIdx {
+  int base;
+  __device__ __forceinline__ int operator()(int t) const { return base + t; }
+};
+struct GenColIdx {
+  int W, c;
+  __device__ __forceinline__ int operator()(int t) const { return t * W + c; }
+};
+
+constexpr int kGenThreads = 256;
+
+template <typename Real, int DIR, bool CONTIG, bool SPEC = false>
+__global__ void __launch_bounds__(kGenThreads) fft_generic_kernel(const __grid_constant__ PassArgs a) {
+  using C = typename CT<Real>::type;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int n = a.gen.n, per = a.gen_per;
+  const int TP = kGenThreads / per;  // threads per line / column
+  C* buf[2] = {reinterpret_cast<C*>(smem_raw), reinterpret_cast<C*>(smem_raw) + (size_t)per * n};
+  int q, j;
+  long long l0, l1;
+  bool active;
+  bool part;  // the thread has a line / column slot (per need not divide the CTA size)
+  if constexpr (CONTIG) {
+    q = threadIdx.x / TP;
+    j = threadIdx.x % TP;
+    part = q < per;
+    const long long line = (long long)blockIdx.x * per + q;
+    active = part && line < a.L0 * a.L1;
+    l1 = active ? line / a.L0 : 0;
+    l0 = active ? line - l1 * a.L0 : 0;
+  } else {
+    q = threadIdx.x % per;
+    j = threadIdx.x / per;
+    part = j < TP;
+    const long long ntile = (a.L0 + per - 1) / per;
+    l1 = blockIdx.x / ntile;
+    l0 = (blockIdx.x - l1 * ntile) * per + q;
+    active = part && l0 < a.L0;
+    if (!active) l0 = 0;
+  }
+  if (!part) j = 1 << 30;  // no butterflies (the loops below start past the end); still at every barrier
+  GIO<C, CONTIG, SPEC> io;
+  io.init(a.in, a.out, l0, l1, a.scale);
+  io.spectral(a, l0, l1);
+  const C* tw = reinterpret_cast<const C*>(a.tw);
+  const int np = a.gen.npass;
+  int Ns = 1, twoff = 0;
+  for (int p = 0; p < np; ++p) {
+    const int R = a.gen.rad[p];
+    const bool first = p == 0, last = p == np - 1;
+    const C* src = buf[p & 1];
+    C* dst = buf[(p + 1) & 1];
+    const C* twp = tw + twoff;
+    if constexpr (CONTIG) {
+      GenLineIdx idx{q * n};
+      if (first && last) gen_pass_any<C, DIR, true, true>(R, io, idx, src, dst, twp, n, Ns, j, TP, active);
+      else if (first) gen_pass_any<C, DIR, true, false>(R, io, idx, src, dst, twp, n, Ns, j, TP, active);
+      else if (last) gen_pass_any<C, DIR, false, true>(R, io, idx, src, dst, twp, n, Ns, j, TP, active);
+      else gen_pass_any<C, DIR, false, false>(R, io, idx, src, dst, twp, n, Ns, j, TP, active);
+    } else {
+      GenColIdx idx{per, q};
+      if (first && last) gen_pass_any<C, DIR, true, true>(R, io, idx, src, dst, twp, n, Ns, j, TP, active);
+      else if (first) gen_pass_any<C, DIR, true, false>(R, io, idx, src, dst, twp, n, Ns, j, TP, active);
+      else if (last) gen_pass_any<C, DIR, false, true>(R, io, idx, src, dst, twp, n, Ns, j, TP, active);
+      else gen_pass_any<C, DIR, false, false>(R, io, idx, src, dst, twp, n, Ns, j, TP, active);
+    }
+    if (p > 0) twoff += (R - 1) * Ns;
+    Ns *= R;
+    if (!last) __syncthreads();
+  }
 }
 
 }  // namespace dfft

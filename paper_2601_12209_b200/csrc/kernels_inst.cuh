@@ -63,6 +63,22 @@ KernelInfo make_strided() {
   }
   return k;
 }
+// generic lengths: lines (contig) or columns (strided) per CTA so that the ping-pong line buffers
+// stay within 64 KB and every line keeps >= 32 threads
+template <typename Real, int DIR, bool CONTIG, bool SPEC = false>
+KernelInfo make_generic(int n) {
+  KernelInfo k;
+  k.generic = true;
+  k.fn = (const void*)&fft_generic_kernel<Real, DIR, CONTIG>;
+  if constexpr (!CONTIG && DIR < 0) k.spec_fn = (const void*)&fft_generic_kernel<Real, DIR, false, true>;
+  const int es = (int)sizeof(Real) * 2;
+  int per = 32768 / (n * es);
+  per = per < 1 ? 1 : per > 8 ? 8 : per;
+  k.threads = kGenThreads;
+  k.per_cta = per;
+  k.smem = (size_t)2 * per * n * es;
+  return k;
+}
 }  // namespace
 
 bool DFFT_LOOKUP(int family, int n, int dir, KernelInfo* out) {
@@ -80,7 +96,10 @@ bool DFFT_LOOKUP(int family, int n, int dir, KernelInfo* out) {
   switch (n) {
     DFFT_LENGTHS(DFFT_CASE)
     default:
-      return false;
+      if (!length_supported(n) || (family != kContig && family != kStrided)) return false;
+      if (family == kContig) *out = dir < 0 ? make_generic<DFFT_REAL, -1, true>(n) : make_generic<DFFT_REAL, 1, true>(n);
+      else *out = dir < 0 ? make_generic<DFFT_REAL, -1, false>(n) : make_generic<DFFT_REAL, 1, false>(n);
+      return true;
   }
 #undef DFFT_CASE
 }

@@ -28,6 +28,7 @@ struct KernelInfo {
   bool tma_st_only = false;              // the TMA variant exists only with TMA stores (R2R)
   int tma_threads = 0, tma_w = 0, tma_boxr = 0, tma_maxr = 16;  // tma_maxr: its radix schedule
   size_t tma_smem = 0;
+  bool generic = false;  // fft_generic_kernel: the radix schedule is passed at run time (PassArgs::gen)
 };
 
 // Supported axis lengths: 2^a (2..4096), 3·2^a (3..3072), and the paper's
@@ -39,7 +40,8 @@ struct KernelInfo {
 
 bool lookup_kernel_f32(int family, int n, int dir, KernelInfo* out);
 bool lookup_kernel_f64(int family, int n, int dir, KernelInfo* out);
-bool length_supported(long long n);
+bool length_supported(long long n);    // c2c axis: specialised or generic (2^a 3^b 5^c 7^d <= 4096)
+bool length_specialised(long long n);  // one of DFFT_LENGTHS (R2C / C2R / DCT / DST need it)
 // radix schedule of length n (for twiddle generation): returns npass, fills rad[]
 int length_schedule(int n, int rad[kMaxPass], int maxr = 16);
 

@@ -560,3 +560,45 @@ def test_cuda_graph_capture_single_gpu(oracle_mod):
     a = oracle_mod.gen_complex(7, shape)
     assert oracle_mod.rel_l2(y.cpu().numpy(), oracle_mod.fft3d(a, -1)) <= 1e-12
     assert oracle_mod.rel_l2(z.cpu().numpy(), a) <= 1e-12
+
+
+# ------------------------------------------------------------------------------ generic lengths
+GENERIC = [10, 14, 45, 49, 60, 100, 343, 600, 960, 1000, 2187, 4000]
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("n", GENERIC)
+def test_fft1d_generic_lengths(oracle_mod, n, prec):
+    """2^a 3^b 5^c 7^d lengths without a specialised kernel run the generic runtime-schedule kernel
+    (csrc/fft_kernels.cuh fft_generic_kernel): the DFT definition vs the oracle."""
+    batch = 11
+    x = inputs.gen_complex_np(3, (n, batch, 1), f32=(prec == "f32"))[0]
+    xt = _t(x, prec)
+    for sign in (-1, 1):
+        y = torch.empty_like(xt)
+        dfft.fft1d(xt, y, sign)
+        torch.cuda.synchronize()
+        ref = np.stack([oracle_mod.fft1d(row.astype(np.complex128), sign) for row in x])
+        e = rel_l2(y.cpu().numpy(), ref)
+        assert e <= QUALITY[prec], (n, sign, e)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape", [(60, 50, 42), (100, 14, 96), (600, 10, 8)])
+def test_3d_generic_lengths_single_gpu(oracle_mod, shape, prec):
+    ef, er, ei = _run_single(oracle_mod, shape, "pencil", prec)
+    assert ef <= QUALITY[prec] and ei <= QUALITY[prec] and er <= GATE[prec], (ef, er, ei)
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,grid,exchange", [((60, 50, 42), (2, 2), "p2p"), ((100, 14, 96), (2, 4), "p2p"),
+                                                 ((60, 50, 42), (2, 2), "nccl")])
+def test_generic_lengths_simulated_ranks(oracle_mod, shape, grid, exchange, prec):
+    ef, er, _ = _run_sim(oracle_mod, shape, "pencil", grid, prec, 0, exchange=exchange)
+    assert ef <= QUALITY[prec] and er <= GATE[prec], (ef, er)
+
+
+def test_generic_length_poisson(oracle_mod):
+    # the strided generic kernel carries the Poisson multiplier too (last forward stage)
+    e = _poisson_case(oracle_mod, (60, 50, 42), "pencil", (1, 1), "f64", (1.0, 2.0, 0.5), "c2c")
+    assert e <= GATE["f64"], e
