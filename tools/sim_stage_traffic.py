@@ -2,7 +2,7 @@
 
     python tools/sim_stage_traffic.py P1 P2 [n] [prec]
 Runs fwd+inv twice on simulated ranks (the product schedule, fused-store layouts); under
-    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:fft_ \
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:"fft_(strided|contig|generic)" \
         -s <launches per fwd+inv> -c <launches per fwd+inv> --csv
 the second fwd+inv's stage kernels are captured.  Prints the launch count per fwd+inv and the
 algorithmic bytes of every stage launch (read + write of the local array chunk) in issue order.
