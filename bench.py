@@ -384,7 +384,15 @@ def main():
             traffic_tab = json.load(f).get(f"{shape[0]}x{shape[1]}x{shape[2]}_{args.precision}_{grid[0]}x{grid[1]}", {})
     except Exception:
         pass
-    if P == 1:  # single GPU: forward x, z, y; inverse y, z, x
+    if P == 1 and any(d["family"] == "xz8" for d in fwd.describe()):
+        # single GPU, nz = 8·M: the x pass carries one radix-8 z step; the z stage is M points long
+        stage_names = {"fwd": {"stage_A": "x-FFT + radix-8 z step (xz8, whole lines to [q][z1][y][x])",
+                               "stage_B": "z-FFT, M = nz/8 points (strided TMA, 256 B rows)",
+                               "stage_C": "y-FFT (strided TMA)"},
+                       "inv": {"stage_A": "y-IFFT (strided TMA)",
+                               "stage_B": "z-IFFT, M = nz/8 points (strided TMA, 256 B rows)",
+                               "stage_C": "inverse radix-8 z step + x-IFFT (xz8, 1/N)"}}
+    elif P == 1:  # single GPU: forward x, z, y; inverse y, z, x
         stage_names = {"fwd": {"stage_A": "x-FFT (contig)", "stage_B": "z-FFT (strided TMA, reads [y][z][x])",
                                "stage_C": "y-FFT (strided TMA)"},
                        "inv": {"stage_A": "y-IFFT (strided TMA)", "stage_B": "z-IFFT (strided TMA, writes [y][z][x])",

@@ -272,6 +272,12 @@ dfft_status_t dfft_plan_set_poisson(dfft_plan_t plan, double dx, double dy, doub
 dfft_status_t dfft_plan_set_profiling(dfft_plan_t plan, int on);
 dfft_status_t dfft_plan_phase_times(dfft_plan_t plan, double ms[5], long long launches[5], int reset);
 dfft_status_t dfft_plan_stage_bytes(dfft_plan_t plan, double bytes[5]);
+/* Plan description (rank 0's stages): one text line per stage launch unit, "<phase> <kernel
+ * family> n=<length> L0=.. L1=.. in_tstride=.. out_tstride=.. tma=0|1", NUL-terminated in buf
+ * (caller-owned, len bytes).  DFFT_ERR_INVALID_VALUE when it does not fit (buf holds a truncated
+ * copy).  Families: contig, strided, contig_r2c, contig_c2r, contig_dct, strided_dct, contig_dst,
+ * strided_dst, xz8 (the single-GPU x-FFT fused with a radix-8 z step). */
+dfft_status_t dfft_plan_describe(dfft_plan_t plan, char* buf, size_t len);
 /* Timeline of the profiled executes (Fig. 9 per-chunk analog): one span per stage launch or
  * exchange step, on stream 0 (compute X) or 1 (Y), with its chunk and rank, in milliseconds
  * relative to the origin event its execute recorded on the caller's stream (exec numbers count

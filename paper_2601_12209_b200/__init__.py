@@ -34,6 +34,7 @@ EXPORTS = [
     "dfft_comm_init_sim", "dfft_comm_destroy", "dfft_plan_create", "dfft_plan_box", "dfft_plan_box_rank",
     "dfft_plan_bytes", "dfft_decomp_box", "dfft_plan_chunks", "dfft_execute", "dfft_execute_host", "dfft_execute_sim",
     "dfft_destroy", "dfft_fft1d", "dfft_plan_set_profiling", "dfft_plan_phase_times", "dfft_plan_stage_bytes",
+    "dfft_plan_describe",
     "dfft_plan_set_poisson", "dfft_kernel_launches", "dfft_plan_timeline", "dfft_set_timeout_ms", "dfft_plan_status",
     "dfft_execute_host_chain", "dfft_plan_create_kinds",
 ]
@@ -102,6 +103,7 @@ def lib():
             L.dfft_plan_set_poisson.argtypes = [_vp, ctypes.c_double, ctypes.c_double, ctypes.c_double]
         L.dfft_plan_phase_times.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_longlong), _int]
         L.dfft_plan_stage_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_double)]
+        L.dfft_plan_describe.argtypes = [_vp, ctypes.c_char_p, ctypes.c_size_t]
         L.dfft_plan_timeline.argtypes = [_vp, ctypes.POINTER(Span), _int, ctypes.POINTER(_int)]
         L.dfft_set_timeout_ms.argtypes = [ctypes.c_longlong]
         L.dfft_plan_status.argtypes = [_vp]
@@ -326,6 +328,18 @@ class Plan:
         b = (ctypes.c_double * 5)()
         _check(lib().dfft_plan_stage_bytes(self.h, b), "dfft_plan_stage_bytes")
         return {PHASES[q]: b[q] for q in range(5)}
+
+    def describe(self):
+        """Rank 0's stages: [{"phase", "family", "n", "L0", "L1", "in_tstride", "out_tstride", "tma"}]."""
+        buf = ctypes.create_string_buffer(8192)
+        _check(lib().dfft_plan_describe(self.h, buf, len(buf)), "dfft_plan_describe")
+        out = []
+        for line in buf.value.decode().splitlines():
+            ph, fam, *kv = line.split()
+            d = {"phase": ph, "family": fam}
+            d.update({k: int(v) for k, v in (t.split("=") for t in kv)})
+            out.append(d)
+        return out
 
     def destroy(self):
         if getattr(self, "h", None):

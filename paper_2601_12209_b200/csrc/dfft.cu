@@ -215,6 +215,39 @@ dfft_status_t get_dct_twiddles(int L, bool f64, int dir, int dev, const void** o
   return DFFT_SUCCESS;
 }
 
+// w_M^e = exp(dir·2πi·e/M), e < M, long double once each (the radix-8 z step of fft_xz8_kernel)
+dfft_status_t get_root_twiddles(int M, bool f64, int dir, int dev, const void** out) {
+  static std::map<TwKey, void*> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  TwKey key{M, f64, dir, dev, -3};
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return DFFT_SUCCESS;
+  }
+  const size_t es = f64 ? 16 : 8;
+  std::vector<unsigned char> h((size_t)M * es);
+  for (int e = 0; e < M; ++e) {
+    const long double a = 2.0L * 3.141592653589793238462643383279502884L * (long double)e / (long double)M;
+    const long double c = cosl(a), sn = (long double)dir * sinl(a);
+    if (f64) {
+      reinterpret_cast<double*>(h.data())[2 * e] = (double)c;
+      reinterpret_cast<double*>(h.data())[2 * e + 1] = (double)sn;
+    } else {
+      reinterpret_cast<float*>(h.data())[2 * e] = (float)c;
+      reinterpret_cast<float*>(h.data())[2 * e + 1] = (float)sn;
+    }
+  }
+  void* d = nullptr;
+  CU(cudaSetDevice(dev));
+  CU(cudaMalloc(&d, h.size()));
+  CU(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
+  cache[key] = d;
+  *out = d;
+  return DFFT_SUCCESS;
+}
+
 dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
   bool ok = f64 ? lookup_kernel_f64(family, n, dir, k) : lookup_kernel_f32(family, n, dir, k);
   if (!ok) return fail(DFFT_ERR_UNSUPPORTED, "axis length %d not instantiated", n);
@@ -379,6 +412,7 @@ struct dfft_plan_s {
     const void* in;
     void* out;
     cudaGraphExec_t exec;
+    long long launches;  // library kernels in the graph (credited to dfft_kernel_launches per replay)
   };
   std::vector<GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;
@@ -524,7 +558,8 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
       linearize_tblocked(*in_segs, s.in, s.in_bases, s.a.in, (long long)pl->es))
     in_segs = nullptr;
   if (out_segs && linearize(*out_segs, n, s.out, s.out_bases, s.a.out, (long long)pl->es)) out_segs = nullptr;
-  if (is_contig(family) && ((!in_segs && s.a.in.tstride != 1) || (!out_segs && s.a.out.tstride != 1)))
+  if (is_contig(family) && family != kContigXZ8 &&
+      ((!in_segs && s.a.in.tstride != 1) || (!out_segs && s.a.out.tstride != 1)))
     return fail(DFFT_ERR_INTERNAL, "contig stage with a non-unit t-stride side");
   std::vector<longlong2> in_tab_h, out_tab_h;
   if (in_segs) in_tab_h = seg_table(*in_segs, n);
@@ -573,7 +608,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
     }
   }
   // contig: walk lines so that consecutive CTAs write adjacent lines (unsegmented outputs)
-  if (is_contig(family) && !out_tab && !getenv("DFFT_LORDER0") && s.a.out.bw == 0 && L1 > 1 &&
+  if (is_contig(family) && family != kContigXZ8 && !out_tab && !getenv("DFFT_LORDER0") && s.a.out.bw == 0 && L1 > 1 &&
       std::llabs(s.a.out.s1) < std::llabs(s.a.out.s0))
     s.a.lorder = 1;
   if (is_contig(family)) s.grid = (L0 * L1 + s.k.per_cta - 1) / s.k.per_cta;
@@ -1040,7 +1075,96 @@ dfft_status_t build_inverse_bc(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
 //            y (ws -> out, natural -> natural)
 //   inverse: y (in -> out, natural), z (natural -> ws as [y][z][x]: the large-pitch read),
 //            x (ws -> out, natural, ×1/N)
+// Single GPU, c2c, nz = 8·M: the z-FFT split by one radix-8 Cooley-Tukey step (fft_xz8_kernel).
+//   forward: A = x-FFT + radix-8 z step (natural in -> ws [q][z1][y][x], whole lines),
+//            B = M-point z-FFTs (ws, rows ny·nx apart -> natural, rows 8·ny·nx apart; both sides
+//                256-512 B wide: the strided kernel's tile for an M-row column is 32 columns),
+//            C = y-FFT (natural -> natural, in place on `out`)
+//   inverse: A = y-IFFT (in -> out), B = M-point z-IFFTs (out -> ws), C = inverse radix-8 step +
+//            x-IFFT (ws -> out, ×1/N)
+// No pass reads or writes 64 B rows at a multi-MB pitch, the pattern that caps the plain z-pass at
+// ~4.5 TB/s.  Needs c2c, nz % 8 == 0 with a specialised TMA kernel for nz/8, and the
+// fused kernel for nx.
+bool xz8_ok(dfft_plan_t pl, const Geo& g) {
+  if (pl->r2c || pl->r2r || g.nz % 8 || g.nz < 64 || getenv("DFFT_NO_XZ8") || !g_use_tma || !tensor_map_encoder())
+    return false;
+  if (pl->kind[2] != DFFT_KIND_DFT || pl->kind[1] != DFFT_KIND_DFT) return false;
+  KernelInfo kx, kz;
+  const long long M = g.nz / 8;
+  const bool okx = pl->f64 ? lookup_kernel_f64(kContigXZ8, (int)g.nx, pl->dir, &kx)
+                           : lookup_kernel_f32(kContigXZ8, (int)g.nx, pl->dir, &kx);
+  const bool okz = length_specialised(M) && (pl->f64 ? lookup_kernel_f64(kStrided, (int)M, pl->dir, &kz)
+                                                     : lookup_kernel_f32(kStrided, (int)M, pl->dir, &kz));
+  return okx && kx.fn && okz && kz.tma_fn && (g.nx * (long long)pl->es) % 16 == 0;
+}
+
+dfft_status_t build_single_xz8(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
+  const long long nx = g.nx, ny = g.ny, nz = g.nz, M = nz / 8, es = (long long)pl->es;
+  rp.ws_bytes = (size_t)(nx * ny * nz * es);
+  rp.A.resize(1);
+  rp.B.resize(1);
+  rp.E1.resize(1);
+  rp.E2.resize(1);
+  Stage &A = rp.A[0], &B = rp.B[0], &C = rp.C;
+  const double inv_scale = 1.0 / ((double)nx * (double)ny * (double)nz);
+  // the intermediate [q][z1][y][x]: line (l0 = y, l1 = z1, q), so consecutive CTAs of the fused
+  // stage touch adjacent lines on both sides; the M-point z stage sees (x, y) as one contiguous
+  // l0 axis: t = z1 (pitch ny·nx), l1 = q; natural seen by that stage: t = m (z = 8m + q), l1 = q
+  auto mid_lines = [&](SideMap& m) { set_side(m, M * ny * nx, nx, ny * nx); };  // tstride = q stride
+  auto nat_lines = [&](SideMap& m) { set_side(m, M * ny * nx, nx, ny * nx); };  // tstride = k stride
+  auto mid_z = [&](SideMap& m) { set_side(m, ny * nx, 1, M * ny * nx); };
+  auto nat_z = [&](SideMap& m) { set_side(m, 8 * ny * nx, 1, ny * nx); };
+  auto nat_y = [&](SideMap& m) { set_side(m, nx, 1, ny * nx); };  // t = y, l0 = x, l1 = z
+  const void* root = nullptr;
+  ST(get_root_twiddles((int)nz, pl->f64, pl->dir, pl->comm->device, &root));
+  if (pl->dir == DFFT_FORWARD) {
+    A.in = {kUserIn, 0};
+    nat_lines(A.a.in);
+    A.out = {kWs, 0};
+    mid_lines(A.a.out);
+    A.a.scale = 1.0;
+    ST(finish_stage(pl, A, kContigXZ8, (int)nx, ny, M, nullptr, nullptr));
+    A.a.tw2 = root;
+    B.in = {kWs, 0};
+    mid_z(B.a.in);
+    B.out = {kUserOut, 0};
+    nat_z(B.a.out);
+    B.a.scale = 1.0;
+    ST(finish_stage(pl, B, kStrided, (int)M, nx * ny, 8, nullptr, nullptr));
+    C.in = {kUserOut, 0};
+    nat_y(C.a.in);
+    C.out = {kUserOut, 0};
+    nat_y(C.a.out);
+    C.a.scale = 1.0;
+    C.last_fwd = true;  // t = y, l0 = x, l1 = z
+    C.gax[0] = 1, C.gax[1] = 0, C.gax[2] = 2;
+    ST(finish_stage(pl, C, fam_y(pl), (int)ny, nx, nz, nullptr, nullptr));
+  } else {
+    A.in = {kUserIn, 0};
+    nat_y(A.a.in);
+    A.out = {kUserOut, 0};
+    nat_y(A.a.out);
+    A.a.scale = 1.0;
+    ST(finish_stage(pl, A, fam_y(pl), (int)ny, nx, nz, nullptr, nullptr));
+    B.in = {kUserOut, 0};
+    nat_z(B.a.in);
+    B.out = {kWs, 0};
+    mid_z(B.a.out);
+    B.a.scale = 1.0;
+    ST(finish_stage(pl, B, kStrided, (int)M, nx * ny, 8, nullptr, nullptr));
+    C.in = {kWs, 0};
+    mid_lines(C.a.in);
+    C.out = {kUserOut, 0};
+    nat_lines(C.a.out);
+    C.a.scale = inv_scale;
+    ST(finish_stage(pl, C, kContigXZ8, (int)nx, ny, M, nullptr, nullptr));
+    C.a.tw2 = root;
+  }
+  return DFFT_SUCCESS;
+}
+
 dfft_status_t build_single(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
+  if (xz8_ok(pl, g)) return build_single_xz8(pl, g, rp);
   const long long nx = g.nx, ny = g.ny, nz = g.nz, nxc = g.nxc, es = (long long)pl->es;
   const long long nxl = xreal(pl) ? nx / 2 : nx;
   const long long W = nxc * ny * nz;
@@ -1825,11 +1949,14 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
   for (size_t q = 0; q < pl->graphs.size(); ++q)
     if (pl->graphs[q].in == in && pl->graphs[q].out == out) {
       CU(cudaGraphLaunch(pl->graphs[q].exec, user));
+      g_launches.fetch_add(pl->graphs[q].launches, std::memory_order_relaxed);
       return DFFT_SUCCESS;
     }
   if (!pl->cap_stream) CU(cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking));
   CU(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
+  const long long n0 = g_launches.load(std::memory_order_relaxed);
   const dfft_status_t st = issue_rank(pl, in, out, pl->cap_stream);
+  const long long nk = g_launches.load(std::memory_order_relaxed) - n0;  // (counted once: the first replay)
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(pl->cap_stream, &graph);
   if (st != DFFT_SUCCESS || ec != cudaSuccess || !graph) {  // capture failed: issue directly
@@ -1849,7 +1976,7 @@ dfft_status_t execute_rank(dfft_plan_t pl, const void* in, void* out, cudaStream
     cudaGraphExecDestroy(pl->graphs.front().exec);
     pl->graphs.erase(pl->graphs.begin());
   }
-  pl->graphs.push_back({in, out, exec});
+  pl->graphs.push_back({in, out, exec, nk});
   CU(cudaGraphLaunch(exec, user));
   return DFFT_SUCCESS;
 }
@@ -2831,6 +2958,7 @@ dfft_status_t dfft_plan_stage_bytes(dfft_plan_t pl, double bytes[5]) {
   auto stage_b = [&](const Stage& s) {
     if (s.empty) return 0.0;
     double elems = (double)s.a.L0 * (double)s.a.L1 * (double)s.n;  // complex elements of the FFT
+    if (s.family == kContigXZ8) elems *= 8;                             // a (l0, l1) pair is 8 lines
     return 2.0 * elems * (double)pl->es;
   };
   // off-rank bytes of each exchange from the rank's boxes (identical for every transport; with
@@ -2857,6 +2985,28 @@ dfft_status_t dfft_plan_stage_bytes(dfft_plan_t pl, double bytes[5]) {
   bytes[4] = stage_b(rp.C);
   for (const Stage& c : rp.Cc) bytes[4] += stage_b(c);
   return DFFT_SUCCESS;
+}
+
+dfft_status_t dfft_plan_describe(dfft_plan_t pl, char* buf, size_t len) {
+  if (!pl || !buf || len == 0) return fail(DFFT_ERR_INVALID_VALUE, "null argument");
+  static const char* fam[] = {"contig", "strided", "contig_r2c", "contig_c2r", "contig_dct", "strided_dct",
+                              "contig_dst", "strided_dst", "xz8"};
+  const RankPlan& rp = pl->ranks[0];
+  std::string out;
+  auto one = [&](const char* phase, const Stage& s) {
+    if (s.empty) return;
+    char line[256];
+    const int f = s.family >= 0 && s.family <= kContigXZ8 ? s.family : 0;
+    snprintf(line, sizeof line, "%s %s n=%d L0=%lld L1=%lld in_tstride=%lld out_tstride=%lld tma=%d\n", phase,
+             fam[f], s.n, s.a.L0, s.a.L1, s.a.in.tstride, s.a.out.tstride, s.tma_variant);
+    out += line;
+  };
+  for (const Stage& s : rp.A) one("stage_A", s);
+  for (const Stage& s : rp.B) one("stage_B", s);
+  one("stage_C", rp.C);
+  for (const Stage& s : rp.Cc) one("stage_C", s);
+  snprintf(buf, len, "%s", out.c_str());
+  return out.size() < len ? DFFT_SUCCESS : fail(DFFT_ERR_INVALID_VALUE, "buffer of %zu bytes too small", len);
 }
 
 dfft_status_t dfft_destroy(dfft_plan_t pl) {

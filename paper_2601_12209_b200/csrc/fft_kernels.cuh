@@ -729,6 +729,111 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ x-FFT fused with a radix-8 z step
+// The z axis of length Nz = 8·M is split by one Cooley-Tukey step (z = z1 + M·k, K = 8·m + q):
+//   X[8m + q] = Σ_{z1} w_M^{z1·m} · Y_q[z1],    Y_q[z1] = w_Nz^{z1·q} · Σ_{k<8} x[z1 + M·k] · w_8^{k·q}
+// Forward (DIR -1): a CTA takes the 8 x-lines (y, z1 + M·k), runs their x-FFT, then the radix-8 step
+// across the lines and the twiddle, and writes Y_q as line q of the intermediate.  The remaining
+// M-point z-FFTs run as a strided stage whose tiles are only M rows deep, so they are 256-512 B wide
+// — the row width the DRAM wants at any pitch.  Inverse (DIR +1): the mirror — the 8
+// lines q in, conjugate twiddle, inverse radix-8 step, then the x-IFFT of each line k.
+// Line addressing (complex elements): line (l0, l1, r) starts at base + l0·s0 + l1·s1 + r·tstride,
+// r = k or q; the t stride along a line is 1.
+template <int N> struct XZ8Cfg {
+  static constexpr Sched S = make_sched(N);
+  static constexpr int T = S.T, THREADS = 8 * T, LS = N + (N >> 4);
+  static constexpr bool OK = THREADS <= 1024 && THREADS >= 64;
+  // 8 padded lines in shared memory; minimum resident CTAs for __launch_bounds__: 2 where two
+  // fit by shared memory and still leave 64 (f32) / 128 (f64) registers a thread — the budgets
+  // the radix-16 butterflies compile in without spills (f32 N = 1024: 64) — else 1
+  static constexpr int smem(int es) { return 8 * LS * es; }
+  static constexpr bool fits(int es) { return smem(es) <= 227 * 1024; }
+  static constexpr int minb(int es) {
+    return 2 * (smem(es) + 1024) <= 228 * 1024 && 2 * THREADS * (es == 16 ? 128 : 64) <= 65536 ? 2 : 1;
+  }
+};
+template <typename C, int N, int DIR> struct XZ8IO : GIO<C, true> {
+  static constexpr bool kSyncAfterLoad = DIR > 0;  // inverse: pass 0 reads the line from smem in place
+  const C* src;  // forward: this line in global memory; inverse: unused (smem)
+  C* dst;        // inverse: this line in global memory
+  C* line;       // this line in shared memory, ContigSM positions (base applied)
+  __device__ __forceinline__ C load(int t) const {
+    if constexpr (DIR < 0) return src[t];
+    else return line[t + (t >> 4)];
+  }
+  __device__ __forceinline__ void store(int t, C v) const {
+    if constexpr (DIR < 0) {
+      line[t + (t >> 4)] = v;
+    } else {
+      if (this->scale != 1) {
+        v.x *= this->scale;
+        v.y *= this->scale;
+      }
+      dst[t] = v;
+    }
+  }
+};
+
+template <typename Real, int N, int DIR>
+__global__ void __launch_bounds__(XZ8Cfg<N>::THREADS, XZ8Cfg<N>::minb(2 * sizeof(Real))) fft_xz8_kernel(const __grid_constant__ PassArgs a) {
+  using C = typename CT<Real>::type;
+  using Cfg = XZ8Cfg<N>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  C* smem = reinterpret_cast<C*>(smem_raw);
+  const int li = threadIdx.x / Cfg::T, j = threadIdx.x % Cfg::T;
+  const long long l1 = blockIdx.x / a.L0, l0 = blockIdx.x - l1 * a.L0;
+  const C* in = reinterpret_cast<const C*>(a.in.base) + l0 * a.in.s0 + l1 * a.in.s1;
+  C* out = reinterpret_cast<C*>(a.out.base) + l0 * a.out.s0 + l1 * a.out.s1;
+  const C* tw = reinterpret_cast<const C*>(a.tw);
+  const C* tw2 = reinterpret_cast<const C*>(a.tw2);  // w_Nz^e, e < Nz (sign DIR)
+  C* line = smem + li * Cfg::LS;
+  XZ8IO<C, N, DIR> io;
+  io.scale = (Real)a.scale;
+  io.line = line;
+  ContigSM sm{li * Cfg::LS};
+  if constexpr (DIR < 0) {
+    io.src = in + li * a.in.tstride;  // x-line k = li
+    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, true);
+    __syncthreads();
+    for (int t = threadIdx.x; t < N; t += Cfg::THREADS) {  // radix-8 step across the 8 lines
+      C v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = smem[k * Cfg::LS + t + (t >> 4)];
+      dft<DIR, 8>(v);
+      out[t] = v[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) out[q * a.out.tstride + t] = cmul(v[q], __ldg(tw2 + l1 * q));
+    }
+  } else {
+    // the 8 lines q at column t straight from global memory (8 loads in flight per column),
+    // conjugate twiddle, inverse radix-8 step, lines k into shared memory
+    constexpr int IT = (N + Cfg::THREADS - 1) / Cfg::THREADS;
+    C v[IT][8];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {  // every load of the thread in flight at once
+      const int t = threadIdx.x + it * Cfg::THREADS;
+      if (t < N) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[it][q] = in[q * a.in.tstride + t];
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int t = threadIdx.x + it * Cfg::THREADS;
+      if (t < N) {
+#pragma unroll
+        for (int q = 1; q < 8; ++q) v[it][q] = cmul(v[it][q], __ldg(tw2 + l1 * q));
+        dft<DIR, 8>(v[it]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) smem[k * Cfg::LS + t + (t >> 4)] = v[it][k];
+      }
+    }
+    __syncthreads();
+    io.dst = out + li * a.out.tstride;  // x-line k = li
+    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, true);
+  }
+}
+
 // ------------------------------------------------------------------ strided-axis family
 template <typename Real, int N> struct StridedCfg {
   static constexpr Sched S = make_sched(N);

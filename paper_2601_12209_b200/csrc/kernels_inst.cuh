@@ -63,6 +63,20 @@ KernelInfo make_strided() {
   }
   return k;
 }
+template <typename Real, int N, int DIR>
+KernelInfo make_xz8() {
+  KernelInfo k;
+  if constexpr (XZ8Cfg<N>::OK && XZ8Cfg<N>::fits(2 * sizeof(Real))) {
+    using Cfg = XZ8Cfg<N>;
+    k.fn = (const void*)&fft_xz8_kernel<Real, N, DIR>;
+    k.threads = Cfg::THREADS;
+    k.per_cta = 1;  // one (y, z1) pair of 8 lines per CTA
+    k.smem = (size_t)8 * Cfg::LS * sizeof(Real) * 2;
+    k.twlen = sched_twlen(Cfg::S);
+  }
+  return k;
+}
+
 // generic lengths: lines (contig) or columns (strided) per CTA so that the ping-pong line buffers
 // stay within 64 KB and every line keeps >= 32 threads
 template <typename Real, int DIR, bool CONTIG, bool SPEC = false>
@@ -90,6 +104,7 @@ bool DFFT_LOOKUP(int family, int n, int dir, KernelInfo* out) {
     else if (family == kContigDct) *out = dir < 0 ? make_contig<DFFT_REAL, N, -1, 3>() : make_contig<DFFT_REAL, N, 1, 4>(); \
     else if (family == kStridedDct) *out = dir < 0 ? make_strided_dct<DFFT_REAL, N, -1>() : make_strided_dct<DFFT_REAL, N, 1>(); \
     else if (family == kContigDst) *out = dir < 0 ? make_contig<DFFT_REAL, N, -1, 5>() : make_contig<DFFT_REAL, N, 1, 6>(); \
+    else if (family == kContigXZ8) { *out = dir < 0 ? make_xz8<DFFT_REAL, N, -1>() : make_xz8<DFFT_REAL, N, 1>(); return out->fn != nullptr; } \
     else if (family == kStridedDst) *out = dir < 0 ? make_strided_dct<DFFT_REAL, N, -1, true>() : make_strided_dct<DFFT_REAL, N, 1, true>(); \
     else *out = dir < 0 ? make_strided<DFFT_REAL, N, -1>() : make_strided<DFFT_REAL, N, 1>();    \
     return true;

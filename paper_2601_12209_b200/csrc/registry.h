@@ -9,7 +9,8 @@
 namespace dfft {
 
 enum Family {
-  kContig = 0, kStrided = 1, kContigR2C = 2, kContigC2R = 3, kContigDct = 4, kStridedDct = 5, kContigDst = 6, kStridedDst = 7
+  kContig = 0, kStrided = 1, kContigR2C = 2, kContigC2R = 3, kContigDct = 4, kStridedDct = 5, kContigDst = 6, kStridedDst = 7,
+  kContigXZ8 = 8  // x-FFT fused with a radix-8 z step (fft_xz8_kernel; n = the x length)
 };
 
 struct KernelInfo {

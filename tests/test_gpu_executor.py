@@ -272,3 +272,20 @@ def test_execute_host_and_chain(oracle_mod):
         assert oracle_mod.rel_l2(z.numpy(), x.numpy()) <= GATE["f64"]
     with pytest.raises(dfft.DfftError):  # asynchronous calls need pinned host memory
         dfft.execute_host_chain([fwd, inv], np.ascontiguousarray(a), np.empty_like(a), async_=True)
+
+
+def test_kernel_launch_counter_counts_graph_replays():
+    # dfft_kernel_launches credits each replay of a plan's internal graph with the kernels it holds
+    comm = dfft.Comm.create(nranks=1, rank=0, device=0)
+    shape = (64, 48, 64)
+    fwd = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_f32", dfft.FORWARD)
+    x = fwd.alloc_in()
+    y = fwd.alloc_out()
+    x.normal_()
+    deltas = []
+    for _ in range(4):
+        n0 = dfft.kernel_launches()
+        fwd.execute(x, y)
+        deltas.append(dfft.kernel_launches() - n0)
+    torch.cuda.synchronize()
+    assert deltas == [3] * 4, deltas  # three FFT stages per execute, captured or replayed

@@ -602,3 +602,50 @@ def test_generic_length_poisson(oracle_mod):
     # the strided generic kernel carries the Poisson multiplier too (last forward stage)
     e = _poisson_case(oracle_mod, (60, 50, 42), "pencil", (1, 1), "f64", (1.0, 2.0, 0.5), "c2c")
     assert e <= GATE["f64"], e
+
+
+# ------------------------------------------------------------------ single-GPU radix-8 z split (xz8)
+# nz = 8·M with M specialised: the single-GPU c2c plan splits the z-FFT by one radix-8 DIF step fused
+# into the x pass (fft_xz8_kernel).  The oracle's plain 3D DFT is the reference; the
+# DFFT_NO_XZ8 plan (three whole-axis passes) is a second, independent check of the same transform.
+XZ8_SHAPES = [(128, 16, 256), (256, 6, 512), (480, 5, 384), (840, 3, 256), (720, 4, 512), (1024, 4, 256),
+              (128, 9, 1024), (768, 3, 192), (2048, 2, 256), (480, 5, 96)]
+# nx without the fused kernel (64: fewer than 64 threads; 60: generic; 4096: over 1024 threads) or
+# nz/8 without a TMA strided kernel (8, 16: one pass; 21: not specialised): the whole-axis plan
+XZ8_FALLBACK = [(64, 16, 256), (64, 16, 64), (256, 6, 128), (96, 7, 168), (60, 5, 64), (4096, 2, 256)]
+
+
+def _families(shape, prec):
+    comm = dfft.Comm.create(nranks=1, rank=0, device=0)
+    return [d["family"] for d in dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_" + prec, dfft.FORWARD).describe()]
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape", XZ8_SHAPES + XZ8_FALLBACK)
+def test_3d_single_gpu_xz8(oracle_mod, shape, prec):
+    fused = shape in XZ8_SHAPES and not (prec == "f64" and shape[0] == 2048)  # f64 2048: 8 lines > 227 KB
+    assert ("xz8" in _families(shape, prec)) == fused, (_families(shape, prec), shape, prec)
+    ef, er, ei = _run_single(oracle_mod, shape, "pencil", prec, seed=31)
+    assert ef <= GATE[prec] and er <= GATE[prec] and ei <= GATE[prec], (ef, er, ei)
+    assert ef <= QUALITY[prec] and ei <= QUALITY[prec], (ef, er, ei)
+
+
+@pytest.mark.parametrize("shape", [(256, 6, 512), (1024, 4, 256)])
+def test_xz8_matches_whole_axis_plan(shape, monkeypatch):
+    comm = dfft.Comm.create(nranks=1, rank=0, device=0)
+    x = None
+    outs = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("DFFT_NO_XZ8", "1")
+        fwd = dfft.Plan(comm, shape, "pencil", (1, 1), "c2c_f64", dfft.FORWARD)
+        fams = [d["family"] for d in fwd.describe()]
+        assert ("xz8" in fams) == (not off) and fams[1] == "strided", fams
+        if x is None:
+            x = fwd.alloc_in()
+            inputs.fill_box_cuda(x, 17, shape, (0, 0, 0), shape, True)
+        y = fwd.alloc_out()
+        fwd.execute(x, y)
+        torch.cuda.synchronize()
+        outs.append(y.cpu().numpy())
+    assert rel_l2(outs[0], outs[1]) < 1e-14
