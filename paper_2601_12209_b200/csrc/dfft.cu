@@ -576,7 +576,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
     return DFFT_SUCCESS;
   }
   ST(get_kernel(family, n, pl->f64, pl->dir, &s.k));
-  ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw));
+  ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw, family == kContigXZ8 ? s.k.tma_maxr : 16));
   if (s.k.generic) {  // the radix schedule at run time
     s.a.gen = make_sched(n);
     s.a.gen_per = s.k.per_cta;

@@ -35,8 +35,14 @@ template <> struct CT<double> { using type = double2; };
 
 template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return {a.x + b.x, a.y + b.y}; }
 template <typename C> __device__ __forceinline__ C csub(C a, C b) { return {a.x - b.x, a.y - b.y}; }
+// Fixed contraction (a.x·b.x − a.y·b.y as one fma over a rounded product, likewise the imaginary
+// part): every kernel rounds a twiddle multiply the same way whether the twiddle sits in a register
+// or comes from a load, so the transports' outputs stay bit-identical (test_gpu_executor.py).
 template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
-  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+  if constexpr (sizeof(a.x) == 4)
+    return {__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)), __fmaf_rn(a.x, b.y, __fmul_rn(a.y, b.x))};
+  else
+    return {__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x))};
 }
 // a · (DIR·i):  forward (DIR=-1) multiplies by -i, inverse by +i
 template <int DIR, typename C> __device__ __forceinline__ C mul_i(C a) {
@@ -396,12 +402,45 @@ __device__ __forceinline__ void tile_coords(long long tile, long long ntile, lon
   tx = base + (r - l1 * gw);
 }
 
+// Twiddles of passes >= 1 held in registers.  In a persistent kernel a thread's butterflies are
+// the same in every tile, so the table is read once per CTA instead of once per tile per pass
+// (r02 ncu: the M = 128 z kernel's top stall was long_scoreboard on these loads).
+struct TwNone {
+  static constexpr bool kHoisted = false;
+};
+template <typename C, int N, int MAXR> struct TwHoist {
+  static constexpr bool kHoisted = true;
+  static constexpr Sched S = make_sched(N, MAXR);
+  static constexpr int nb(int p) { return (N / S.rad[p] + S.T - 1) / S.T; }
+  static constexpr int off(int p) {
+    int o = 0;
+    for (int q = 1; q < p; ++q) o += nb(q) * (S.rad[q] - 1);
+    return o;
+  }
+  static constexpr int K = off(S.npass);
+  C w[K > 0 ? K : 1];
+  template <int P> __device__ __forceinline__ void fill(const C* __restrict__ tw, int j) {
+    if constexpr (P < S.npass) {
+      constexpr int R = S.rad[P], NR = N / R, Ns = sched_ns(S, P);
+#pragma unroll
+      for (int u = 0; u < nb(P); ++u) {
+        const int b = j + S.T * u;
+        const int m = (b < NR ? b : 0) % Ns;
+#pragma unroll
+        for (int r = 1; r < R; ++r) w[off(P) + u * (R - 1) + r - 1] = __ldg(tw + sched_twoff(S, P) + (r - 1) * Ns + m);
+      }
+      fill<P + 1>(tw, j);
+    }
+  }
+  template <int P> __device__ __forceinline__ C get(int u, int r) const { return w[off(P) + u * (S.rad[P] - 1) + r - 1]; }
+};
+
 // --------------------------------------------------------------------------------- Stockham core
 // One thread's part of the passes of one line.  IO supplies the global side:
 //   C load(int t)  and  void store(int t, C v); SM maps t to a shared-memory slot.
-template <typename C, int N, int DIR, int P, int MAXR = 16, class IO, class SM>
+template <typename C, int N, int DIR, int P, int MAXR = 16, class IO, class SM, class TWR = TwNone>
 __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, const C* __restrict__ tw, int j,
-                                              bool active) {
+                                              bool active, const TWR& twr = TWR{}) {
   constexpr Sched S = make_sched(N, MAXR);
   constexpr int R = S.rad[P];
   constexpr int NR = N / R;
@@ -436,7 +475,10 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
     const int b = j + S.T * u;
     if (EXACT || b < NR) {
       const int m = b % Ns;
-      if constexpr (P > 0) {
+      if constexpr (P > 0 && TWR::kHoisted) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], twr.template get<P>(u, r));
+      } else if constexpr (P > 0) {
         const C* twp = tw + sched_twoff(S, P);
 #pragma unroll
         for (int r = 1; r < R; ++r) v[u][r] = cmul(v[u][r], __ldg(twp + (r - 1) * Ns + m));
@@ -455,7 +497,7 @@ __device__ __forceinline__ void stockham_pass(IO& io, const SM& sm, C* smem, con
   }
   if constexpr (!LAST) {
     io.bar();
-    stockham_pass<C, N, DIR, P + 1, MAXR>(io, sm, smem, tw, j, active);
+    stockham_pass<C, N, DIR, P + 1, MAXR>(io, sm, smem, tw, j, active, twr);
   }
 }
 
@@ -739,31 +781,41 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
 // lines q in, conjugate twiddle, inverse radix-8 step, then the x-IFFT of each line k.
 // Line addressing (complex elements): line (l0, l1, r) starts at base + l0·s0 + l1·s1 + r·tstride,
 // r = k or q; the t stride along a line is 1.
-template <int N> struct XZ8Cfg {
-  static constexpr Sched S = make_sched(N);
-  static constexpr int T = S.T, THREADS = 8 * T, LS = N + (N >> 4);
+#ifndef DFFT_XZ8_MAXR32
+#define DFFT_XZ8_MAXR32 1
+#endif
+template <int N, int ES> struct XZ8Cfg {
+  // fp32 lines of >= 512 points: radix-32 passes (1024 = 32·32, two passes), as the TMA kernels
+  static constexpr int MAXR = (DFFT_XZ8_MAXR32 && ES == 8 && N >= 512 && N % 32 == 0) ? 32 : 16;
+  static constexpr Sched S = make_sched(N, MAXR);
+  // one pad slot per 2^SH elements: the first pass scatters to b·MAXR + r, conflict-free per half-warp
+  static constexpr int SH = MAXR == 32 ? 5 : 4;
+  static constexpr int T = S.T, THREADS = 8 * T, LS = N + (N >> SH);
   static constexpr bool OK = THREADS <= 1024 && THREADS >= 64;
   // 8 padded lines in shared memory; minimum resident CTAs for __launch_bounds__: 2 where two
-  // fit by shared memory and still leave 64 (f32) / 128 (f64) registers a thread — the budgets
-  // the radix-16 butterflies compile in without spills (f32 N = 1024: 64) — else 1
-  static constexpr int smem(int es) { return 8 * LS * es; }
-  static constexpr bool fits(int es) { return smem(es) <= 227 * 1024; }
-  static constexpr int minb(int es) {
-    return 2 * (smem(es) + 1024) <= 228 * 1024 && 2 * THREADS * (es == 16 ? 128 : 64) <= 65536 ? 2 : 1;
-  }
+  // fit by shared memory and still leave 64 (f32, radix 16) / 128 (f64 or radix 32) registers a
+  // thread — the budgets the butterflies compile in without spills — else 1
+  static constexpr int SMEM = 8 * LS * ES;
+  static constexpr bool FITS = SMEM <= 227 * 1024;
+  static constexpr int MINB =
+      2 * (SMEM + 1024) <= 228 * 1024 && 2 * THREADS * (ES == 16 || MAXR == 32 ? 128 : 64) <= 65536 ? 2 : 1;
 };
-template <typename C, int N, int DIR> struct XZ8IO : GIO<C, true> {
+template <int SH> struct PadSM {
+  int base;
+  __device__ __forceinline__ int operator()(int t) const { return base + t + (t >> SH); }
+};
+template <typename C, int N, int DIR, int SH> struct XZ8IO : GIO<C, true> {
   static constexpr bool kSyncAfterLoad = DIR > 0;  // inverse: pass 0 reads the line from smem in place
   const C* src;  // forward: this line in global memory; inverse: unused (smem)
   C* dst;        // inverse: this line in global memory
   C* line;       // this line in shared memory, ContigSM positions (base applied)
   __device__ __forceinline__ C load(int t) const {
     if constexpr (DIR < 0) return src[t];
-    else return line[t + (t >> 4)];
+    else return line[t + (t >> SH)];
   }
   __device__ __forceinline__ void store(int t, C v) const {
     if constexpr (DIR < 0) {
-      line[t + (t >> 4)] = v;
+      line[t + (t >> SH)] = v;
     } else {
       if (this->scale != 1) {
         v.x *= this->scale;
@@ -775,9 +827,10 @@ template <typename C, int N, int DIR> struct XZ8IO : GIO<C, true> {
 };
 
 template <typename Real, int N, int DIR>
-__global__ void __launch_bounds__(XZ8Cfg<N>::THREADS, XZ8Cfg<N>::minb(2 * sizeof(Real))) fft_xz8_kernel(const __grid_constant__ PassArgs a) {
+__global__ void __launch_bounds__(XZ8Cfg<N, 2 * sizeof(Real)>::THREADS, XZ8Cfg<N, 2 * sizeof(Real)>::MINB)
+    fft_xz8_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
-  using Cfg = XZ8Cfg<N>;
+  using Cfg = XZ8Cfg<N, 2 * sizeof(Real)>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int li = threadIdx.x / Cfg::T, j = threadIdx.x % Cfg::T;
@@ -787,18 +840,18 @@ __global__ void __launch_bounds__(XZ8Cfg<N>::THREADS, XZ8Cfg<N>::minb(2 * sizeof
   const C* tw = reinterpret_cast<const C*>(a.tw);
   const C* tw2 = reinterpret_cast<const C*>(a.tw2);  // w_Nz^e, e < Nz (sign DIR)
   C* line = smem + li * Cfg::LS;
-  XZ8IO<C, N, DIR> io;
+  XZ8IO<C, N, DIR, Cfg::SH> io;
   io.scale = (Real)a.scale;
   io.line = line;
-  ContigSM sm{li * Cfg::LS};
+  PadSM<Cfg::SH> sm{li * Cfg::LS};
   if constexpr (DIR < 0) {
     io.src = in + li * a.in.tstride;  // x-line k = li
-    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, true);
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, smem, tw, j, true);
     __syncthreads();
     for (int t = threadIdx.x; t < N; t += Cfg::THREADS) {  // radix-8 step across the 8 lines
       C v[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = smem[k * Cfg::LS + t + (t >> 4)];
+      for (int k = 0; k < 8; ++k) v[k] = smem[k * Cfg::LS + t + (t >> Cfg::SH)];
       dft<DIR, 8>(v);
       out[t] = v[0];
 #pragma unroll
@@ -825,12 +878,12 @@ __global__ void __launch_bounds__(XZ8Cfg<N>::THREADS, XZ8Cfg<N>::minb(2 * sizeof
         for (int q = 1; q < 8; ++q) v[it][q] = cmul(v[it][q], __ldg(tw2 + l1 * q));
         dft<DIR, 8>(v[it]);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) smem[k * Cfg::LS + t + (t >> 4)] = v[it][k];
+        for (int k = 0; k < 8; ++k) smem[k * Cfg::LS + t + (t >> Cfg::SH)] = v[it][k];
       }
     }
     __syncthreads();
     io.dst = out + li * a.out.tstride;  // x-line k = li
-    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, true);
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, smem, tw, j, true);
   }
 }
 
@@ -844,7 +897,8 @@ template <typename Real, int N> struct StridedCfg {
 #define DFFT_STRIDED_W0 64
 #endif
   static constexpr int W0 = DFFT_STRIDED_W0 / ES;  // row segment bytes / element size
-  static constexpr int Wthr = S.T * W0 >= 256 ? W0 : 256 / S.T;
+  // whole 32 B sectors per row (see TmaCfg: partial-sector stores cost a DRAM read each)
+  static constexpr int Wthr = S.T * W0 >= 256 ? W0 : (256 / S.T + 32 / ES - 1) / (32 / ES) * (32 / ES);
   static constexpr int Wcap = (96 * 1024) / (N * ES) >= 1 ? (96 * 1024) / (N * ES) : 1;
   static constexpr int W = Wthr < Wcap ? Wthr : (Wcap >= 8 ? 8 : Wcap >= 4 ? 4 : Wcap >= 2 ? 2 : 1);
   static constexpr int THREADS = S.T * W;
@@ -1055,7 +1109,11 @@ template <typename Real, int N> struct TmaCfg {
 #endif
   // fp32 lines of >= 512 points use radix-32 passes (1024 = 32·32: two passes, fewer barriers and
   // less shared-memory traffic per tile); fp64 keeps radix 16 (register budget)
-  static constexpr int MAXR = (DFFT_TMA_MAXR32 && ES == 8 && N >= 512 && N % 32 == 0) ? 32 : 16;
+  // fp64 lines with a factor 5 (480, 720): radix-8 passes.  A thread holds ceil(rmax/R)·R values of
+  // a radix-R pass; at rmax = 16 the radix-3/5 passes of 720 need 18-20 complex doubles and the
+  // kernel spilled 1.2 KB a thread (r02 ptxas), at rmax = 8 it needs 9-10.
+  static constexpr int MAXR =
+      (DFFT_TMA_MAXR32 && ES == 8 && N >= 512 && N % 32 == 0) ? 32 : (ES == 16 && N % 5 == 0) ? 8 : 16;
   static constexpr Sched S = make_sched(N, MAXR);
 #ifndef DFFT_TMA_ROWB
 #define DFFT_TMA_ROWB 64
@@ -1064,12 +1122,23 @@ template <typename Real, int N> struct TmaCfg {
 #define DFFT_TMA_MINTHR 256
 #endif
   static constexpr int W0 = DFFT_TMA_ROWB / ES;  // row segment of a tile (bytes / element size)
-  static constexpr int W = S.T * W0 >= DFFT_TMA_MINTHR ? W0 : DFFT_TMA_MINTHR / S.T;
-  static constexpr int THREADS = S.T * W;
   static constexpr int NS = 2;
+  static constexpr int R0 = S.rad[0];
+  static constexpr size_t smem_for(int w) {
+    return (size_t)(NS * N * w + N * w + (N / R0) * (w * ES < 128 ? w : 0)) * ES + NS * 8 + 16;
+  }
+  // at least DFFT_TMA_MINTHR threads, in whole 32 B sectors per tile row: a row that ends inside a
+  // sector (f64 N = 768: 5 columns = 80 B) makes every tile store a partial-sector write, which
+  // L2 completes with a DRAM read (r02: the f64 768 strided pass ran at 1.6 TB/s).  Round up to a
+  // sector multiple while the tile fits, else down.
+  static constexpr int SECT = 32 / ES;
+  static constexpr int Wraw = S.T * W0 >= DFFT_TMA_MINTHR ? W0 : DFFT_TMA_MINTHR / S.T;
+  static constexpr int Wup = (Wraw + SECT - 1) / SECT * SECT;
+  static constexpr int Wdn = Wraw >= SECT ? Wraw / SECT * SECT : Wraw;
+  static constexpr int W = (smem_for(Wup) <= 227 * 1024 && 2 * Wup <= 256 && S.T * Wup <= 1024) ? Wup : Wdn;
+  static constexpr int THREADS = S.T * W;
   static constexpr int BOXR = largest_divisor_le(N, 256);
   static constexpr int NBOX = N / BOXR;
-  static constexpr int R0 = S.rad[0];
   static constexpr int PAD = (W * ES < 128) ? W : 0;
   static constexpr int STAGE_ELEMS = N * W;
   static constexpr int WORK_ELEMS = N * W + (N / R0) * PAD;
@@ -1184,6 +1253,14 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
       if (tile < total) issue(tile, s);
     }
   }
+  // twiddles in registers where they are few (M-point z passes of the xz8 plan: 14 at M = 128)
+#ifndef DFFT_TW_HOIST_MAX
+#define DFFT_TW_HOIST_MAX 16
+#endif
+  using TH = TwHoist<C, N, Cfg::MAXR>;
+  constexpr bool kHoist = TH::K > 0 && TH::K <= DFFT_TW_HOIST_MAX;
+  TH twh;
+  if constexpr (kHoist) twh.template fill<1>(reinterpret_cast<const C*>(a.tw), j);
   __syncthreads();
   int it = 0;
   for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
@@ -1220,7 +1297,8 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     io.bytes = kBytes;
     mbar_wait(&bars[s], parity);
     StridedSM<Cfg::W, Cfg::R0, Cfg::PAD> sm{c};
-    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, work, reinterpret_cast<const C*>(a.tw), j, active);
+    if constexpr (kHoist) stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, work, reinterpret_cast<const C*>(a.tw), j, active, twh);
+    else stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, work, reinterpret_cast<const C*>(a.tw), j, active);
     if constexpr (DCT < 0) {  // forward R2R: finish the row pairs (k, N−k) of the output tile
       constexpr bool DST = DCT == -2;
       constexpr int NP = (N / 2 + Cfg::S.T) / Cfg::S.T;  // pairs per thread (upper bound)

@@ -66,13 +66,16 @@ KernelInfo make_strided() {
 template <typename Real, int N, int DIR>
 KernelInfo make_xz8() {
   KernelInfo k;
-  if constexpr (XZ8Cfg<N>::OK && XZ8Cfg<N>::fits(2 * sizeof(Real))) {
-    using Cfg = XZ8Cfg<N>;
+  using Cfg = XZ8Cfg<N, (int)sizeof(Real) * 2>;
+  // only where two CTAs fit an SM: with one (f32 N = 2048, f64 N = 1024: 135-139 KB of lines) the
+  // fused pass measured 1.3x slower than the plain x pass and the plan keeps the whole-axis passes
+  if constexpr (Cfg::OK && Cfg::FITS && Cfg::MINB == 2) {
     k.fn = (const void*)&fft_xz8_kernel<Real, N, DIR>;
     k.threads = Cfg::THREADS;
     k.per_cta = 1;  // one (y, z1) pair of 8 lines per CTA
-    k.smem = (size_t)8 * Cfg::LS * sizeof(Real) * 2;
+    k.smem = (size_t)Cfg::SMEM;
     k.twlen = sched_twlen(Cfg::S);
+    k.tma_maxr = Cfg::MAXR;  // the twiddle tables follow its radix schedule
   }
   return k;
 }
