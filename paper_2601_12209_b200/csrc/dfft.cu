@@ -576,7 +576,7 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
     return DFFT_SUCCESS;
   }
   ST(get_kernel(family, n, pl->f64, pl->dir, &s.k));
-  ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw, family == kContigXZ8 ? s.k.tma_maxr : 16));
+  ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw, is_contig(family) ? s.k.tma_maxr : 16));
   if (s.k.generic) {  // the radix schedule at run time
     s.a.gen = make_sched(n);
     s.a.gen_per = s.k.per_cta;
@@ -3022,7 +3022,7 @@ dfft_status_t dfft_fft1d(const void* in, void* out, int64_t n, int64_t howmany, 
   CU(cudaGetDevice(&dev));
   Stage s;
   ST(get_kernel(kContig, (int)n, f64 != 0, sign, &s.k));
-  ST(get_twiddles((int)n, f64 != 0, sign, dev, &s.a.tw));
+  ST(get_twiddles((int)n, f64 != 0, sign, dev, &s.a.tw, s.k.tma_maxr));
   if (s.k.generic) {
     s.a.gen = make_sched((int)n);
     s.a.gen_per = s.k.per_cta;

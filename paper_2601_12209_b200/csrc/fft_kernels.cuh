@@ -574,16 +574,29 @@ template <typename C, bool UNIT_T = false, bool SPEC = false, bool TB = false> s
   }
 };
 
-struct ContigSM {
+// shared-memory slot of element t of a line: one pad slot per 2^SH elements
+template <int SH> struct PadSM {
   int base;
-  __device__ __forceinline__ int operator()(int t) const { return base + t + (t >> 4); }
+  __device__ __forceinline__ int operator()(int t) const { return base + t + (t >> SH); }
 };
 
-template <int N> struct ContigCfg {
-  static constexpr Sched S = make_sched(N);
+#ifndef DFFT_CONTIG_MAXR32
+#define DFFT_CONTIG_MAXR32 1
+#endif
+template <int N, int ES> struct ContigCfg {
+  // fp32 lines of >= 512 points: radix-32 passes (1024 = 32·32), as the xz8 and TMA kernels
+  static constexpr int MAXR = (DFFT_CONTIG_MAXR32 && ES == 8 && N >= 512 && N % 32 == 0) ? 32 : 16;
+  static constexpr Sched S = make_sched(N, MAXR);
+  static constexpr int SH = MAXR == 32 ? 5 : 4;  // one pad slot per 2^SH elements (see XZ8Cfg)
   static constexpr int LPC = S.T >= 256 ? 1 : 256 / S.T;  // lines per CTA
   static constexpr int THREADS = S.T * LPC;
-  static constexpr int LS = N + (N >> 4);  // padded line stride in smem
+  static constexpr int LS = N + (N >> SH);  // padded line stride in smem
+  // resident CTAs the register budget allows: 64 registers a thread (f32, radix 16: what ptxas used
+  // unbounded) or 128 (f64, radix 32).  A bare minBlocks = 1 lets ptxas take up to 255 and halves
+  // the occupancy (r02: cfg5's f64 x-stages 0.97 -> 1.29 ms, 1.42 -> 2.26 ms)
+  static constexpr int BUDGET = (ES == 16 || MAXR == 32) ? 128 : 64;
+  static constexpr int MINB_RAW = 65536 / (THREADS * BUDGET);
+  static constexpr int MINB = MINB_RAW < 1 ? 1 : MINB_RAW > 4 ? 4 : MINB_RAW;
 };
 
 // R2C / C2R (reading R8; "exploiting Hermitian symmetry"): a real line of nx = 2N samples
@@ -671,10 +684,10 @@ template <typename C, int N, bool DST = false> struct DctXInvIO : GIO<C, true> {
 
 // MODE 0 c2c, 1 R2C, 2 C2R, 3 / 4 DCT-II / DCT-III of real x-lines, 5 / 6 DST-II / DST-III
 template <typename Real, int N, int DIR, int MODE, bool TB = false>
-__global__ void __launch_bounds__(ContigCfg<N>::THREADS)
+__global__ void __launch_bounds__(ContigCfg<N, 2 * sizeof(Real)>::THREADS, ContigCfg<N, 2 * sizeof(Real)>::MINB)
 fft_contig_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
-  using Cfg = ContigCfg<N>;
+  using Cfg = ContigCfg<N, 2 * sizeof(Real)>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int li = threadIdx.x / Cfg::S.T;
@@ -691,18 +704,18 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
       l0 = line - l1 * a.L0;
     }
   }
-  ContigSM sm{li * Cfg::LS};
+  PadSM<Cfg::SH> sm{li * Cfg::LS};
   const C* tw = reinterpret_cast<const C*>(a.tw);
   if constexpr (MODE == 0) {
     GIO<C, true, false, TB> io;
     io.init(a.in, a.out, l0, l1, a.scale);
-    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, smem, tw, j, active);
   } else if constexpr (MODE == 1) {
     SmemZ<C> io;
     io.init(a.in, a.out, l0, l1, a.scale);
     C* zb = smem + li * Cfg::LS;
     io.zb = zb;
-    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, smem, tw, j, active);
     __syncthreads();
     if (active) {
       const C* tw2 = reinterpret_cast<const C*>(a.tw2);
@@ -720,7 +733,7 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
     C2RIO<C, N> io;
     io.init(a.in, a.out, l0, l1, a.scale);
     io.tw2 = reinterpret_cast<const C*>(a.tw2);
-    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, smem, tw, j, active);
   } else if constexpr (MODE == 3 || MODE == 5) {  // forward DCT-II / DST-II of real x-lines of length 2N
     using R = Real;
     constexpr bool DST = MODE == 5;
@@ -728,7 +741,7 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
     io.init(a.in, a.out, l0, l1, a.scale);
     C* zb = smem + li * Cfg::LS;
     io.zb = zb;
-    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, smem, tw, j, active);
     __syncthreads();
     if (active) {
       const C* tw2 = reinterpret_cast<const C*>(a.tw2);  // exp(-2πi k / 2N)
@@ -761,7 +774,7 @@ fft_contig_kernel(const __grid_constant__ PassArgs a) {
     if (active)
       for (int t = j; t < N; t += Cfg::S.T) zb[t] = io.GIO<C, true>::load(t);
     __syncthreads();
-    stockham_pass<C, N, DIR, 0>(io, sm, smem, tw, j, active);
+    stockham_pass<C, N, DIR, 0, Cfg::MAXR>(io, sm, smem, tw, j, active);
     __syncthreads();
     if (active) {  // output element q = (x_{2q}, x_{2q+1}) = (v_q, v_{2N-1-q}); coalesced stores
       const R* vr = reinterpret_cast<const R*>(zb);
@@ -800,15 +813,11 @@ template <int N, int ES> struct XZ8Cfg {
   static constexpr int MINB =
       2 * (SMEM + 1024) <= 228 * 1024 && 2 * THREADS * (ES == 16 || MAXR == 32 ? 128 : 64) <= 65536 ? 2 : 1;
 };
-template <int SH> struct PadSM {
-  int base;
-  __device__ __forceinline__ int operator()(int t) const { return base + t + (t >> SH); }
-};
 template <typename C, int N, int DIR, int SH> struct XZ8IO : GIO<C, true> {
   static constexpr bool kSyncAfterLoad = DIR > 0;  // inverse: pass 0 reads the line from smem in place
   const C* src;  // forward: this line in global memory; inverse: unused (smem)
   C* dst;        // inverse: this line in global memory
-  C* line;       // this line in shared memory, ContigSM positions (base applied)
+  C* line;       // this line in shared memory, PadSM positions (base applied)
   __device__ __forceinline__ C load(int t) const {
     if constexpr (DIR < 0) return src[t];
     else return line[t + (t >> SH)];

@@ -7,7 +7,7 @@ namespace dfft {
 namespace {
 template <typename Real, int N, int DIR, int MODE = 0>
 KernelInfo make_contig() {
-  using Cfg = ContigCfg<N>;
+  using Cfg = ContigCfg<N, (int)sizeof(Real) * 2>;
   KernelInfo k;
   k.fn = (const void*)&fft_contig_kernel<Real, N, DIR, MODE>;
   if constexpr (MODE == 0) k.fn_tb = (const void*)&fft_contig_kernel<Real, N, DIR, 0, true>;
@@ -15,6 +15,7 @@ KernelInfo make_contig() {
   k.per_cta = Cfg::LPC;
   k.smem = (Cfg::S.npass > 1 || MODE == 1 || MODE >= 3) ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
   k.twlen = sched_twlen(Cfg::S);
+  k.tma_maxr = Cfg::MAXR;  // the twiddle tables follow its radix schedule
   return k;
 }
 template <typename Real, int N, int DIR, bool DST = false>
