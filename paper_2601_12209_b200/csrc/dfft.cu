@@ -1251,6 +1251,9 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
     return Lr.R1 + Zn * g.Y1n(ir) * (g.Xlo(is) + g.x0(is, k));
   };
   const long long nxl = xreal(pl) ? g.nx / 2 : g.nx;
+  // P1 = 1 with fused stores: the y-IFFT writes natural x-lines and the x-IFFT reads them whole,
+  // instead of R1's wy-column blocks (64 B pieces at a plane pitch: 2.4 ms at 1×2, 1024³ c64)
+  const bool nat1 = p2p && g.P1 == 1 && !getenv("DFFT_NO_NAT1");
   rp.A.resize(K);
   rp.B.resize(K);
   rp.E1.resize(K);
@@ -1312,6 +1315,15 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
       // blocked input (adjacent z adjacent) and per-tile contiguous blocked output: z fastest
       B.a.g0 = tile_g0(1, "DFFT_G0_INV_B");
     }
+    if (nat1) {  // 1×P2: T1⁻¹ is local; natural [z][y][x] (x over the Xn spectral columns) in R1
+      B.out = {kWs, (L.R1 + x0) * es};
+      set_side(B.a.out, Xn, 1, Y1n * Xn);
+      B.a.scale = 1.0;
+      ST(finish_stage(pl, B, fam_y(pl), (int)g.ny, xc, Zn, nullptr, nullptr));
+      rp.E2[k].comm = 0;  // T1⁻¹ has no peer
+      rp.E2[k].fused = true;
+      continue;
+    }
     B.out = {kWs, 0};
     B.out_bases.push_back({kWs, 0});
     if (p2p)
@@ -1356,6 +1368,14 @@ dfft_status_t build_inverse(dfft_plan_t pl, const Geo& g, RankPlan& rp) {
   // ---- stage C: x-IFFT of lines (l0 = y, l1 = z); input segmented by (source row, chunk); ×1/N
   Stage& C = rp.C;
   C.in = {kWs, 0};
+  if (nat1) {  // whole x-lines from the natural layout stage B wrote
+    C.in = {kWs, L.R1 * es};
+    set_side(C.a.in, 1, Xn, Y1n * Xn);
+    C.out = {kUserOut, 0};
+    set_side(C.a.out, 1, nxl, Y1n * nxl);
+    C.a.scale = (xreal(pl) ? 2.0 : 1.0) / ((double)g.nx * (double)g.ny * (double)g.nz);
+    return finish_stage(pl, C, fam_x_inv(pl), (int)nxl, Y1n, Zn, nullptr, nullptr);
+  }
   Segs cseg;
   if (p2p) {  // R1' [source][xt][z][y][wy]: one segment per (source, column block)
     long long src = L.R1;
