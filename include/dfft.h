@@ -114,6 +114,10 @@ typedef enum { DFFT_FORWARD = -1, DFFT_INVERSE = 1 } dfft_direction_t;
  *   same plan, which plan creation checks): DFFT_EXCHANGE=p2p|ce|hybrid|nccl, DFFT_NO_BC=1 (no
  *   B→C pipeline), DFFT_NO_BC_1XP=1 (no B→C pipeline on 1×P2 forwards), DFFT_NVL_SMS=n (SMs of
  *   the NVLink-bound stage of a pipelined pair, default 80).
+ *   Layout overrides (local to a rank, any communicator): DFFT_NO_XZ8=1 (single GPU: the
+ *   whole-axis x, z, y passes instead of the x-FFT fused with a radix-8 z step),
+ *   DFFT_NO_NAT1=1 (1×P2 fused stores: the inverse y-IFFT writes wy-column blocks instead of
+ *   natural x-lines).  dfft_plan_describe reports the plan each resolves to.
  */
 #define DFFT_FLAG_CHUNKS(k) ((uint64_t)((k) & 0xff))
 #define DFFT_FLAG_NO_OVERLAP ((uint64_t)1 << 8)

@@ -576,6 +576,22 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
     return DFFT_SUCCESS;
   }
   ST(get_kernel(family, n, pl->f64, pl->dir, &s.k));
+  // x-FFTs of plans whose T1 exchange crosses ranks (P1 > 1): radix-16 passes.  Their epilogue
+  // (forward) stores into peers' windows, where the radix-32 kernel's fewer, wider threads keep
+  // fewer stores in flight, and the inverse runs beside the NVLink-bound y-IFFT (r02, 1024³ at
+  // 2×2: fwd x 1.53 -> 1.65 ms, inverse y-IFFT 0.48 -> 0.66 ms a chunk with radix 32)
+  if (family == kContig && s.k.r16_fn && pl->P1 > 1 && !getenv("DFFT_CONTIG_R32")) {
+    s.k.fn = s.k.r16_fn;
+    s.k.fn_tb = s.k.r16_fn_tb;
+    s.k.threads = s.k.r16_threads;
+    s.k.per_cta = s.k.r16_per_cta;
+    s.k.smem = s.k.r16_smem;
+    s.k.tma_maxr = 16;
+    if (s.k.smem > 48 * 1024) {
+      CU(cudaFuncSetAttribute(s.k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.k.smem));
+      CU(cudaFuncSetAttribute(s.k.fn_tb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.k.smem));
+    }
+  }
   ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.a.tw, is_contig(family) ? s.k.tma_maxr : 16));
   if (s.k.generic) {  // the radix schedule at run time
     s.a.gen = make_sched(n);

@@ -583,9 +583,10 @@ template <int SH> struct PadSM {
 #ifndef DFFT_CONTIG_MAXR32
 #define DFFT_CONTIG_MAXR32 1
 #endif
-template <int N, int ES> struct ContigCfg {
+template <int N, int ES, bool R32 = true> struct ContigCfg {
   // fp32 lines of >= 512 points: radix-32 passes (1024 = 32·32), as the xz8 and TMA kernels
-  static constexpr int MAXR = (DFFT_CONTIG_MAXR32 && ES == 8 && N >= 512 && N % 32 == 0) ? 32 : 16;
+  // (R32 = false: the radix-16 variant, for x-FFTs that store into peers' windows)
+  static constexpr int MAXR = (R32 && DFFT_CONTIG_MAXR32 && ES == 8 && N >= 512 && N % 32 == 0) ? 32 : 16;
   static constexpr Sched S = make_sched(N, MAXR);
   static constexpr int SH = MAXR == 32 ? 5 : 4;  // one pad slot per 2^SH elements (see XZ8Cfg)
   static constexpr int LPC = S.T >= 256 ? 1 : 256 / S.T;  // lines per CTA
@@ -683,11 +684,11 @@ template <typename C, int N, bool DST = false> struct DctXInvIO : GIO<C, true> {
 };
 
 // MODE 0 c2c, 1 R2C, 2 C2R, 3 / 4 DCT-II / DCT-III of real x-lines, 5 / 6 DST-II / DST-III
-template <typename Real, int N, int DIR, int MODE, bool TB = false>
-__global__ void __launch_bounds__(ContigCfg<N, 2 * sizeof(Real)>::THREADS, ContigCfg<N, 2 * sizeof(Real)>::MINB)
+template <typename Real, int N, int DIR, int MODE, bool TB = false, bool R32 = true>
+__global__ void __launch_bounds__(ContigCfg<N, 2 * sizeof(Real), R32>::THREADS, ContigCfg<N, 2 * sizeof(Real), R32>::MINB)
 fft_contig_kernel(const __grid_constant__ PassArgs a) {
   using C = typename CT<Real>::type;
-  using Cfg = ContigCfg<N, 2 * sizeof(Real)>;
+  using Cfg = ContigCfg<N, 2 * sizeof(Real), R32>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* smem = reinterpret_cast<C*>(smem_raw);
   const int li = threadIdx.x / Cfg::S.T;

@@ -16,6 +16,14 @@ KernelInfo make_contig() {
   k.smem = (Cfg::S.npass > 1 || MODE == 1 || MODE >= 3) ? (size_t)Cfg::LPC * Cfg::LS * sizeof(Real) * 2 : 0;
   k.twlen = sched_twlen(Cfg::S);
   k.tma_maxr = Cfg::MAXR;  // the twiddle tables follow its radix schedule
+  if constexpr (MODE == 0 && Cfg::MAXR == 32) {
+    using C16 = ContigCfg<N, (int)sizeof(Real) * 2, false>;
+    k.r16_fn = (const void*)&fft_contig_kernel<Real, N, DIR, 0, false, false>;
+    k.r16_fn_tb = (const void*)&fft_contig_kernel<Real, N, DIR, 0, true, false>;
+    k.r16_threads = C16::THREADS;
+    k.r16_per_cta = C16::LPC;
+    k.r16_smem = (size_t)C16::LPC * C16::LS * sizeof(Real) * 2;
+  }
   return k;
 }
 template <typename Real, int N, int DIR, bool DST = false>

@@ -30,6 +30,11 @@ struct KernelInfo {
   int tma_threads = 0, tma_w = 0, tma_boxr = 0, tma_maxr = 16;  // tma_maxr: its radix schedule
   size_t tma_smem = 0;
   bool generic = false;  // fft_generic_kernel: the radix schedule is passed at run time (PassArgs::gen)
+  // contig c2c with radix-32 passes: the radix-16 variant (x-FFTs whose epilogue stores to peers)
+  const void* r16_fn = nullptr;
+  const void* r16_fn_tb = nullptr;
+  int r16_threads = 0, r16_per_cta = 0;
+  size_t r16_smem = 0;
 };
 
 // Supported axis lengths: 2^a (2..4096), 3·2^a (3..3072), and the paper's
