@@ -1263,12 +1263,14 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
       if (tile < total) issue(tile, s);
     }
   }
-  // twiddles in registers where they are few (M-point z passes of the xz8 plan: 14 at M = 128)
-#ifndef DFFT_TW_HOIST_MAX
-#define DFFT_TW_HOIST_MAX 16
+  // twiddles in registers where they take at most 256 B a thread (32 in fp32: the 1024-row y pass
+  // has 31, the M = 128 z pass 14; 16 in fp64) and the CTA is at most 256 threads (larger CTAs —
+  // 840: 840 threads, 384: 288 — have no register room and spilled)
+#ifndef DFFT_TW_HOIST_BYTES
+#define DFFT_TW_HOIST_BYTES 256
 #endif
   using TH = TwHoist<C, N, Cfg::MAXR>;
-  constexpr bool kHoist = TH::K > 0 && TH::K <= DFFT_TW_HOIST_MAX;
+  constexpr bool kHoist = TH::K > 0 && TH::K * Cfg::ES <= DFFT_TW_HOIST_BYTES && Cfg::THREADS <= 256;
   TH twh;
   if constexpr (kHoist) twh.template fill<1>(reinterpret_cast<const C*>(a.tw), j);
   __syncthreads();
