@@ -397,11 +397,12 @@ def main():
                                "stage_C": "y-FFT (strided TMA)"},
                        "inv": {"stage_A": "y-IFFT (strided TMA)", "stage_B": "z-IFFT (strided TMA, writes [y][z][x])",
                                "stage_C": "x-IFFT (contig, 1/N)"}}
-    else:
-        stage_names = {"fwd": {"stage_A": "x-FFT (contig, fused T1 pack/store)",
-                               "stage_B": "y-FFT (strided, fused T2 pack/store)", "stage_C": "z-FFT (strided)"},
-                       "inv": {"stage_A": "z-IFFT (strided, fused T2 pack/store)",
-                               "stage_B": "y-IFFT (strided, fused T1 pack/store)",
+    else:  # fused stores: the epilogue writes the peers' windows; NCCL / CE: it packs local send blocks
+        pk = "fused T{} pack/store" if fused else "T{} pack into send blocks"
+        stage_names = {"fwd": {"stage_A": f"x-FFT (contig, {pk.format(1)})",
+                               "stage_B": f"y-FFT (strided, {pk.format(2)})", "stage_C": "z-FFT (strided)"},
+                       "inv": {"stage_A": f"z-IFFT (strided, {pk.format(2)})",
+                               "stage_B": f"y-IFFT (strided, {pk.format(1)})",
                                "stage_C": "x-IFFT (contig, fused unpack, 1/N)"}}
     stages = []
     for tag, pt, bt in (("fwd", pf, bf), ("inv", pi, bi)):

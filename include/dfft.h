@@ -277,7 +277,8 @@ dfft_status_t dfft_plan_set_profiling(dfft_plan_t plan, int on);
 dfft_status_t dfft_plan_phase_times(dfft_plan_t plan, double ms[5], long long launches[5], int reset);
 dfft_status_t dfft_plan_stage_bytes(dfft_plan_t plan, double bytes[5]);
 /* Plan description (rank 0's stages): one text line per stage launch unit, "<phase> <kernel
- * family> n=<length> L0=.. L1=.. in_tstride=.. out_tstride=.. tma=0|1", NUL-terminated in buf
+ * family> n=<length> L0=.. L1=.. in_tstride=.. out_tstride=.. tma=0|1 maxr=<largest radix of the
+ * kernel's passes>", NUL-terminated in buf
  * (caller-owned, len bytes).  DFFT_ERR_INVALID_VALUE when it does not fit (buf holds a truncated
  * copy).  Families: contig, strided, contig_r2c, contig_c2r, contig_dct, strided_dct, contig_dst,
  * strided_dst, xz8 (the single-GPU x-FFT fused with a radix-8 z step). */

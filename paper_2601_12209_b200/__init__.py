@@ -330,7 +330,7 @@ class Plan:
         return {PHASES[q]: b[q] for q in range(5)}
 
     def describe(self):
-        """Rank 0's stages: [{"phase", "family", "n", "L0", "L1", "in_tstride", "out_tstride", "tma"}]."""
+        """Rank 0's stages: [{"phase", "family", "n", "L0", "L1", "in_tstride", "out_tstride", "tma", "maxr"}]."""
         buf = ctypes.create_string_buffer(8192)
         _check(lib().dfft_plan_describe(self.h, buf, len(buf)), "dfft_plan_describe")
         out = []

@@ -3030,11 +3030,13 @@ dfft_status_t dfft_plan_describe(dfft_plan_t pl, char* buf, size_t len) {
   const RankPlan& rp = pl->ranks[0];
   std::string out;
   auto one = [&](const char* phase, const Stage& s) {
-    if (s.empty) return;
+    if (s.empty || s.n == 0) return;  // (n = 0: a stage the plan runs as chunks, rp.Cc)
     char line[256];
     const int f = s.family >= 0 && s.family <= kContigXZ8 ? s.family : 0;
-    snprintf(line, sizeof line, "%s %s n=%d L0=%lld L1=%lld in_tstride=%lld out_tstride=%lld tma=%d\n", phase,
-             fam[f], s.n, s.a.L0, s.a.L1, s.a.in.tstride, s.a.out.tstride, s.tma_variant);
+    // maxr: the largest radix of the kernel that runs (contig / xz8: its own; strided: the TMA variant's)
+    const int maxr = is_contig(s.family) || s.tma_variant == 1 ? s.k.tma_maxr : 16;
+    snprintf(line, sizeof line, "%s %s n=%d L0=%lld L1=%lld in_tstride=%lld out_tstride=%lld tma=%d maxr=%d\n",
+             phase, fam[f], s.n, s.a.L0, s.a.L1, s.a.in.tstride, s.a.out.tstride, s.tma_variant, maxr);
     out += line;
   };
   for (const Stage& s : rp.A) one("stage_A", s);

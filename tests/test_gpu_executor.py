@@ -289,3 +289,19 @@ def test_kernel_launch_counter_counts_graph_replays():
         deltas.append(dfft.kernel_launches() - n0)
     torch.cuda.synchronize()
     assert deltas == [3] * 4, deltas  # three FFT stages per execute, captured or replayed
+
+
+@pytest.mark.parametrize("grid,x_maxr", [((1, 2), 32), ((2, 2), 16)])
+def test_x_radix_by_plan(oracle_mod, grid, x_maxr):
+    # fp32 x-lines of 512: radix-32 passes unless the plan's T1 exchange has remote peers (P1 > 1),
+    # whose x-FFTs keep radix 16; both are checked against the oracle
+    shape = (512, 16, 8)
+    fwd, inv, xs, ys, zs = _run(shape, "pencil", grid, "f32", "p2p", 2)
+    fx = [d for d in fwd.describe() if d["phase"] == "stage_A"]
+    ix = [d for d in inv.describe() if d["phase"] == "stage_C"]
+    assert all(d["family"] == "contig" and d["n"] == 512 and d["maxr"] == x_maxr for d in fx + ix), (fx, ix)
+    a = oracle_mod.gen_complex(5, shape, f32=True)
+    A = oracle_mod.fft3d(a, -1)
+    ef = oracle_mod.rel_l2(_gather(fwd, ys, 1, A), A)
+    er = oracle_mod.rel_l2(_gather(inv, zs, 1, a), a)
+    assert ef <= QUALITY["f32"] and er <= GATE["f32"], (ef, er)
