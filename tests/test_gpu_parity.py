@@ -449,6 +449,7 @@ def _poisson_case(oracle_mod, shape, decomp, grid, prec, spacing, kind="r2c", ex
     ((16, 12, 8), "pencil", (1, 1), (1.0, 1.0, 1.0), "r2c"),
     ((64, 48, 24), "pencil", (1, 1), (0.5, 2.0, 1.5), "r2c"),
     ((32, 24, 16), "pencil", (1, 1), (1.0, 0.25, 3.0), "c2c"),
+    ((128, 12, 256), "pencil", (1, 1), (1.0, 0.5, 2.0), "c2c"),  # the xz8 plan: multiplier in its y pass
     ((48, 24, 12), "pencil", (2, 4), (1.0, 2.0, 0.5), "r2c"),   # fused-store layouts, B->C chunks
     ((96, 48, 24), "pencil", (2, 2), (1.0, 1.0, 1.0), "c2c"),
     ((64, 32, 16), "slab", (4, 1), (2.0, 1.0, 1.0), "r2c"),
