@@ -656,3 +656,22 @@ def test_xz8_matches_whole_axis_plan(shape, monkeypatch):
         torch.cuda.synchronize()
         outs.append(y.cpu().numpy())
     assert rel_l2(outs[0], outs[1]) < 1e-14
+
+
+def _sweep_shapes(count=16, seed=2601):
+    """Seeded 3D shapes over the specialised lengths, <= 2^21 points: the plan picks xz8 or the
+    whole-axis passes, radix 16 or 32, by the rules of DESIGN.md §5 — none chosen by hand."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        s = tuple(int(v) for v in rng.choice(LENGTHS, 3))
+        if 8 <= s[0] * s[1] * s[2] <= (1 << 21) and (s[0], s[1], s[2]) not in out:
+            out.append(s)
+    return out
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape", _sweep_shapes())
+def test_3d_single_gpu_seeded_sweep(oracle_mod, shape, prec):
+    ef, er, ei = _run_single(oracle_mod, shape, "pencil", prec, seed=47)
+    assert ef <= GATE[prec] and er <= GATE[prec] and ei <= GATE[prec], (shape, ef, er, ei)
