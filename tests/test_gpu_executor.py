@@ -305,3 +305,42 @@ def test_x_radix_by_plan(oracle_mod, grid, x_maxr):
     ef = oracle_mod.rel_l2(_gather(fwd, ys, 1, A), A)
     er = oracle_mod.rel_l2(_gather(inv, zs, 1, a), a)
     assert ef <= QUALITY["f32"] and er <= GATE["f32"], (ef, er)
+
+
+def _sim_sweep_cases(count=12, seed=2602):
+    """Seeded (shape, grid, chunks, transport) cases for the simulated product executor: lengths
+    from the specialised set, 2-8 ranks, 1-4 chunks; a grid that does not fit the shape is skipped
+    by plan creation (DFFT_ERR_INVALID_VALUE / UNSUPPORTED)."""
+    from helpers import LENGTHS
+    rng = np.random.default_rng(seed)
+    grids = [(1, 2), (2, 1), (2, 2), (1, 4), (4, 1), (2, 4), (4, 2), (1, 8)]
+    lens = [n for n in LENGTHS if n >= 8]
+    out = []
+    while len(out) < count:
+        s = tuple(int(v) for v in rng.choice(lens, 3))
+        if not (1 << 12) <= s[0] * s[1] * s[2] <= (1 << 20):
+            continue
+        g = grids[int(rng.integers(len(grids)))]
+        out.append((s, g, int(rng.integers(1, 5)), ["p2p", "ce"][int(rng.integers(2))]))
+    return out
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("shape,grid,chunks,exchange", _sim_sweep_cases())
+def test_sim_product_executor_seeded_sweep(oracle_mod, shape, grid, chunks, exchange, prec):
+    try:
+        fwd, inv, xs, ys, zs = _run(shape, "pencil", grid, prec, exchange, chunks)
+    except dfft.DfftError as e:
+        if e.status in (1, 3):  # the grid does not divide / fit this shape
+            pytest.skip(str(e))
+        raise
+    a = oracle_mod.gen_complex(5, shape, f32=(prec == "f32"))
+    A = oracle_mod.fft3d(a, -1)
+    Y = _gather(fwd, ys, 1, A)
+    ef, er = oracle_mod.rel_l2(Y, A), oracle_mod.rel_l2(_gather(inv, zs, 1, a), a)
+    assert ef <= GATE[prec] and er <= GATE[prec], (ef, er)
+    _, fwd_n, _ = _sim_plans(shape, "pencil", grid, "c2c_" + prec, "nccl", chunks)
+    ys_n = [fwd_n.alloc_out(r) for r in range(len(xs))]
+    fwd_n.execute_sim(xs, ys_n)
+    torch.cuda.synchronize()
+    assert np.array_equal(Y, _gather(fwd_n, ys_n, 1, A))
