@@ -264,6 +264,8 @@ dfft_status_t get_kernel(int family, int n, bool f64, int dir, KernelInfo* k) {
     if (k->tma_st_spec_fn)
       CU(cudaFuncSetAttribute(k->tma_st_spec_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_smem));
   }
+  if (k->tma_ip_fn && k->tma_ip_smem > 48 * 1024)
+    CU(cudaFuncSetAttribute(k->tma_ip_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k->tma_ip_smem));
   return DFFT_SUCCESS;
 }
 
@@ -302,6 +304,8 @@ struct Stage {
   int sm_cap = 0;          // > 0: run the persistent variant on at most this many SMs (leaves the
                            // rest to a concurrently running HBM-bound stage)
   int tma_variant = 0;     // 1 = the persistent TMA kernel is used
+  long long ip_grid = 0;   // grid / resident CTAs of the in-place TMA-store variant (0 = not used)
+  int ip_occ = 0;
   const void* tw_tma = nullptr;  // twiddles of the TMA variant's radix schedule
   bool empty = false;
   // last forward stage: which global axis (0 x, 1 y, 2 z) its t / l0 / l1 run along and the
@@ -648,6 +652,14 @@ dfft_status_t finish_stage(dfft_plan_t pl, Stage& s, int family, int n, long lon
         s.tma_variant = 1;
         s.tma_grid = std::min<long long>(tiles, (long long)sms * occ);
         s.tma_occ = occ;
+      }
+      if (s.tma_variant == 1 && s.k.tma_ip_fn && !(getenv("DFFT_TMA_IP") && atoi(getenv("DFFT_TMA_IP")) == 0)) {
+        int occ_ip = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ip, s.k.tma_ip_fn, thr, s.k.tma_ip_smem));
+        if (occ_ip > 0) {
+          s.ip_grid = std::min<long long>(tiles, (long long)sms * occ_ip);
+          s.ip_occ = occ_ip;
+        }
       }
       if (s.tma_variant == 1)  // the TMA variant's own radix schedule
         ST(get_twiddles(n, pl->f64, pl->dir, pl->comm->device, &s.tw_tma, s.k.tma_maxr));
@@ -1503,6 +1515,10 @@ dfft_status_t launch_impl(const Stage& s, const Ctx& c, cudaStream_t st) {
       if (spec && !s.k.tma_st_only && !(use_st && s.tma_variant == 1 && s.k.tma_st_spec_fn)) goto plain;
       if (spec && !s.k.tma_st_only)
         CU(cudaLaunchKernel(s.k.tma_st_spec_fn, dim3((unsigned)grid), dim3(s.k.tma_threads), targs, s.k.tma_smem, st));
+      else if (use_st && !spec && a.out.nbulk == 0 && s.ip_grid > 0 && !s.k.tma_st_only) {
+        const long long gip = s.sm_cap > 0 ? std::min<long long>(s.ip_grid, (long long)s.sm_cap * s.ip_occ) : s.ip_grid;
+        CU(cudaLaunchKernel(s.k.tma_ip_fn, dim3((unsigned)gip), dim3(s.k.tma_threads), targs, s.k.tma_ip_smem, st));
+      }
       else
         CU(cudaLaunchKernel(a.out.nbulk > 0 ? s.k.tma_bk_fn
                             : use_st        ? s.k.tma_st1_fn

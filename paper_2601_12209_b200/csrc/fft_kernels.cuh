@@ -1154,6 +1154,15 @@ template <typename Real, int N> struct TmaCfg {
   static constexpr int WORK_ELEMS = N * W + (N / R0) * PAD;
   static constexpr size_t SMEM = (size_t)(NS * STAGE_ELEMS + WORK_ELEMS) * ES + NS * 8 + 16;
   static constexpr bool OK = S.npass >= 2 && THREADS <= 1024 && SMEM <= 227 * 1024 && 2 * W <= 256;
+  // in-place variant (IP): the passes run in the stage buffer itself (pass 0 reads the whole tile
+  // before it writes), so the shared memory of the separate work tile buys another stage in flight
+  static constexpr int BUF_IP = (WORK_ELEMS * ES + 127) / 128 * 128 / ES;
+  static constexpr int NS_IP = 3 * BUF_IP * ES + 64 <= 227 * 1024 ? 3 : 2;
+  static constexpr size_t SMEM_IP = (size_t)NS_IP * BUF_IP * ES + NS_IP * 8 + 16;
+  // where it measured faster (r02 same-box A/B, tools/ab/tma_inplace_lengths.sh): f32 M = 96 / 192
+  // (the xz8 plan's z passes: 1.43 -> 1.07 ms, 1.36 -> 1.26 ms), f64 128 (0.36 -> 0.34 ms); equal
+  // or slower elsewhere (the 1024-row y pass 2.96 -> 3.05 ms)
+  static constexpr bool IP_PREFER = (ES == 8 && (N == 96 || N == 192)) || (ES == 16 && N == 128);
 };
 
 // DCT (R2R strided stages on the TMA kernel, OM 1 only): -1 forward (permuted loads from the
@@ -1227,19 +1236,22 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_
 // stores at a large stride from the SMs throttles the LSU (r01 ncu: lg_throttle); 2 = the
 // output is segmented into column-blocked windows (possibly peers' over NVLink) and each
 // segment of a tile leaves as one contiguous cp.async.bulk copy.
-template <typename Real, int N, int DIR, int OM, bool SPEC = false, int DCT = 0>
+template <typename Real, int N, int DIR, int OM, bool SPEC = false, int DCT = 0, bool IP = false>
 __global__ void __launch_bounds__(TmaCfg<Real, N>::THREADS)
 fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
                        const __grid_constant__ PassArgs a) {
   constexpr bool TST = OM != 0;
+  static_assert(!IP || (OM == 1 && DCT == 0), "the in-place variant stores its tile with TMA stores");
   using C = typename CT<Real>::type;
   using Cfg = TmaCfg<Real, N>;
+  constexpr int NSK = IP ? Cfg::NS_IP : Cfg::NS;             // stages in flight
+  constexpr int BUF = IP ? Cfg::BUF_IP : Cfg::STAGE_ELEMS;    // elements a stage
   // 1024-byte aligned: TMA destinations need 128 B alignment, and a cluster launch does not
   // otherwise guarantee it for the dynamic shared-memory base
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* stages = reinterpret_cast<C*>(smem_raw);
-  C* work = stages + Cfg::NS * Cfg::STAGE_ELEMS;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(work + Cfg::WORK_ELEMS);
+  C* work = stages + NSK * BUF;  // (IP: the current stage, set per tile)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(IP ? stages + NSK * BUF : work + Cfg::WORK_ELEMS);
   const int c = threadIdx.x % Cfg::W;
   const int j = threadIdx.x / Cfg::W;
   const long long ntile = (a.L0 + Cfg::W - 1) / Cfg::W;
@@ -1252,13 +1264,13 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
     const int c0 = (int)(tx * Cfg::W * 2);
     mbar_expect_tx(&bars[s], kBytes);
     for (int q = 0; q < Cfg::NBOX; ++q)
-      tma_load_tile(stages + s * Cfg::STAGE_ELEMS + q * Cfg::BOXR * Cfg::W, &tmap, a.in.bw, c0, q * Cfg::BOXR, (int)l1,
+      tma_load_tile(stages + s * BUF + q * Cfg::BOXR * Cfg::W, &tmap, a.in.bw, c0, q * Cfg::BOXR, (int)l1,
                     &bars[s]);
   };
   if (threadIdx.x == 0) {
-    for (int s = 0; s < Cfg::NS; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < NSK; ++s) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < Cfg::NS; ++s) {
+    for (int s = 0; s < NSK; ++s) {
       long long tile = blockIdx.x + (long long)s * gridDim.x;
       if (tile < total) issue(tile, s);
     }
@@ -1276,27 +1288,28 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
   __syncthreads();
   int it = 0;
   for (long long tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-    const int s = it % Cfg::NS;
-    const uint32_t parity = (uint32_t)((it / Cfg::NS) & 1);
+    const int s = it % NSK;
+    const uint32_t parity = (uint32_t)((it / NSK) & 1);
+    if constexpr (IP) work = stages + s * BUF;
     long long tx, l1;
     tile_coords(tile, ntile, a.L1, a.g0, tx, l1);
     const long long l0 = tx * Cfg::W + c;
     const bool active = l0 < a.L0;
-    if (TST && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
+    if (TST && !IP && threadIdx.x == 0) bulk_wait_read0();  // previous tile's TMA store has read `work`
     TmaIO<C, Cfg::W, OM, SPEC, N, DCT> io;
     io.tw3 = reinterpret_cast<const C*>(a.tw3);
     io.init(a.in, a.out, active ? l0 : 0, l1, a.scale);
     io.spectral(a, active ? l0 : 0, l1);
-    io.stage = stages + s * Cfg::STAGE_ELEMS;
+    io.stage = stages + s * BUF;
     io.obuf = work;
     io.c = c;
     // refill: the drained stage gets the tile NS steps ahead
     const int rs = s;
-    const long long next = tile + (long long)Cfg::NS * gridDim.x;
-    io.refill = next < total;
+    const long long next = tile + (long long)NSK * gridDim.x;
+    io.refill = !IP && next < total;  // (IP: the stage is the work tile; refilled after its store)
     io.tmap = &tmap;
     io.mbar = &bars[rs];
-    io.stage_ptr = stages + rs * Cfg::STAGE_ELEMS;
+    io.stage_ptr = stages + rs * BUF;
     {
       long long ntx, nl1;
       tile_coords(next, ntile, a.L1, a.g0, ntx, nl1);
@@ -1363,6 +1376,12 @@ fft_strided_tma_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_co
           }
         }
         bulk_commit();
+        if constexpr (IP) {
+          if (next < total) {  // the store has read the stage: the tile NSK steps ahead goes in
+            bulk_wait_read0();
+            issue(next, s);
+          }
+        }
       }
     }
   }

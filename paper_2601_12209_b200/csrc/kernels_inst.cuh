@@ -63,6 +63,10 @@ KernelInfo make_strided() {
     k.tma_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 0>;
     k.tma_st1_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1>;  // TMA stores
     k.tma_bk_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 2>;
+    if constexpr (TC::IP_PREFER) {  // in place in the stage, three stages in flight
+      k.tma_ip_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, false, 0, true>;
+      k.tma_ip_smem = TC::SMEM_IP;
+    }
     if constexpr (DIR < 0) k.tma_st_spec_fn = (const void*)&fft_strided_tma_kernel<Real, N, DIR, 1, true>;
     k.tma_threads = TC::THREADS;
     k.tma_w = TC::W;

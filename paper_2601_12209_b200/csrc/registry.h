@@ -29,6 +29,8 @@ struct KernelInfo {
   bool tma_st_only = false;              // the TMA variant exists only with TMA stores (R2R)
   int tma_threads = 0, tma_w = 0, tma_boxr = 0, tma_maxr = 16;  // tma_maxr: its radix schedule
   size_t tma_smem = 0;
+  const void* tma_ip_fn = nullptr;  // TMA stores, passes in place in the stage (one more stage in flight)
+  size_t tma_ip_smem = 0;
   bool generic = false;  // fft_generic_kernel: the radix schedule is passed at run time (PassArgs::gen)
   // contig c2c with radix-32 passes: the radix-16 variant (x-FFTs whose epilogue stores to peers)
   const void* r16_fn = nullptr;
