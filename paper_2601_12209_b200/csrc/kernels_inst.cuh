@@ -7,9 +7,14 @@ namespace dfft {
 namespace {
 template <typename Real, int N, int DIR, int MODE = 0>
 KernelInfo make_contig() {
-  using Cfg = ContigCfg<N, (int)sizeof(Real) * 2>;
+#ifndef DFFT_CONTIG_R32_ALLMODES
+#define DFFT_CONTIG_R32_ALLMODES 0
+#endif
+  // radix-32 passes for c2c lines only (MODE 0); the R2C / C2R / DCT / DST modes keep radix 16
+  constexpr bool R32 = MODE == 0 || DFFT_CONTIG_R32_ALLMODES;
+  using Cfg = ContigCfg<N, (int)sizeof(Real) * 2, R32>;
   KernelInfo k;
-  k.fn = (const void*)&fft_contig_kernel<Real, N, DIR, MODE>;
+  k.fn = (const void*)&fft_contig_kernel<Real, N, DIR, MODE, false, R32>;
   if constexpr (MODE == 0) k.fn_tb = (const void*)&fft_contig_kernel<Real, N, DIR, 0, true>;
   k.threads = Cfg::THREADS;
   k.per_cta = Cfg::LPC;
